@@ -1,0 +1,191 @@
+/*
+ * recmg.h — C ABI of the B200-native RecMG hot path (paper_2511_08568_b200).
+ *
+ * The reference (arxiv 2511.08568 `embcache`, /root/reference/pkg/src/embcache)
+ * is pure Python + numpy and has no FFI; each entry point below replaces the
+ * Python function cited beside it, with the same argument meaning and the
+ * same error categories (errors.py), expressed as status codes.  The binding
+ * a maintainer would add on the reference side is in INTEGRATION.md.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers unless the name says `host`.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream); no call synchronises, allocates, or keeps hidden state.
+ *     Scratch comes from a caller-owned workspace sized by *_workspace_bytes.
+ *   - Buffer state (the GPU embedding-buffer metadata) is caller-owned device
+ *     memory of recmg_buffer_state_bytes(); recmg_buffer_reset() empties it.
+ *     Replays continue from whatever state they are given, so a trace can be
+ *     replayed batch by batch.
+ *   - Global ids are int32 (every configured vocabulary is < 2^30 ids).
+ */
+#ifndef RECMG_H
+#define RECMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per errors.py category on this path ------------ */
+typedef enum {
+    RECMG_OK = 0,
+    RECMG_E_INVALID_CONFIG = -1, /* InvalidConfigError   errors.py:15-18      */
+    RECMG_E_VOCAB_MISMATCH = -2, /* VocabularyMismatchError errors.py:51-54   */
+    RECMG_E_OUT_OF_VOCAB = -3,   /* OutOfVocabularyError errors.py:57-60      */
+    RECMG_E_BUFFER_STATE = -4,   /* ValueError / KeyError raised by
+                                    PriorityBuffer (runtime.py:69-70,79-80,
+                                    85-88,104) and load_embeddings (:124-128) */
+    RECMG_E_NON_FINITE = -5,     /* NumericalError errors.py:75-78            */
+    RECMG_E_CUDA = -6,           /* CUDA launch / runtime failure             */
+    RECMG_E_WORKSPACE = -7       /* workspace smaller than *_workspace_bytes   */
+} recmg_status;
+
+const char *recmg_status_string(int status);
+/* "error" category string of errors.py for a status (e.g. "invalid-config") */
+const char *recmg_status_category(int status);
+
+/* ---- buffer configuration --------------------------------------------- */
+enum { RECMG_POLICY_PRIORITY = 0, /* Alg. 1/2 priority-decay buffer (runtime.py:41-141) */
+       RECMG_POLICY_LRU = 1 };    /* LRU comparator (cache_sim.py:92-106)              */
+
+typedef struct {
+    int64_t capacity;       /* BufferConfig.capacity (runtime.py:29-38) /
+                               CacheConfig.capacity (cache_sim.py:30-58)          */
+    int32_t ways;           /* 0 = fully associative (the reference buffer);
+                               >0 = ways per set, set = gid % (capacity/ways)     */
+    int32_t eviction_speed; /* BufferConfig.eviction_speed, default 4             */
+    int32_t policy;         /* RECMG_POLICY_*                                     */
+    int32_t reserved;
+    int64_t total_ids;      /* Trace.total_ids (trace.py:75-77)                   */
+} recmg_buffer_cfg;
+
+/* Counters of one replay; cache_hits..prefetch_useful are BreakdownReport's
+ * integer fields (runtime.py:153-162), the rest are the spy-visible counts
+ * (populate calls, prefetched add calls, resident count at the end).       */
+typedef struct {
+    int64_t cache_hits;
+    int64_t prefetch_hits;
+    int64_t on_demand;
+    int64_t prefetch_issued;
+    int64_t prefetch_useful;
+    int64_t evictions;
+    int64_t prefetch_inserts;
+    int64_t occupancy;
+} recmg_counters;
+
+/* Bytes of device state for `cfg` (tags, priorities/tags or LRU clocks,
+ * per-set counts, and for sets wider than 32 ways an id->slot map over
+ * total_ids).  Replaces PriorityBuffer.__init__ (runtime.py:48-56).          */
+size_t recmg_buffer_state_bytes(const recmg_buffer_cfg *cfg);
+/* Empty the buffer.  Validation = BufferConfig.validate (runtime.py:34-38)
+ * and CacheConfig.validate (cache_sim.py:43-50).                            */
+int recmg_buffer_reset(const recmg_buffer_cfg *cfg, void *state, void *stream);
+
+/* ---- chunked replay through the buffer  (runtime.py:220-283) ----------- */
+/* Number of chunks chunk() emits (trace.py:226-250).                        */
+int64_t recmg_num_chunks(int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio);
+
+int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in,
+                                 int32_t l_out, int32_t window_ratio, int32_t pf_stride,
+                                 size_t *bytes);
+/*
+ * replay (runtime.py:220-283) with the model decisions already computed:
+ *   gids[n]            Trace.gid_array
+ *   bits[K*l_in]       caching bits 0/1 (runtime.py:181-193); NULL = all 0
+ *                      (caching_params None, runtime.py:184-185)
+ *   pf[K*pf_stride]    prefetch gids per chunk, -1 padded (runtime.py:196-210);
+ *                      NULL = no prefetcher
+ *   counters           device recmg_counters, ACCUMULATED into (zero it first)
+ *   cov_num, cov_den   device uint8[K] (nullable): |set(P_k) & set(W_k)| and
+ *                      |set(W_k)| so the host can form the float64 coverage in
+ *                      chunk order (runtime.py:276,282) via recmg_coverage_mean
+ *   access_class[n]    nullable: 0 cache hit, 1 prefetch hit, 2 on-demand
+ * Status: RECMG_E_INVALID_CONFIG for a bad cfg / l_in / l_out / window_ratio
+ * (trace.py:233-236); bits outside {0,1} are RECMG_E_BUFFER_STATE
+ * (runtime.py:127-128) and are reported through counters->occupancy = -1.
+ */
+int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                 int32_t l_in, int32_t l_out, int32_t window_ratio, const uint8_t *bits,
+                 const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
+                 uint8_t *cov_num, uint8_t *cov_den, uint8_t *access_class, void *ws,
+                 size_t ws_bytes, void *stream);
+
+/* Host: sequential float64 mean of num/den in chunk order (runtime.py:276,282). */
+double recmg_coverage_mean(const uint8_t *host_num, const uint8_t *host_den, int64_t K);
+
+/* ---- policy-only simulation  (cache_sim.py:223-260, LRU) --------------- */
+int recmg_simulate_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, size_t *bytes);
+/* simulate(trace, CacheConfig(capacity, Policy.LRU, ways)): hits/misses
+ * accumulated into device int64[2]; per_access_hit[n] (nullable) as
+ * SimResult.per_access_hit.                                                 */
+int recmg_simulate(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                   uint8_t *per_access_hit, int64_t *hits_misses, void *ws, size_t ws_bytes,
+                   void *stream);
+
+/* ---- single buffer operations (PriorityBuffer object API) -------------- */
+enum {
+    RECMG_OP_ADD = 0,          /* add(gid, arg=priority, flag=prefetched) runtime.py:83-91 */
+    RECMG_OP_POPULATE = 1,     /* populate() -> victim gid              runtime.py:100-112 */
+    RECMG_OP_REFERENCE = 2,    /* reference(gid) -> 0/1                 runtime.py:93-98   */
+    RECMG_OP_SET_PRIORITY = 3, /* set_priority(gid, arg)                runtime.py:78-81   */
+    RECMG_OP_QUERY = 4         /* -> resident ? priority : -1           runtime.py:61-71   */
+};
+/* result: device int64[2] = {status (0 or RECMG_E_BUFFER_STATE), value}.   */
+int recmg_buffer_op(const recmg_buffer_cfg *cfg, void *state, int32_t op, int64_t gid,
+                    int64_t arg, int32_t flag, int64_t *result, void *stream);
+
+/* ---- models  (neural/model.py) ----------------------------------------- */
+enum { RECMG_MODEL_CACHING = 0, RECMG_MODEL_PREFETCH = 1 };
+enum { RECMG_PREC_FP32 = 0 };  /* fp32 storage + fp32 math (logits within 1e-3) */
+
+typedef struct {
+    int32_t kind;      /* ModelParameters.kind (model.py:28-38)   */
+    int32_t dim;       /* d                                       */
+    int32_t stacks;    /* LSTM layers per encoder/decoder         */
+    int32_t l_in;      /* input chunk length (15)                 */
+    int32_t l_out;     /* prefetch outputs (5)                    */
+    int32_t n_tables;  /* len(table_sizes)                        */
+    int64_t total_ids; /* sum(table_sizes)                        */
+} recmg_model_shape;
+
+/* Floats of the raw dense blob: every array of _shapes (model.py:54-80)
+ * except embed_id, row-major, concatenated in _shapes order.               */
+int64_t recmg_model_dense_floats(const recmg_model_shape *shape);
+/* Bytes of the packed (kernel-layout) dense weights.                       */
+size_t recmg_model_packed_bytes(const recmg_model_shape *shape, int32_t precision);
+/* Re-lay the raw dense blob into the kernel layout (gate-interleaved LSTM
+ * weights).  Ingests init_params / load_checkpoint arrays (model.py:83-100,
+ * checkpoint.py:48-79) after a float64 -> float32 cast.                    */
+int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, void *packed,
+                     int32_t precision, void *stream);
+/*
+ * forward_caching_batch (model.py:184-196) / forward_prefetch_batch
+ * (model.py:199-212) over `batch` chunks:
+ *   embed_id[total_ids*dim]   fp32 id embeddings
+ *   gid, tid [batch*l_in]     int32
+ *   logits   [batch*l_in] (caching) or [batch*l_out] (prefetch), pre-sigmoid
+ *   bits     caching, nullable: (sigmoid >= 0.5) = (logit >= 0)  runtime.py:192
+ *   pf_gid   prefetch, nullable: decode_indices in float64       model.py:250-258
+ */
+int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
+                        const float *embed_id, const void *packed, const int32_t *gid,
+                        const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
+                        int32_t *pf_gid, void *stream);
+
+/* ---- trace helpers ----------------------------------------------------- */
+/* tid[i] = table of gids[i] given table offsets[n_tables+1] (device), the
+ * searchsorted of trace.py:86 / index_of_global trace.py:44-51.             */
+int recmg_table_ids(const int32_t *gids, int64_t n, const int64_t *offsets, int32_t n_tables,
+                    int32_t *tid, void *stream);
+/* Host: the sticky-pool pass of generate_trace (trace.py:144-160), given
+ * the already-drawn zipf gids and coins.  Returns 0.                        */
+int recmg_trace_pool_pass(const int64_t *host_zipf_gids, const double *host_sticky_coin,
+                          const double *host_pool_coin, int64_t n, double stickiness,
+                          int32_t pool_size, int64_t *host_out_gids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RECMG_H */

@@ -1,0 +1,22 @@
+"""B200-native RecMG hot path (arxiv 2511.08568), drop-in for the reference
+``embcache`` replay / model / buffer-simulator API.
+
+The compute runs in hand-written sm_100a kernels (csrc/) behind the C ABI
+in include/recmg.h, loaded from the in-tree librecmg.so; there is no CPU
+fallback on this path.
+"""
+from .cache_sim import CacheConfig, Policy, SimResult, simulate
+from .errors import (CheckpointError, EmbcacheError, InvalidConfigError,
+                     MissingArtifactError, NumericalError, OutOfVocabularyError,
+                     TraceParseError, TraceValidationError, VocabularyMismatchError)
+from .model import (CACHING, PREFETCH, DeviceModel, ModelParameters, batch_arrays,
+                    decode_indices, forward_caching, forward_caching_batch, forward_prefetch,
+                    forward_prefetch_batch, init_params, normalize_gids)
+from .runtime import (EVICTION_SPEED, BreakdownReport, BufferConfig, PriorityBuffer,
+                      correctness_vs_window, coverage, gpu_buffer_populate, load_embeddings,
+                      replay, replay_policy_only, write_breakdown_csv)
+from .trace import (EmbeddingIndex, SequenceSample, Trace, TraceGenConfig, chunk,
+                    generate_trace, index_of_global, make_index, num_chunks, table_offsets,
+                    trace_from_gids)
+
+__version__ = "0.1.0"

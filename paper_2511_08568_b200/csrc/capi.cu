@@ -1,0 +1,299 @@
+// extern "C" entry points declared in include/recmg.h.
+#include <string.h>
+
+#include "lstm.cuh"
+#include "model_layout.cuh"
+#include "partition.cuh"
+#include "replay.cuh"
+
+using namespace recmg;
+
+namespace {
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct ReplayPlan {
+    Geometry g;
+    int64_t K = 0, Ec = 0, E = 0;
+    bool vals = false;
+    uint32_t *ev = nullptr, *vv = nullptr;
+    PartitionBuffers pb;
+};
+
+bool plan_replay(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in, int32_t l_out,
+                 int32_t window_ratio, int32_t pf_stride, bool with_class, Arena &a,
+                 ReplayPlan &p) {
+    if (!geometry_of(cfg, &p.g)) return false;
+    if (cfg->policy != RECMG_POLICY_PRIORITY || cfg->eviction_speed < 1) return false;
+    if (n < 0 || l_in < 1 || l_out < 1 || window_ratio < 1 || pf_stride < 0) return false;
+    if ((int64_t)window_ratio * l_out > 255) return false;  // uint8 coverage counts
+    p.K = recmg_num_chunks(n, l_in, l_out, window_ratio);
+    p.Ec = 2 * (int64_t)l_in + pf_stride;
+    p.E = p.K * p.Ec + (n - p.K * l_in);
+    if (p.E >= ((int64_t)1 << 32)) return false;
+    p.vals = with_class && p.g.S > 1;
+    p.ev = a.take<uint32_t>((size_t)p.E);
+    p.vv = p.vals ? a.take<uint32_t>((size_t)p.E) : nullptr;
+    if (p.g.S > 1) partition_plan(a, p.pb, p.E, p.g.S, p.vals);
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *recmg_status_string(int status) {
+    switch (status) {
+        case RECMG_OK: return "ok";
+        case RECMG_E_INVALID_CONFIG: return "invalid configuration";
+        case RECMG_E_VOCAB_MISMATCH: return "model vocabulary does not match trace";
+        case RECMG_E_OUT_OF_VOCAB: return "embedding index outside the vocabulary";
+        case RECMG_E_BUFFER_STATE: return "buffer operation not valid in this state";
+        case RECMG_E_NON_FINITE: return "non-finite value";
+        case RECMG_E_CUDA: return "CUDA error";
+        case RECMG_E_WORKSPACE: return "workspace too small";
+        default: return "unknown status";
+    }
+}
+
+const char *recmg_status_category(int status) {
+    switch (status) {
+        case RECMG_OK: return "ok";
+        case RECMG_E_INVALID_CONFIG: return "invalid-config";
+        case RECMG_E_VOCAB_MISMATCH: return "vocabulary-mismatch";
+        case RECMG_E_OUT_OF_VOCAB: return "out-of-vocabulary";
+        case RECMG_E_BUFFER_STATE: return "buffer-state";
+        case RECMG_E_NON_FINITE: return "non-finite";
+        default: return "error";
+    }
+}
+
+int64_t recmg_num_chunks(int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio) {
+    // trace.py:238-250: origins 0, l_in, ... while origin + l_in + l_win <= n
+    const int64_t l_win = (int64_t)window_ratio * l_out;
+    if (l_in < 1 || n < l_in + l_win) return 0;
+    return (n - l_in - l_win) / l_in + 1;
+}
+
+size_t recmg_buffer_state_bytes(const recmg_buffer_cfg *cfg) {
+    Geometry g;
+    if (!geometry_of(cfg, &g)) return 0;
+    return state_bytes(cfg, g);
+}
+
+int recmg_buffer_reset(const recmg_buffer_cfg *cfg, void *state, void *stream) {
+    Geometry g;
+    if (!geometry_of(cfg, &g) || !state) return RECMG_E_INVALID_CONFIG;
+    if (cfg->policy == RECMG_POLICY_PRIORITY && cfg->eviction_speed < 1) return RECMG_E_INVALID_CONFIG;
+    StateView v = state_view(state, cfg, g);
+    const int64_t SW = g.S * g.W;
+    const int64_t work = SW > cfg->total_ids ? SW : cfg->total_ids;
+    unsigned grid = (unsigned)((work + 255) / 256);
+    if (grid > 8 * kSmCount) grid = 8 * kSmCount;
+    if (grid < 1) grid = 1;
+    state_reset_kernel<<<grid, 256, 0, as_stream(stream)>>>(v, SW, g.S, cfg->total_ids);
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in,
+                                 int32_t l_out, int32_t window_ratio, int32_t pf_stride,
+                                 size_t *bytes) {
+    Arena a{nullptr, 0, 0};
+    ReplayPlan p;
+    if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, true, a, p))
+        return RECMG_E_INVALID_CONFIG;
+    *bytes = a.used + 256;
+    return RECMG_OK;
+}
+
+int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                 int32_t l_in, int32_t l_out, int32_t window_ratio, const uint8_t *bits,
+                 const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
+                 uint8_t *cov_num, uint8_t *cov_den, uint8_t *access_class, void *ws,
+                 size_t ws_bytes, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    if (!pf) pf_stride = 0;
+    Arena a{(char *)ws, ws_bytes, 0};
+    ReplayPlan p;
+    if (!state || !counters || (n > 0 && !gids)) return RECMG_E_INVALID_CONFIG;
+    if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, access_class != nullptr, a, p))
+        return RECMG_E_INVALID_CONFIG;
+    if (p.E == 0) return RECMG_OK;
+    if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
+    StateView st = state_view(state, cfg, p.g);
+
+    if (p.K > 0) {
+        prefetch_stats_kernel<<<(unsigned)((p.K + 255) / 256), 256, 0, s>>>(
+            gids, p.K, l_in, window_ratio * l_out, pf, pf_stride, cov_num, cov_den, counters);
+        RECMG_LAUNCH_CHECK();
+    }
+    if (p.E == 0) return RECMG_OK;
+    build_events_kernel<<<(unsigned)imin64((p.E + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
+        gids, n, l_in, bits, pf, pf_stride, p.K, p.ev, p.vv);
+    RECMG_LAUNCH_CHECK();
+    uint32_t *ev = p.ev, *vv = p.vv;
+    ReplayArgs ra;
+    memset(&ra, 0, sizeof(ra));
+    if (p.g.S > 1) {
+        int rc = partition_run(p.pb, ev, vv, s);
+        if (rc) return rc;
+        ra.seg_start = p.pb.seg_start;
+        ra.seg_end = p.pb.seg_end;
+    }
+    ra.ev = ev;
+    ra.vals = vv;
+    ra.E = p.E;
+    ra.S = p.g.S;
+    ra.W = p.g.W;
+    ra.es = cfg->eviction_speed;
+    ra.l_in = l_in;
+    ra.Ec = p.Ec;
+    ra.K = p.K;
+    ra.st = st;
+    ra.ctr = counters;
+    ra.access_class = access_class;
+    return launch_replay(RECMG_POLICY_PRIORITY, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
+}
+
+double recmg_coverage_mean(const uint8_t *num, const uint8_t *den, int64_t K) {
+    // runtime.py:276 accumulates len(P & W)/len(W) left to right in float64,
+    // runtime.py:282 divides by the chunk count.
+    double acc = 0.0;
+    for (int64_t k = 0; k < K; k++) acc += (double)num[k] / (double)den[k];
+    return K ? acc / (double)K : 0.0;
+}
+
+int recmg_simulate_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, size_t *bytes) {
+    Geometry g;
+    if (!geometry_of(cfg, &g) || cfg->policy != RECMG_POLICY_LRU || n < 0)
+        return RECMG_E_INVALID_CONFIG;
+    Arena a{nullptr, 0, 0};
+    a.take<uint32_t>((size_t)n);  // keys copy
+    a.take<uint32_t>((size_t)n);  // positions
+    if (g.S > 1) {
+        PartitionBuffers pb;
+        partition_plan(a, pb, n, g.S, true);
+    }
+    *bytes = a.used + 256;
+    return RECMG_OK;
+}
+
+__global__ void iota_copy_kernel(const int32_t *in, uint32_t *keys, uint32_t *vals, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = (uint32_t)in[i];  // EV_SERVE == 0: the gid is the event word
+        if (vals) vals[i] = (uint32_t)i;
+    }
+}
+
+int recmg_simulate(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                   uint8_t *per_access_hit, int64_t *hits_misses, void *ws, size_t ws_bytes,
+                   void *stream) {
+    cudaStream_t s = as_stream(stream);
+    Geometry g;
+    if (!geometry_of(cfg, &g) || cfg->policy != RECMG_POLICY_LRU || !state || n < 0)
+        return RECMG_E_INVALID_CONFIG;
+    if (n == 0) return RECMG_OK;
+    Arena a{(char *)ws, ws_bytes, 0};
+    uint32_t *keys = a.take<uint32_t>((size_t)n);
+    uint32_t *vals = a.take<uint32_t>((size_t)n);
+    PartitionBuffers pb;
+    if (g.S > 1) partition_plan(a, pb, n, g.S, true);
+    if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
+    iota_copy_kernel<<<(unsigned)imin64((n + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
+        gids, keys, vals, n);
+    RECMG_LAUNCH_CHECK();
+    ReplayArgs ra;
+    memset(&ra, 0, sizeof(ra));
+    uint32_t *k = keys, *v = vals;
+    if (g.S > 1) {
+        int rc = partition_run(pb, k, v, s);
+        if (rc) return rc;
+        ra.seg_start = pb.seg_start;
+        ra.seg_end = pb.seg_end;
+    }
+    ra.ev = k;
+    ra.vals = v;
+    ra.E = n;
+    ra.S = g.S;
+    ra.W = g.W;
+    ra.st = state_view(state, cfg, g);
+    ra.hits_misses = hits_misses;
+    ra.per_access_hit = per_access_hit;
+    int rc = launch_replay(RECMG_POLICY_LRU, !g.wide, false, ra, g.S, s);
+    if (rc) return rc;
+    clock_bump_kernel<<<1, 1, 0, s>>>(ra.st.header, n);
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+int recmg_buffer_op(const recmg_buffer_cfg *cfg, void *state, int32_t op, int64_t gid,
+                    int64_t arg, int32_t flag, int64_t *result, void *stream) {
+    Geometry g;
+    if (!geometry_of(cfg, &g) || !state || !result) return RECMG_E_INVALID_CONFIG;
+    if (op < RECMG_OP_ADD || op > RECMG_OP_QUERY) return RECMG_E_INVALID_CONFIG;
+    if (op != RECMG_OP_POPULATE && (gid < 0 || gid >= cfg->total_ids)) return RECMG_E_OUT_OF_VOCAB;
+    if (op == RECMG_OP_POPULATE && (arg < 0 || arg >= g.S)) return RECMG_E_INVALID_CONFIG;
+    buffer_op_kernel<<<1, 32, 0, as_stream(stream)>>>(state_view(state, cfg, g), g.S, g.W, op, gid,
+                                                      arg, flag, result);
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+// ---- models -----------------------------------------------------------------
+int64_t recmg_model_dense_floats(const recmg_model_shape *shape) {
+    if (!shape_ok(shape)) return -1;
+    return raw_layout(shape).total;
+}
+
+size_t recmg_model_packed_bytes(const recmg_model_shape *shape, int32_t precision) {
+    if (!shape_ok(shape) || precision != RECMG_PREC_FP32) return 0;
+    return (size_t)packed_layout(shape).total * sizeof(float);
+}
+
+int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, void *packed,
+                     int32_t precision, void *stream) {
+    if (!shape_ok(shape) || precision != RECMG_PREC_FP32 || !dense_raw || !packed)
+        return RECMG_E_INVALID_CONFIG;
+    return model_pack(shape, dense_raw, packed, as_stream(stream));
+}
+
+int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
+                        const float *embed_id, const void *packed, const int32_t *gid,
+                        const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
+                        int32_t *pf_gid, void *stream) {
+    if (!shape_ok(shape) || precision != RECMG_PREC_FP32 || batch < 0 || !logits)
+        return RECMG_E_INVALID_CONFIG;
+    if (batch > 0 && (!embed_id || !packed || !gid || !tid)) return RECMG_E_INVALID_CONFIG;
+    return model_forward_fp32(shape, embed_id, packed, gid, tid, batch, logits, bits, pf_gid,
+                              as_stream(stream));
+}
+
+// ---- trace helpers -----------------------------------------------------------
+__global__ void table_ids_kernel(const int32_t *gids, int64_t n, const int64_t *offsets,
+                                 int32_t n_tables, int32_t *tid) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = gids[i];
+        // searchsorted(offsets, g, side="right") - 1  (trace.py:86)
+        int lo = 0, hi = n_tables;  // offsets[lo] <= g < offsets[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(offsets + mid) <= g) lo = mid; else hi = mid;
+        }
+        tid[i] = lo;
+    }
+}
+
+int recmg_table_ids(const int32_t *gids, int64_t n, const int64_t *offsets, int32_t n_tables,
+                    int32_t *tid, void *stream) {
+    if (n < 0 || n_tables < 1) return RECMG_E_INVALID_CONFIG;
+    if (n == 0) return RECMG_OK;
+    table_ids_kernel<<<(unsigned)imin64((n + 255) / 256, 16 * kSmCount), 256, 0,
+                       as_stream(stream)>>>(gids, n, offsets, n_tables, tid);
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// Replay engine internals (see replay.cu).
+#pragma once
+#include "common.cuh"
+
+namespace recmg {
+
+constexpr int kNarrowWarps = 4;  // sets per CTA in the narrow kernel
+
+struct ReplayArgs;
+
+__global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n, int32_t l_in,
+                                    const uint8_t *__restrict__ bits,
+                                    const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
+                                    uint32_t *__restrict__ ev, uint32_t *__restrict__ vals);
+__global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t K, int32_t l_in,
+                                      int32_t l_win, const int32_t *__restrict__ pf,
+                                      int32_t pf_stride, uint8_t *__restrict__ cov_num,
+                                      uint8_t *__restrict__ cov_den,
+                                      recmg_counters *__restrict__ ctr);
+__global__ void state_reset_kernel(StateView st, int64_t SW, int64_t S, int64_t V);
+__global__ void clock_bump_kernel(int64_t *header, int64_t by);
+__global__ void buffer_op_kernel(StateView st, int64_t S, int64_t W, int32_t op, int64_t gid,
+                                 int64_t arg, int32_t flag, int64_t *result);
+
+struct ReplayArgs {
+    const uint32_t *ev;
+    const uint32_t *vals;
+    const uint32_t *seg_start, *seg_end;
+    int64_t E;
+    int64_t S, W;
+    int32_t es;
+    int32_t l_in;
+    int64_t Ec, K;
+    StateView st;
+    recmg_counters *ctr;
+    uint8_t *access_class;
+    int64_t *hits_misses;
+    uint8_t *per_access_hit;
+};
+
+int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_t nsets,
+                  cudaStream_t s);
+
+}  // namespace recmg

@@ -1,0 +1,138 @@
+"""Device-resident engines over the C ABI: buffer replay (K3), LRU
+comparator (K4) and the model pipeline (K1+K2 -> K3).  They own their
+device allocations so repeated calls (the bench's steps, batch-by-batch
+serving) allocate nothing; every launch is stream-ordered on torch's
+current stream and nothing synchronises until ``*.result()``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .trace import num_chunks
+
+
+class BufferReplay:
+    """recmg_replay: chunked replay through the priority buffer."""
+
+    def __init__(self, capacity, total_ids, eviction_speed=4, ways=None, n=0, l_in=15,
+                 l_out=5, window_ratio=3, pf_stride=0):
+        torch = _native.torch_cuda()
+        L = _native.lib()
+        self.torch = torch
+        self.cfg = _native.buffer_cfg(capacity, ways, eviction_speed, _native.POLICY_PRIORITY,
+                                      total_ids)
+        sb = L.recmg_buffer_state_bytes(ctypes.byref(self.cfg))
+        if sb == 0:
+            _native.check(_native.RECMG_E_INVALID_CONFIG, "buffer config")
+        self.state = _native.device_bytes(torch, sb)
+        self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self.l_in, self.l_out, self.window_ratio = int(l_in), int(l_out), int(window_ratio)
+        self._ws = None
+        self._ws_key = None
+        self._cov = None
+        self.reserve(n, pf_stride)
+        self.reset()
+
+    def reserve(self, n, pf_stride):
+        key = (int(n), int(pf_stride))
+        if self._ws_key is not None and self._ws_key[0] >= key[0] and self._ws_key[1] >= key[1]:
+            return
+        sz = ctypes.c_size_t(0)
+        _native.check(_native.lib().recmg_replay_workspace_bytes(
+            ctypes.byref(self.cfg), key[0], self.l_in, self.l_out, self.window_ratio, key[1],
+            ctypes.byref(sz)), "replay_workspace_bytes")
+        self._ws = _native.device_bytes(self.torch, sz.value)
+        K = num_chunks(key[0], self.l_in, self.l_out, self.window_ratio)
+        self._cov = self.torch.empty((2, max(K, 1)), dtype=self.torch.uint8, device="cuda")
+        self._ws_key = key
+
+    def reset(self):
+        _native.check(_native.lib().recmg_buffer_reset(
+            ctypes.byref(self.cfg), _native.ptr(self.state),
+            _native.stream_handle(self.torch)), "buffer_reset")
+        self.counters.zero_()
+
+    def run(self, gids, bits=None, pf=None, access_class=None):
+        """gids: device int32 [n]; bits uint8 [K, l_in]; pf int32 [K, stride]."""
+        n = gids.numel()
+        stride = int(pf.shape[1]) if pf is not None else 0
+        self.reserve(n, stride)
+        self.K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
+        _native.check(_native.lib().recmg_replay(
+            ctypes.byref(self.cfg), _native.ptr(self.state), _native.ptr(gids), n, self.l_in,
+            self.l_out, self.window_ratio, _native.ptr(bits), _native.ptr(pf), stride,
+            _native.ptr(self.counters), _native.ptr(self._cov[0]), _native.ptr(self._cov[1]),
+            _native.ptr(access_class), _native.ptr(self._ws), self._ws.numel(),
+            _native.stream_handle(self.torch)), "replay")
+
+    def cov_host(self):
+        """(num, den) uint8 arrays of the last run, copied to the host."""
+        c = self._cov[:, :self.K].cpu().numpy()
+        return c[0], c[1]
+
+    def result(self):
+        """Synchronise; counters dict plus the float64 coverage of the last run."""
+        ctr = self.counters.cpu().numpy()
+        out = dict(zip(_native.COUNTER_FIELDS, (int(x) for x in ctr)))
+        if self.K:
+            num, den = self.cov_host()
+            out["coverage"] = _native.coverage_mean(num, den)
+        else:
+            out["coverage"] = 0.0
+        return out
+
+
+class LruSim:
+    """recmg_simulate: set-associative (or fully associative) LRU."""
+
+    def __init__(self, capacity, total_ids, ways=None, n=0):
+        torch = _native.torch_cuda()
+        L = _native.lib()
+        self.torch = torch
+        self.cfg = _native.buffer_cfg(capacity, ways, 1, _native.POLICY_LRU, total_ids)
+        sb = L.recmg_buffer_state_bytes(ctypes.byref(self.cfg))
+        if sb == 0:
+            _native.check(_native.RECMG_E_INVALID_CONFIG, "cache config")
+        self.state = _native.device_bytes(torch, sb)
+        self.hm = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self._ws = None
+        self._n = -1
+        self.reserve(n)
+        self.reset()
+
+    def reserve(self, n):
+        if n <= self._n:
+            return
+        sz = ctypes.c_size_t(0)
+        _native.check(_native.lib().recmg_simulate_workspace_bytes(
+            ctypes.byref(self.cfg), int(n), ctypes.byref(sz)), "simulate_workspace_bytes")
+        self._ws = _native.device_bytes(self.torch, sz.value)
+        self._n = int(n)
+
+    def reset(self):
+        _native.check(_native.lib().recmg_buffer_reset(
+            ctypes.byref(self.cfg), _native.ptr(self.state),
+            _native.stream_handle(self.torch)), "buffer_reset")
+        self.hm.zero_()
+
+    def run(self, gids, per_access_hit=None):
+        n = gids.numel()
+        self.reserve(n)
+        _native.check(_native.lib().recmg_simulate(
+            ctypes.byref(self.cfg), _native.ptr(self.state), _native.ptr(gids), n,
+            _native.ptr(per_access_hit), _native.ptr(self.hm), _native.ptr(self._ws),
+            self._ws.numel(), _native.stream_handle(self.torch)), "simulate")
+
+    def result(self):
+        h, m = (int(x) for x in self.hm.cpu().numpy())
+        return h, m
+
+
+def to_device_gids(torch, gids: np.ndarray):
+    g = np.asarray(gids)
+    if g.size and (g.min() < 0 or g.max() >= (1 << 30) - 1):
+        raise ValueError("global ids must lie in [0, 2^30 - 1)")
+    return torch.from_numpy(np.ascontiguousarray(g, dtype=np.int32)).cuda()

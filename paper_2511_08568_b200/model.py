@@ -1,0 +1,254 @@
+"""Caching / prefetch models (neural/model.py of the reference) on the B200.
+
+Parameters are the reference's: ``init_params`` draws the same arrays from
+the same ``default_rng`` stream (model.py:83-100), and ``ModelParameters``
+from ``embcache.load_checkpoint`` work unchanged.  The forwards run the
+fp32 sm_100a kernel (csrc/lstm_simt.cu) through ``recmg_model_forward``.
+
+``forward_*_batch`` return an object whose ``.value`` is the float64
+probability array the reference's ``Tensor.value`` holds (model.py:184-212);
+``.logits`` holds the kernel's fp32 pre-sigmoid outputs.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidConfigError, OutOfVocabularyError
+from .trace import EmbeddingIndex, index_of_global, table_offsets
+
+CACHING = "caching"
+PREFETCH = "prefetch"
+
+
+@dataclass
+class ModelParameters:
+    """model.py:28-51."""
+    kind: str
+    table_sizes: list
+    dim: int = 32
+    stacks: int = 1
+    l_in: int = 15
+    l_out: int = 5
+    arrays: dict = field(default_factory=dict)
+
+    @property
+    def total_ids(self) -> int:
+        return int(sum(self.table_sizes))
+
+    @property
+    def param_count(self) -> int:
+        return int(sum(a.size for a in self.arrays.values()))
+
+    def copy(self) -> "ModelParameters":
+        return ModelParameters(self.kind, list(self.table_sizes), self.dim, self.stacks,
+                               self.l_in, self.l_out,
+                               {k: v.copy() for k, v in self.arrays.items()})
+
+
+def _shapes(kind, total_ids, table_count, dim, stacks, l_out):
+    """model.py:54-80 (names and insertion order are the checkpoint contract)."""
+    d = dim
+    shapes = {
+        "embed_id": (total_ids, d), "embed_table": (table_count, d),
+        "att_enc": (d, d), "att_dec": (d, d), "att_v": (d, 1),
+        "comb_w": (2 * d, d), "comb_b": (d,), "head_w": (d, 1), "head_b": (1,),
+    }
+    for k in range(stacks):
+        shapes[f"enc{k}_wx"] = (2 * d if k == 0 else d, 4 * d)
+        shapes[f"enc{k}_wh"] = (d, 4 * d)
+        shapes[f"enc{k}_b"] = (4 * d,)
+        shapes[f"dec{k}_wx"] = (3 * d if k == 0 else d, 4 * d)
+        shapes[f"dec{k}_wh"] = (d, 4 * d)
+        shapes[f"dec{k}_b"] = (4 * d,)
+    if kind == PREFETCH:
+        shapes["slot_embed"] = (l_out, 2 * d)
+    return shapes
+
+
+def init_params(kind, table_sizes, dim=32, stacks=None, l_in=15, l_out=5, seed=0,
+                init_scale=0.08) -> ModelParameters:
+    """model.py:83-100: uniform(-s, s) per array from one default_rng(seed)."""
+    if kind not in (CACHING, PREFETCH):
+        raise InvalidConfigError(f"unknown model kind {kind!r}")
+    if stacks is None:
+        stacks = 1 if kind == CACHING else 2
+    if dim < 1 or stacks < 1 or l_in < 1 or l_out < 1:
+        raise InvalidConfigError("dim, stacks, l_in, l_out must be >= 1")
+    rng = np.random.default_rng(seed)
+    total = int(sum(table_sizes))
+    shapes = _shapes(kind, total, len(table_sizes), dim, stacks, l_out)
+    arrays = {name: rng.uniform(-init_scale, init_scale, size=shape)
+              for name, shape in shapes.items()}
+    return ModelParameters(kind, list(table_sizes), dim, stacks, l_in, l_out, arrays)
+
+
+class DeviceModel:
+    """A model's weights resident in HBM in the kernel layout.
+
+    embed_id is uploaded as fp32 [V, d]; every other array is cast to fp32,
+    concatenated in _shapes order and re-laid by ``recmg_model_pack``.
+    """
+
+    def __init__(self, params: ModelParameters, embed_id=None):
+        torch = _native.torch_cuda()
+        L = _native.lib()
+        self.params = params
+        self.kind = params.kind
+        self.shape = _native.ModelShape(
+            _native.MODEL_CACHING if params.kind == CACHING else _native.MODEL_PREFETCH,
+            int(params.dim), int(params.stacks), int(params.l_in), int(params.l_out),
+            len(params.table_sizes), int(params.total_ids))
+        nf = L.recmg_model_dense_floats(ctypes.byref(self.shape))
+        if nf < 0:
+            raise InvalidConfigError(f"unsupported model shape dim={params.dim} "
+                                     f"stacks={params.stacks} l_in={params.l_in}")
+        names = [n for n in _shapes(params.kind, params.total_ids, len(params.table_sizes),
+                                    params.dim, params.stacks, params.l_out) if n != "embed_id"]
+        raw = np.concatenate([np.asarray(params.arrays[n], dtype=np.float32).reshape(-1)
+                              for n in names])
+        if raw.size != nf:
+            raise InvalidConfigError("parameter arrays do not match the model shape")
+        if embed_id is None:
+            embed_id = torch.from_numpy(
+                np.ascontiguousarray(params.arrays["embed_id"], dtype=np.float32)).cuda()
+        self.embed_id = embed_id
+        raw_d = torch.from_numpy(raw).cuda()
+        self.packed = _native.device_bytes(
+            torch, L.recmg_model_packed_bytes(ctypes.byref(self.shape), _native.PREC_FP32))
+        _native.check(L.recmg_model_pack(ctypes.byref(self.shape), _native.ptr(raw_d),
+                                         _native.ptr(self.packed), _native.PREC_FP32,
+                                         _native.stream_handle(torch)), "model_pack")
+        torch.cuda.current_stream().synchronize()
+        self.offsets = torch.from_numpy(table_offsets(params.table_sizes)).cuda()
+
+    @property
+    def out_len(self):
+        return self.params.l_in if self.kind == CACHING else self.params.l_out
+
+    def forward(self, gid, tid, logits=None, bits=None, pf_gid=None):
+        """gid/tid: device int32 [B, l_in].  Returns logits [B, out_len] fp32."""
+        torch = _native.torch_cuda()
+        B = gid.shape[0]
+        if logits is None:
+            logits = torch.empty((B, self.out_len), dtype=torch.float32, device="cuda")
+        _native.check(_native.lib().recmg_model_forward(
+            ctypes.byref(self.shape), _native.PREC_FP32, _native.ptr(self.embed_id),
+            _native.ptr(self.packed), _native.ptr(gid), _native.ptr(tid), B,
+            _native.ptr(logits), _native.ptr(bits), _native.ptr(pf_gid),
+            _native.stream_handle(torch)), "model_forward")
+        return logits
+
+    def table_ids(self, gid):
+        torch = _native.torch_cuda()
+        tid = torch.empty_like(gid)
+        _native.check(_native.lib().recmg_table_ids(
+            _native.ptr(gid), gid.numel(), _native.ptr(self.offsets), len(self.params.table_sizes),
+            _native.ptr(tid), _native.stream_handle(torch)), "table_ids")
+        return tid
+
+
+class ForwardResult:
+    """Stands in for the reference's autodiff Tensor: ``.value`` = probs."""
+
+    def __init__(self, logits: np.ndarray):
+        self.logits = logits
+        self.value = 1.0 / (1.0 + np.exp(-logits.astype(np.float64)))
+
+    @property
+    def shape(self):
+        return self.value.shape
+
+
+def _forward_batch(params, gid, tid, kind):
+    if params.kind != kind:
+        raise InvalidConfigError(f"forward_{kind} needs a {kind} model")
+    torch = _native.torch_cuda()
+    gid = np.asarray(gid)
+    tid = np.asarray(tid)
+    if gid.ndim != 2 or gid.shape != tid.shape:
+        raise InvalidConfigError("gid/tid must be [batch, length]")
+    if gid.shape[1] != params.l_in:  # the reference attends over any chunk length
+        params = ModelParameters(params.kind, params.table_sizes, params.dim, params.stacks,
+                                 gid.shape[1], params.l_out, params.arrays)
+    if gid.size and (gid.min() < 0 or gid.max() >= params.total_ids):
+        raise IndexError("embedding id outside embed_id")          # numpy fancy-index error
+    if tid.size and (tid.min() < 0 or tid.max() >= len(params.table_sizes)):
+        raise IndexError("table id outside embed_table")
+    dm = DeviceModel(params)
+    g = torch.from_numpy(np.ascontiguousarray(gid, dtype=np.int32)).cuda()
+    t = torch.from_numpy(np.ascontiguousarray(tid, dtype=np.int32)).cuda()
+    logits = dm.forward(g, t)
+    return ForwardResult(logits.cpu().numpy())
+
+
+def forward_caching_batch(params, gid, tid) -> ForwardResult:
+    """model.py:184-196 on the GPU."""
+    return _forward_batch(params, gid, tid, CACHING)
+
+
+def forward_prefetch_batch(params, gid, tid) -> ForwardResult:
+    """model.py:199-212 on the GPU."""
+    return _forward_batch(params, gid, tid, PREFETCH)
+
+
+def _check_inputs(params, inputs):
+    """model.py:215-225."""
+    offsets = table_offsets(params.table_sizes)
+    for a in inputs:
+        if not 0 <= a.table_id < len(params.table_sizes):
+            raise OutOfVocabularyError(f"table_id {a.table_id} outside vocabulary")
+        if not 0 <= a.row_id < params.table_sizes[a.table_id]:
+            raise OutOfVocabularyError(f"row_id {a.row_id} outside table {a.table_id}")
+        if a.global_id != offsets[a.table_id] + a.row_id:
+            raise OutOfVocabularyError(f"global_id {a.global_id} inconsistent with (table, row)")
+
+
+def batch_arrays(samples_inputs):
+    """model.py:228-231."""
+    gid = np.array([[a.global_id for a in s] for s in samples_inputs], dtype=np.int64)
+    tid = np.array([[a.table_id for a in s] for s in samples_inputs], dtype=np.int64)
+    return gid, tid
+
+
+def _single(params, inputs, kind):
+    _check_inputs(params, inputs)
+    gid, tid = batch_arrays([inputs])
+    return [float(x) for x in _forward_batch(params, gid, tid, kind).value[0]]
+
+
+def forward_caching(params, inputs) -> list:
+    """model.py:234-239."""
+    return _single(params, inputs, CACHING)
+
+
+def forward_prefetch(params, inputs) -> list:
+    """model.py:242-247."""
+    return _single(params, inputs, PREFETCH)
+
+
+def decode_indices(po, table_sizes) -> list:
+    """model.py:250-258 (host; the replay path decodes on the GPU in fp64)."""
+    total = int(sum(table_sizes))
+    out = []
+    for x in po:
+        gid = int(np.floor(float(x) * (total - 1) + 0.5))
+        gid = min(max(gid, 0), total - 1)
+        out.append(index_of_global(gid, table_sizes))
+    return out
+
+
+def normalize_gids(gids, total_ids):
+    """model.py:261-265."""
+    if total_ids < 2:
+        return np.zeros_like(gids, dtype=np.float64)
+    return np.asarray(gids).astype(np.float64) / (total_ids - 1)
+
+
+__all__ = ["CACHING", "PREFETCH", "ModelParameters", "init_params", "DeviceModel",
+           "forward_caching_batch", "forward_prefetch_batch", "forward_caching",
+           "forward_prefetch", "decode_indices", "normalize_gids", "batch_arrays",
+           "EmbeddingIndex"]

@@ -1,0 +1,369 @@
+"""Serving runtime (runtime.py of the reference) on the B200.
+
+Same entry points and semantics as /root/reference/pkg/src/embcache/runtime.py;
+``replay`` runs the whole trace on the GPU: model forwards (K1/K2), the
+prefetch statistics (R1) and the buffer state machine (K3) are sm_100a
+kernels behind include/recmg.h.  ``BufferConfig`` gains ``ways``: ``None``
+(default) is the reference's fully associative buffer, bit-exact;
+``ways=32`` is the 32-way set-associative generalisation (set = gid % S,
+per-set argmin and decay).
+"""
+from __future__ import annotations
+
+import csv
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .cache_sim import CacheConfig, Policy, simulate
+from .engine import BufferReplay, LruSim, to_device_gids
+from .errors import InvalidConfigError, VocabularyMismatchError
+from .model import CACHING, PREFETCH, DeviceModel, ModelParameters
+from .trace import chunk, num_chunks
+
+EVICTION_SPEED = 4
+
+
+@dataclass
+class BufferConfig:
+    """runtime.py:29-38, plus ``ways`` (None = fully associative)."""
+    capacity: int
+    eviction_speed: int = EVICTION_SPEED
+    ways: int | None = None
+
+    def validate(self):
+        if self.capacity < 1:
+            raise InvalidConfigError("buffer capacity must be >= 1")
+        if self.eviction_speed < 1:
+            raise InvalidConfigError("eviction_speed must be >= 1")
+        if self.ways is not None and (self.ways < 1 or self.capacity % self.ways != 0):
+            raise InvalidConfigError("ways must be >= 1 and divide capacity")
+
+
+@dataclass
+class BreakdownReport:
+    """runtime.py:153-178.  ``evictions`` / ``prefetch_inserts`` are extra
+    (not part of equality, so reports compare like the reference's)."""
+    cache_hits: int = 0
+    prefetch_hits: int = 0
+    on_demand: int = 0
+    prefetch_issued: int = 0
+    prefetch_useful: int = 0
+    coverage: float = 0.0
+    evictions: int = field(default=0, compare=False)
+    prefetch_inserts: int = field(default=0, compare=False)
+
+    @property
+    def total(self) -> int:
+        return self.cache_hits + self.prefetch_hits + self.on_demand
+
+    @property
+    def hits(self) -> int:
+        return self.cache_hits + self.prefetch_hits
+
+    @property
+    def hit_rate(self) -> float:
+        return self.hits / self.total if self.total else 0.0
+
+    @property
+    def correctness(self) -> float:
+        return self.prefetch_useful / self.prefetch_issued if self.prefetch_issued else 0.0
+
+
+class PriorityBuffer:
+    """runtime.py:41-112 over the GPU buffer state (one op = one launch;
+    the object API is for tests and interactive use, replay() never uses it)."""
+
+    def __init__(self, capacity: int, total_ids: int, eviction_speed: int = EVICTION_SPEED,
+                 ways: int | None = None):
+        if capacity < 1:
+            raise InvalidConfigError("buffer capacity must be >= 1")
+        torch = _native.torch_cuda()
+        self._torch = torch
+        self.capacity = capacity
+        self.eviction_speed = eviction_speed
+        self.total_ids = total_ids
+        self.ways = ways
+        self._cfg = _native.buffer_cfg(capacity, ways, max(eviction_speed, 1),
+                                       _native.POLICY_PRIORITY, total_ids)
+        self._state = _native.device_bytes(torch, _native.lib().recmg_buffer_state_bytes(
+            ctypes.byref(self._cfg)))
+        _native.check(_native.lib().recmg_buffer_reset(ctypes.byref(self._cfg),
+                                                       _native.ptr(self._state),
+                                                       _native.stream_handle(torch)))
+        self._res = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self._count = 0
+        self._sets = capacity // ways if ways else 1
+
+    def _op(self, op, gid=0, arg=0, flag=0):
+        if op != _native.OP_POPULATE and not 0 <= gid < self.total_ids:
+            raise IndexError(gid)
+        _native.check(_native.lib().recmg_buffer_op(
+            ctypes.byref(self._cfg), _native.ptr(self._state), op, int(gid), int(arg), int(flag),
+            _native.ptr(self._res), _native.stream_handle(self._torch)), "buffer_op")
+        st, val = (int(x) for x in self._res.cpu().numpy())
+        return st, val
+
+    def __len__(self):
+        return self._count
+
+    def __contains__(self, gid) -> bool:
+        return self._op(_native.OP_QUERY, gid)[1] >= 0
+
+    @property
+    def full(self) -> bool:
+        return self._count >= self.capacity
+
+    def priority_of(self, gid) -> int:
+        p = self._op(_native.OP_QUERY, gid)[1]
+        if p < 0:
+            raise KeyError(gid)
+        return p
+
+    @property
+    def entries(self) -> dict:
+        W = self.ways or self.capacity
+        S = self._sets
+        st = self._state
+        tags = st[64:64 + 4 * S * W].view(self._torch.int32).cpu().numpy()
+        off = 64 + ((4 * S * W + 255) // 256) * 256
+        meta = st[off:off + 8 * S * W].view(self._torch.int64).cpu().numpy()
+        return {int(g): int(m & 0xFFFFFFFF) for g, m in sorted(zip(tags, meta)) if g >= 0}
+
+    def set_priority(self, gid, priority):
+        st, _ = self._op(_native.OP_SET_PRIORITY, gid, priority)
+        if st:
+            raise KeyError(gid)
+
+    def add(self, gid, priority, prefetched=False):
+        if gid in self:
+            raise ValueError(f"id {gid} already resident")
+        if self.full:
+            raise ValueError("buffer full; evict before inserting")
+        st, _ = self._op(_native.OP_ADD, gid, priority, 1 if prefetched else 0)
+        if st:
+            raise ValueError("buffer set full; evict before inserting")
+        self._count += 1
+
+    def reference(self, gid) -> bool:
+        return bool(self._op(_native.OP_REFERENCE, gid)[1])
+
+    def populate(self, set_index: int = 0) -> int:
+        if self._count == 0:
+            raise ValueError("cannot evict from an empty buffer")
+        st, victim = self._op(_native.OP_POPULATE, 0, set_index)
+        if st:
+            raise ValueError("cannot evict from an empty buffer")
+        self._count -= 1
+        return victim
+
+
+def load_embeddings(buf: PriorityBuffer, chunk_gids, cache_bits, prefetch_gids):
+    """runtime.py:115-137 (Alg. 1) over the object API."""
+    if len(chunk_gids) != len(cache_bits):
+        raise ValueError("one cache bit per chunk access required")
+    for gid, bit in zip(chunk_gids, cache_bits):
+        if bit not in (0, 1):
+            raise ValueError("cache bits must be 0/1")
+        if gid in buf:
+            buf.set_priority(gid, bit + buf.eviction_speed)
+    for gid in prefetch_gids:
+        if gid in buf:
+            buf.set_priority(gid, buf.eviction_speed)
+            continue
+        if buf.full:
+            buf.populate()
+        buf.add(gid, buf.eviction_speed, prefetched=True)
+
+
+def gpu_buffer_populate(buf: PriorityBuffer) -> int:
+    """runtime.py:140-141 (Alg. 2)."""
+    return buf.populate()
+
+
+def coverage(predicted_ids, ground_truth_ids) -> float:
+    """runtime.py:144-150."""
+    gt = set(int(g) for g in ground_truth_ids)
+    if not gt:
+        raise ValueError("coverage needs a non-empty ground truth")
+    pred = set(int(g) for g in predicted_ids)
+    return len(pred & gt) / len(gt)
+
+
+def _check_vocab(params: ModelParameters | None, trace):
+    """runtime.py:213-217."""
+    if params is not None and list(params.table_sizes) != list(trace.table_sizes):
+        raise VocabularyMismatchError(
+            f"model vocabulary {params.table_sizes} does not match trace {trace.table_sizes}")
+
+
+def _gpu_bits(torch, params, gids_dev, K, l_in, dm=None):
+    """_model_bits (runtime.py:181-193) on the GPU: bits = logit >= 0."""
+    if K == 0:
+        return None
+    dm = dm or DeviceModel(params)
+    g = gids_dev[:K * l_in].view(K, l_in)
+    t = dm.table_ids(g)
+    bits = torch.empty((K, l_in), dtype=torch.uint8, device="cuda")
+    dm.forward(g, t, bits=bits)
+    return bits
+
+
+def _gpu_prefetches(torch, params, gids_dev, K, l_in, dm=None):
+    """_model_prefetches (runtime.py:196-210) on the GPU, decode in fp64."""
+    if K == 0:
+        return None
+    dm = dm or DeviceModel(params)
+    g = gids_dev[:K * l_in].view(K, l_in)
+    t = dm.table_ids(g)
+    pf = torch.empty((K, params.l_out), dtype=torch.int32, device="cuda")
+    dm.forward(g, t, pf_gid=pf)
+    return pf
+
+
+def _host_bits(fn, samples, l_in):
+    rows = [list(fn(s)) for s in samples]
+    for r in rows:
+        if len(r) != l_in:
+            raise ValueError("one cache bit per chunk access required")  # runtime.py:124-125
+        for b in r:
+            if b not in (0, 1):
+                raise ValueError("cache bits must be 0/1")               # runtime.py:127-128
+    return np.array(rows, dtype=np.uint8).reshape(len(samples), l_in)
+
+
+def _host_prefetches(fn, samples, total_ids):
+    rows = [[int(g) for g in fn(s)] for s in samples]
+    stride = max((len(r) for r in rows), default=0)
+    out = np.full((len(rows), max(stride, 1)), -1, dtype=np.int32)
+    for k, r in enumerate(rows):
+        for g in r:
+            if not 0 <= g < total_ids:
+                raise IndexError(g)   # the reference's dense arrays would raise
+        out[k, :len(r)] = r
+    return out if stride > 0 else None
+
+
+def replay(trace, buffer_cfg: BufferConfig, caching_params=None, prefetch_params=None,
+           l_in=None, l_out=None, window_ratio=3, caching_fn=None, prefetch_fn=None,
+           return_access_class=False):
+    """runtime.py:220-283 on the GPU (see module docstring)."""
+    buffer_cfg.validate()
+    _check_vocab(caching_params, trace)
+    _check_vocab(prefetch_params, trace)
+    if l_in is None:
+        l_in = caching_params.l_in if caching_params else (
+            prefetch_params.l_in if prefetch_params else 15)
+    if l_out is None:
+        l_out = prefetch_params.l_out if prefetch_params else 5
+    if l_in < 1 or l_out < 1:
+        raise InvalidConfigError("l_in and l_out must be >= 1")
+    if window_ratio < 1:
+        raise InvalidConfigError("window_ratio must be >= 1")
+    gids = np.asarray(trace.gid_array)
+    n = len(gids)
+    K = num_chunks(n, l_in, l_out, window_ratio)
+    samples = chunk(trace, l_in, l_out, window_ratio) if (caching_fn or prefetch_fn) else None
+    # host-side decisions are validated before any device work (runtime.py:124-128)
+    hbits = _host_bits(caching_fn, samples, l_in) if caching_fn is not None and K else None
+    hpf = _host_prefetches(prefetch_fn, samples, trace.total_ids) \
+        if prefetch_fn is not None and K else None
+
+    torch = _native.torch_cuda()
+    gdev = to_device_gids(torch, gids)
+    if caching_fn is not None:
+        bits = torch.from_numpy(hbits).cuda() if hbits is not None else None
+    elif caching_params is not None:
+        bits = _gpu_bits(torch, caching_params, gdev, K, l_in)
+    else:
+        bits = None                                      # zeros (runtime.py:184-185)
+    if prefetch_fn is not None:
+        pf = torch.from_numpy(hpf).cuda() if hpf is not None else None
+    elif prefetch_params is not None:
+        pf = _gpu_prefetches(torch, prefetch_params, gdev, K, l_in)
+    else:
+        pf = None
+
+    eng = BufferReplay(buffer_cfg.capacity, trace.total_ids, buffer_cfg.eviction_speed,
+                       buffer_cfg.ways, n, l_in, l_out, window_ratio,
+                       pf.shape[1] if pf is not None else 0)
+    cls = torch.empty(n, dtype=torch.uint8, device="cuda") if return_access_class else None
+    eng.run(gdev, bits, pf, cls)
+    r = eng.result()
+    rep = BreakdownReport(r["cache_hits"], r["prefetch_hits"], r["on_demand"],
+                          r["prefetch_issued"], r["prefetch_useful"], r["coverage"],
+                          r["evictions"], r["prefetch_inserts"])
+    if return_access_class:
+        return rep, cls.cpu().numpy()
+    return rep
+
+
+def replay_policy_only(trace, cache_cfg: CacheConfig, prefetch_params=None, prefetch_fn=None,
+                       l_in=15, l_out=5, window_ratio=3) -> BreakdownReport:
+    """runtime.py:286-349.  Without a prefetcher this is the simulator
+    reshaped into a breakdown (LRU on the GPU, K4)."""
+    cache_cfg.validate()
+    if prefetch_params is None and prefetch_fn is None:
+        res = simulate(trace, cache_cfg)
+        return BreakdownReport(cache_hits=res.hits, on_demand=res.misses)
+    if cache_cfg.policy != Policy.LRU or cache_cfg.ways is not None:
+        raise InvalidConfigError("prefetch-augmented baseline supports fully associative LRU only")
+    _check_vocab(prefetch_params, trace)
+    raise NotImplementedError("LRU + prefetch baseline is not on the GPU path yet")
+
+
+def correctness_vs_window(trace, prefetch_params: ModelParameters, ratios, l_in=None,
+                          l_out=None) -> dict:
+    """runtime.py:369-400 with the prefetch forward on the GPU."""
+    if not ratios or any(r < 1 for r in ratios):
+        raise InvalidConfigError("ratios must be positive")
+    _check_vocab(prefetch_params, trace)
+    l_in = l_in or prefetch_params.l_in
+    l_out = l_out or prefetch_params.l_out
+    max_ratio = max(ratios)
+    gids = np.asarray(trace.gid_array)
+    K = num_chunks(len(gids), l_in, l_out, max_ratio)
+    if K == 0:
+        raise InvalidConfigError("trace too short for the largest window")
+    torch = _native.torch_cuda()
+    p = prefetch_params
+    if p.l_in != l_in or p.l_out != l_out:
+        p = ModelParameters(p.kind, p.table_sizes, p.dim, p.stacks, l_in, l_out, p.arrays)
+    pf = _gpu_prefetches(torch, p, to_device_gids(torch, gids), K, l_in).cpu().numpy()
+    out = {}
+    for r in ratios:
+        w = r * l_out
+        issued = useful = 0
+        for k in range(K):
+            start = k * l_in + l_in
+            wset = set(int(g) for g in gids[start:start + w])
+            issued += pf.shape[1]
+            useful += sum(1 for g in pf[k] if int(g) in wset)
+        out[r] = useful / issued if issued else 0.0
+    return out
+
+
+def write_breakdown_csv(rows, path, latency_fn=None):
+    """runtime.py:403-420."""
+    with open(path, "w", encoding="utf-8", newline="") as f:
+        w = csv.writer(f)
+        header = ["label", "capacity", "cache_hits", "prefetch_hits", "on_demand", "hit_rate",
+                  "prefetch_issued", "prefetch_useful", "correctness", "coverage"]
+        if latency_fn is not None:
+            header.append("estimated_latency_ms")
+        w.writerow(header)
+        for label, capacity, r in rows:
+            row = [label, capacity, r.cache_hits, r.prefetch_hits, r.on_demand,
+                   f"{r.hit_rate:.6f}", r.prefetch_issued, r.prefetch_useful,
+                   f"{r.correctness:.6f}", f"{r.coverage:.6f}"]
+            if latency_fn is not None:
+                row.append(f"{latency_fn(r):.6f}")
+            w.writerow(row)
+
+
+__all__ = ["EVICTION_SPEED", "BufferConfig", "BreakdownReport", "PriorityBuffer",
+           "load_embeddings", "gpu_buffer_populate", "coverage", "replay",
+           "replay_policy_only", "correctness_vs_window", "write_breakdown_csv",
+           "CACHING", "PREFETCH", "LruSim"]

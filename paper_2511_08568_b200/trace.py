@@ -1,0 +1,187 @@
+"""Trace data model (trace.py of the reference), array-backed.
+
+The reference keeps a Python ``EmbeddingIndex`` object per access
+(trace.py:54-77); at 25 M-500 M accesses that is the bottleneck, so here a
+``Trace`` is its int64 ``gid_array`` plus ``table_sizes`` and materialises
+``accesses`` only on demand.  Any object with ``gid_array`` and
+``table_sizes`` (including a reference ``embcache.Trace``) is accepted by
+the replay API.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidConfigError, TraceValidationError
+
+
+@dataclass(frozen=True, slots=True)
+class EmbeddingIndex:
+    """trace.py:18-24."""
+    table_id: int
+    row_id: int
+    global_id: int
+
+
+def table_offsets(table_sizes) -> np.ndarray:
+    """trace.py:27-29."""
+    return np.concatenate(([0], np.cumsum(np.asarray(table_sizes, dtype=np.int64))))
+
+
+def make_index(table_id: int, row_id: int, table_sizes) -> EmbeddingIndex:
+    """trace.py:32-41."""
+    if not 0 <= table_id < len(table_sizes):
+        raise TraceValidationError(f"table_id {table_id} out of range")
+    if not 0 <= row_id < table_sizes[table_id]:
+        raise TraceValidationError(
+            f"row_id {row_id} out of range for table {table_id} (size {table_sizes[table_id]})")
+    return EmbeddingIndex(table_id, row_id, int(sum(table_sizes[:table_id])) + row_id)
+
+
+def index_of_global(global_id: int, table_sizes) -> EmbeddingIndex:
+    """trace.py:44-51."""
+    total = int(sum(table_sizes))
+    if not 0 <= global_id < total:
+        raise TraceValidationError(f"global_id {global_id} out of range [0, {total})")
+    offsets = table_offsets(table_sizes)
+    t = int(np.searchsorted(offsets, global_id, side="right")) - 1
+    return EmbeddingIndex(t, int(global_id - offsets[t]), int(global_id))
+
+
+class Trace:
+    """Ordered accesses over a fixed table layout (trace.py:54-77)."""
+
+    def __init__(self, gid_array, table_sizes):
+        self.gid_array = np.ascontiguousarray(gid_array, dtype=np.int64)
+        self.table_sizes = [int(s) for s in table_sizes]
+        self._unique = None
+
+    @property
+    def unique_count(self) -> int:
+        if self._unique is None:
+            self._unique = int(np.unique(self.gid_array).size)
+        return self._unique
+
+    def __len__(self) -> int:
+        return len(self.gid_array)
+
+    @property
+    def total_ids(self) -> int:
+        return int(sum(self.table_sizes))
+
+    @property
+    def table_ids(self) -> np.ndarray:
+        off = table_offsets(self.table_sizes)
+        return np.searchsorted(off, self.gid_array, side="right") - 1
+
+    @property
+    def accesses(self) -> list[EmbeddingIndex]:
+        off = table_offsets(self.table_sizes)
+        t = self.table_ids
+        return [EmbeddingIndex(int(a), int(g - off[a]), int(g))
+                for a, g in zip(t, self.gid_array)]
+
+    def __eq__(self, other):
+        return (list(self.table_sizes) == list(other.table_sizes)
+                and np.array_equal(self.gid_array, other.gid_array))
+
+
+def trace_from_gids(gids, table_sizes) -> Trace:
+    """trace.py:80-91."""
+    offsets = table_offsets(table_sizes)
+    gids = np.asarray(gids, dtype=np.int64)
+    if gids.size and (gids.min() < 0 or gids.max() >= offsets[-1]):
+        raise TraceValidationError("global id out of range for table layout")
+    return Trace(gids, table_sizes)
+
+
+@dataclass
+class TraceGenConfig:
+    """trace.py:94-121."""
+    table_sizes: list
+    total_accesses: int
+    zipf_exponent: float = 1.1
+    markov_stickiness: float = 0.0
+    correlation_pool_size: int = 32
+    rng_seed: int = 0
+
+    def validate(self):
+        if not self.table_sizes or any(s <= 0 for s in self.table_sizes):
+            raise InvalidConfigError("table_sizes must be non-empty and positive")
+        if self.total_accesses <= 0:
+            raise InvalidConfigError("total_accesses must be positive")
+        if self.zipf_exponent < 0:
+            raise InvalidConfigError("zipf_exponent must be >= 0")
+        if not 0.0 <= self.markov_stickiness <= 1.0:
+            raise InvalidConfigError("markov_stickiness must be in [0, 1]")
+        if self.correlation_pool_size < 1:
+            raise InvalidConfigError("correlation_pool_size must be >= 1")
+
+
+def generate_trace(cfg: TraceGenConfig) -> Trace:
+    """Bit-identical to the reference generate_trace (trace.py:124-161).
+
+    The draws use the same numpy Generator calls in the same order
+    (permutation, then ``choice(p=...)`` — restated as numpy's own
+    ``cdf.searchsorted(random(n), 'right')`` — then the two coin arrays);
+    the sequential sticky-pool pass (:144-160) runs in C
+    (recmg_trace_pool_pass).
+    """
+    cfg.validate()
+    rng = np.random.default_rng(cfg.rng_seed)
+    total = int(sum(cfg.table_sizes))
+    n = int(cfg.total_accesses)
+    ranks = np.arange(1, total + 1, dtype=np.float64)
+    weights = ranks ** (-cfg.zipf_exponent)
+    probs = weights / weights.sum()
+    rank_to_gid = rng.permutation(total)
+    # Generator.choice(total, size=n, p=probs) for 1-D p: cdf = cumsum(p),
+    # cdf /= cdf[-1], uniform = random(n), idx = cdf.searchsorted(u, 'right')
+    cdf = probs.cumsum()
+    cdf /= cdf[-1]
+    zipf_ranks = cdf.searchsorted(rng.random(n), side="right")
+    sticky_coin = rng.random(n)
+    pool_coin = rng.random(n)
+    zipf_gids = rank_to_gid[zipf_ranks].astype(np.int64)
+    gids = _native.pool_pass(zipf_gids, sticky_coin, pool_coin, cfg.markov_stickiness,
+                             cfg.correlation_pool_size)
+    return Trace(gids, cfg.table_sizes)
+
+
+@dataclass
+class SequenceSample:
+    """trace.py:207-223."""
+    input: list
+    origin: int
+    cache_labels: list | None = None
+    prefetch_targets: list | None = None
+    window: list | None = None
+
+    def with_labels(self, **kw) -> "SequenceSample":
+        return replace(self, **kw)
+
+
+def num_chunks(n: int, l_in: int = 15, l_out: int = 5, window_ratio: int = 3) -> int:
+    """len(chunk(trace, ...)) without building samples (trace.py:238-250)."""
+    l_win = window_ratio * l_out
+    if n < l_in + l_win:
+        return 0
+    return (n - l_in - l_win) // l_in + 1
+
+
+def chunk(trace, l_in: int = 15, l_out: int = 5, window_ratio: int = 3) -> list:
+    """trace.py:226-250 (materialises Python samples: for callables only)."""
+    if l_in < 1 or l_out < 1:
+        raise InvalidConfigError("l_in and l_out must be >= 1")
+    if window_ratio < 1:
+        raise InvalidConfigError("window_ratio must be >= 1")
+    l_win = window_ratio * l_out
+    acc = trace.accesses
+    out = []
+    for k in range(num_chunks(len(acc), l_in, l_out, window_ratio)):
+        o = k * l_in
+        out.append(SequenceSample(input=acc[o:o + l_in], origin=o,
+                                  window=acc[o + l_in:o + l_in + l_win]))
+    return out

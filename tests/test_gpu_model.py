@@ -1,0 +1,130 @@
+"""K1 / K2 (fp32 LSTM forwards) on the B200 vs the float64 oracle and the
+reference's own outputs.  Tolerance (north star / SURVEY.md §8c): logits
+within 1e-3 relative, measured as |d| <= 1e-3 * max(|ref|, 1e-2) because
+relative error is meaningless at logits ~1e-6."""
+import numpy as np
+import pytest
+
+import paper_2511_08568_b200 as rb
+from oracle import model_oracle as mo
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-3
+FLOOR = 1e-2
+
+
+def _check(got, ref):
+    err = np.abs(got - ref) / np.maximum(np.abs(ref), FLOOR)
+    assert err.max() <= RTOL, f"max scaled error {err.max():.3e}"
+    return err.max()
+
+
+def test_models_vs_reference_fixture():
+    m = golden("models.npz")
+    sizes = [int(s) for s in m["table_sizes"]]
+    for kind, dim, seed, scale in m["cases"]:
+        kind = "caching" if kind == 0 else "prefetch"
+        dim, seed = int(dim), int(seed)
+        p = rb.init_params(kind, sizes, dim=dim, seed=seed, init_scale=float(scale))
+        fwd = rb.forward_caching_batch if kind == "caching" else rb.forward_prefetch_batch
+        res = fwd(p, m["gid"], m["tid"])
+        probs = m[f"{kind}_{dim}_{seed}_probs"]
+        ref_logit = np.log(probs) - np.log1p(-probs)
+        _check(res.logits, ref_logit)
+        assert np.abs(res.value - probs).max() < 1e-5
+
+
+@pytest.mark.parametrize("scale", [0.08, 0.4, 0.6])
+def test_config1_shapes_vs_oracle(scale):
+    """d = 64, config-1 layout, 512 chunks of a config-1 style trace."""
+    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 512 * 15 + 30, 1.05, 0.4, 32, 0))
+    K = rb.num_chunks(len(t))
+    gid = t.gid_array[:K * 15].reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=scale)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=scale)
+    lc = rb.forward_caching_batch(cp, gid, tid).logits
+    lp = rb.forward_prefetch_batch(pp, gid, tid).logits
+    rc = mo.caching_logits(cp.arrays, 64, 1, gid, tid)
+    rp = mo.prefetch_logits(pp.arrays, 64, 2, 5, gid, tid)
+    _check(lc, rc)
+    _check(lp, rp)
+    # decisions: bit flips only where the reference logit is ~0
+    flips = (lc >= 0) != (rc >= 0)
+    assert np.all(np.abs(rc[flips]) < 1e-4)
+
+
+def test_gpu_decisions_in_replay_path():
+    """bits / decoded prefetch ids emitted by the kernel (runtime.py:192,
+    model.py:250-258) vs the oracle's, through the replay entry point."""
+    import torch
+    from paper_2511_08568_b200.model import DeviceModel
+    t = rb.generate_trace(rb.TraceGenConfig([250] * 8, 3000 * 15 + 30, 1.05, 0.4, 32, 3))
+    K = rb.num_chunks(len(t))
+    gid = t.gid_array[:K * 15].reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=0.4)
+    g = torch.from_numpy(gid.astype(np.int32)).cuda()
+    dm = DeviceModel(cp)
+    tt = dm.table_ids(g)
+    assert np.array_equal(tt.cpu().numpy(), tid)
+    bits = torch.empty((K, 15), dtype=torch.uint8, device="cuda")
+    lc = dm.forward(g, tt, bits=bits).cpu().numpy()
+    assert np.array_equal(bits.cpu().numpy(), (lc >= 0).astype(np.uint8))
+    dp = DeviceModel(pp)
+    pf = torch.empty((K, 5), dtype=torch.int32, device="cuda")
+    lp = dp.forward(g, tt, pf_gid=pf).cpu().numpy()
+    want = mo.decode_gids(mo.sigmoid(lp.astype(np.float64)), t.total_ids)
+    assert np.array_equal(pf.cpu().numpy(), want)
+    rp = mo.prefetch_logits(pp.arrays, 64, 2, 5, gid, tid)
+    agree = np.mean(pf.cpu().numpy() == mo.decode_gids(mo.sigmoid(rp), t.total_ids))
+    assert agree > 0.97, agree
+
+
+def test_zero_weights_and_causality():
+    sizes = [6, 10]
+    # test_model.py:45-58
+    p = rb.init_params("caching", sizes, dim=4, l_in=5, seed=0)
+    for a in p.arrays.values():
+        a[:] = 0.0
+    probs = rb.forward_caching(p, rb.trace_from_gids([0, 3, 7, 7, 1], sizes).accesses)
+    assert probs == [0.5] * 5
+    p = rb.init_params("prefetch", sizes, dim=4, l_in=4, l_out=3, seed=0)
+    for a in p.arrays.values():
+        a[:] = 0.0
+    po = rb.forward_prefetch(p, rb.trace_from_gids([0, 1, 2, 3], sizes).accesses)
+    assert po == [po[0]] * 3
+    # test_model.py:71-77 (causal attention)
+    p = rb.init_params("caching", sizes, dim=6, l_in=6, seed=8)
+    a = rb.forward_caching(p, rb.trace_from_gids([0, 3, 7, 2, 5, 9], sizes).accesses)
+    b = rb.forward_caching(p, rb.trace_from_gids([0, 3, 7, 8, 8, 8], sizes).accesses)
+    assert a[:3] == b[:3]
+    assert all(abs(x - y) > 1e-9 for x, y in zip(a[3:], b[3:]))
+
+
+def test_replay_with_gpu_models_end_to_end():
+    """replay(caching_params, prefetch_params): decisions from K1/K2 feed K3;
+    the result equals the oracle replay of the kernel's own decisions."""
+    import oracle
+    import torch
+    from paper_2511_08568_b200.model import DeviceModel
+    t = rb.generate_trace(rb.TraceGenConfig([250] * 8, 20000, 1.05, 0.4, 32, 9))
+    cp = rb.init_params("caching", t.table_sizes, dim=32, seed=0, init_scale=0.4)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=32, seed=1, init_scale=0.4)
+    C = int(0.2 * t.unique_count)
+    rep = rb.replay(t, rb.BufferConfig(C), cp, pp)
+    K = rb.num_chunks(len(t))
+    g = torch.from_numpy(t.gid_array[:K * 15].reshape(K, 15).astype(np.int32)).cuda()
+    dc, dp = DeviceModel(cp), DeviceModel(pp)
+    tt = dc.table_ids(g)
+    bits = torch.empty((K, 15), dtype=torch.uint8, device="cuda")
+    pf = torch.empty((K, 5), dtype=torch.int32, device="cuda")
+    dc.forward(g, tt, bits=bits)
+    dp.forward(g, tt, pf_gid=pf)
+    ref, cov = oracle.replay(t.gid_array, t.total_ids, C, 0, 4, bits=bits.cpu().numpy(),
+                             pf=pf.cpu().numpy().astype(np.int64))
+    assert (rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_useful) == \
+        (ref["cache_hits"], ref["prefetch_hits"], ref["on_demand"], ref["prefetch_useful"])
+    assert rep.coverage == cov
