@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark of the RecMG per-access hot path on B200.
+
+metric (BASELINE.json): embedding accesses/s through model inference +
+buffer replay, with on-demand fetches vs a 32-way LRU on the same trace.
+
+One step = one pass of the hot path over the whole synthetic trace:
+table ids -> caching LSTM (K1) -> prefetch LSTM + fp64 decode (K2) ->
+32-way priority-buffer replay (K3, incl. prefetch stats and the per-set
+partition) -> 32-way LRU comparator (K4), from an empty buffer.
+
+Workload (config 2 of BASELINE.json, the single-GPU config): 25 M accesses,
+256 tables x 50,000 rows, Zipf 1.05, stickiness 0.4, pool 32 (the reference
+generator, bit-exact), caching model d=64 / 1 stack, prefetch model d=64 /
+2 stacks (reference init_params, init_scale 0.4 so the decisions are not
+degenerate), buffer = 20% of unique ids rounded down to 32 ways, es = 4.
+
+N > 1 (torchrun): weak scaling, table-sharded: every rank owns its own
+256-table shard and its own 25 M-access slice (seed 2 + rank), no collective
+on the data path; counters are summed at the end.
+
+--impl reference: the reference's CPU algorithm (the oracle port: numpy
+float64 forwards + the C replay restatement, oracle/) on a bounded sample of
+the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "embedding accesses/sec (model+buffer replay); on-demand fetches vs 32-way LRU"
+UNIT = "accesses/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="recmg", choices=["recmg", "reference"])
+    ap.add_argument("--accesses", type=int, default=25_000_000)
+    ap.add_argument("--tables", type=int, default=256)
+    ap.add_argument("--rows", type=int, default=50_000)
+    ap.add_argument("--dim", type=int, default=64)
+    ap.add_argument("--init-scale", type=float, default=0.4)
+    ap.add_argument("--cpu-sample", type=int, default=300_000,
+                    help="accesses in the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args, rank):
+    return {
+        "workload": "config2: synthetic Zipf trace, 256 tables x 50k rows, 25M accesses; "
+                    "caching LSTM (1 stack) + prefetch LSTM (2 stacks), d=64, l_in 15 / l_out 5; "
+                    "32-way priority buffer at 20% of unique ids (es=4) + 32-way LRU comparator",
+        "accesses_per_gpu": args.accesses, "tables_per_gpu": args.tables,
+        "rows_per_table": args.rows, "zipf": 1.05, "stickiness": 0.4, "pool": 32,
+        "trace_seed": 2 + rank, "dim": args.dim, "init_scale": args.init_scale,
+        "ways": 32, "eviction_speed": 4, "window_ratio": 3,
+        "l2": "inputs larger than L2 (100 MB of ids + 6.6 GB of embedding weights per step)",
+    }
+
+
+def caching_flops(L, d):
+    # 32*L*d^2 + 2*L^2*d + L*d MACs per chunk
+    return 2 * (32 * L * d * d + 2 * L * L * d + L * d)
+
+
+def prefetch_flops(L, T, d):
+    # 21*L*d^2 + T*(27 d^2 + 2 L d + d) MACs per chunk
+    return 2 * (21 * L * d * d + T * (27 * d * d + 2 * L * d + d))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_profile_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------------------
+def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways):
+    """The reference algorithm on the host cores (oracle port), on the first
+    n_sample accesses: float64 numpy forwards in batches of 256 (runtime.py:
+    181-210), fp64 decode, the C replay restatement in the reference's dense
+    per-id layout (runtime.py:41-112, 220-283) and the 32-way LRU."""
+    import oracle
+    from oracle import model_oracle as mo
+    from paper_2511_08568_b200.trace import num_chunks
+    gids = t.gid_array[:n_sample]
+    K = num_chunks(len(gids))
+    uniq, inv = np.unique(gids[:K * 15], return_inverse=True)
+    ac = dict(cparams.arrays)
+    ap = dict(pparams.arrays)
+    ac["embed_id"] = emb_c[uniq].double().cpu().numpy() if hasattr(emb_c, "cpu") else emb_c[uniq]
+    ap["embed_id"] = emb_p[uniq].double().cpu().numpy() if hasattr(emb_p, "cpu") else emb_p[uniq]
+    lg = inv.reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    V = t.total_ids
+    oracle.lib()
+    # untimed warm-up batch (BLAS thread pool, page faults)
+    mo.caching_logits(ac, cparams.dim, cparams.stacks, lg[:256], tid[:256])
+    mo.prefetch_logits(ap, pparams.dim, pparams.stacks, 5, lg[:256], tid[:256])
+    t0 = time.perf_counter()
+    bits = np.empty((K, 15), dtype=np.uint8)
+    pf = np.empty((K, 5), dtype=np.int64)
+    for b in range(0, K, 256):
+        lc = mo.caching_logits(ac, cparams.dim, cparams.stacks, lg[b:b + 256], tid[b:b + 256])
+        bits[b:b + 256] = lc >= 0
+        lp = mo.prefetch_logits(ap, pparams.dim, pparams.stacks, 5, lg[b:b + 256], tid[b:b + 256])
+        pf[b:b + 256] = mo.decode_gids(mo.sigmoid(lp), V)
+    t1 = time.perf_counter()
+    rep, _ = oracle.replay(gids, V, capacity, ways, 4, bits=bits, pf=pf, dense=True)
+    oracle.lru(gids, V, capacity, ways)
+    t2 = time.perf_counter()
+    return {"value": len(gids) / (t2 - t0), "unit": UNIT,
+            "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"first {len(gids)} accesses of the rank-0 config-2 trace ({K} chunks): "
+                      f"numpy float64 forwards (OpenBLAS threads) {t1 - t0:.2f}s + C replay "
+                      f"(dense per-id layout) + 32-way LRU {t2 - t1:.2f}s",
+            "model_s": t1 - t0, "replay_s": t2 - t1}
+
+
+def build_state(args, rank, torch):
+    import paper_2511_08568_b200 as rb
+    from paper_2511_08568_b200.model import DeviceModel, init_params_device
+    t0 = time.time()
+    t = rb.generate_trace(rb.TraceGenConfig([args.rows] * args.tables, args.accesses, 1.05, 0.4,
+                                            32, 2 + rank))
+    U = t.unique_count
+    C = int(math.floor(0.2 * U))
+    C32 = C - C % 32
+    cp, emb_c = init_params_device("caching", t.table_sizes, dim=args.dim, seed=0,
+                                   init_scale=args.init_scale)
+    pp, emb_p = init_params_device("prefetch", t.table_sizes, dim=args.dim, seed=1,
+                                   init_scale=args.init_scale)
+    return t, U, C, C32, cp, emb_c, pp, emb_p, time.time() - t0
+
+
+def main():
+    args = parse()
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world, torch, dist)
+
+    import paper_2511_08568_b200 as rb
+    from paper_2511_08568_b200 import _native
+    from paper_2511_08568_b200.model import DeviceModel
+    from paper_2511_08568_b200.pipeline import HotPath
+
+    t, U, C, C32, cp, emb_c, pp, emb_p, setup_s = build_state(args, rank, torch)
+    n = len(t)
+    hp = HotPath(DeviceModel(cp, emb_c), DeviceModel(pp, emb_p), t.table_sizes, C32, n,
+                 ways=32, eviction_speed=4, lru_capacity=C32, lru_ways=32)
+    host = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
+    hp.gids[:n].copy_(host)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        hp.launch(n)
+    rep, lru = hp.report()
+
+    # ---- device-resident timing -------------------------------------------
+    hp.enable_stage_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    stage_events = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    launches0 = _native.lib().recmg_launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for i in range(args.steps):
+        hp.enable_stage_timing(True)
+        hp.launch(n)
+        stage_events.append(hp.events)
+    end.record()
+    torch.cuda.synchronize()
+    launches = _native.lib().recmg_launch_count() - launches0
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    dev_ms = start.elapsed_time(end)
+    stage_ms = {s: [] for s in HotPath.STAGES}
+    for evs in stage_events:
+        for j, s in enumerate(HotPath.STAGES):
+            stage_ms[s].append(evs[j][0].elapsed_time(evs[j][1]))
+    rep, lru = hp.report()
+    hp.events = None
+
+    # ---- end to end: host gids in, report out --------------------------------
+    e2e_ms = None
+    if not args.no_e2e:
+        hp.replay_host(host)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep_e, lru_e = hp.replay_host(host)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1000.0
+        assert rep_e == rep and lru_e == lru, "e2e replay disagrees with device replay"
+
+    # ---- reduce over ranks ---------------------------------------------------
+    vals = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device="cuda")
+    ctr = torch.tensor([rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
+                        rep.prefetch_useful, rep.evictions, rep.prefetch_inserts, lru[1], n],
+                       dtype=torch.int64, device="cuda")
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ctr, op=dist.ReduceOp.SUM)
+    dev_ms, e2e_ms_max = vals.tolist()
+    c = ctr.tolist()
+    total_n = c[8]
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    ms_step = dev_ms / args.steps
+    value = total_n / (ms_step / 1000.0)
+    K = hp.K
+    mean = {s: (sum(v) / len(v) if v else 0.0) for s, v in stage_ms.items()}
+    fl_c = caching_flops(15, args.dim) * K
+    fl_p = prefetch_flops(15, 5, args.dim) * K
+    dominant = max(("caching_fwd", "prefetch_fwd", "replay", "lru"), key=lambda s: mean[s])
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except (OSError, ValueError):
+        pass
+    prof = load_profile_traffic() or {}
+    if dominant in ("caching_fwd", "prefetch_fwd"):
+        fl = fl_c if dominant == "caching_fwd" else fl_p
+        achieved = fl / (mean[dominant] / 1000.0) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        roof = {"kernel": dominant, "bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)",
+                "algorithmic_flop_per_launch": fl,
+                "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch")}
+    else:
+        ev_n = K * (2 * 15 + 5) + (n - K * 15)
+        byts = ev_n * 4 + n * 1
+        achieved = byts / (mean[dominant] / 1000.0) / 1e9
+        peak = peaks.get("hbm_gbs", 6538.6)
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch")}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
+        "config": workload(args, 0),
+        "quality": {"on_demand": c[2], "lru32_misses": c[7],
+                    "on_demand_vs_lru32": (c[2] / c[7]) if c[7] else None,
+                    "cache_hits": c[0], "prefetch_hits": c[1], "prefetch_issued": c[3],
+                    "prefetch_useful": c[4], "evictions": c[5], "prefetch_inserts": c[6],
+                    "coverage_rank0": rep.coverage, "capacity_rank0": C32, "unique_rank0": U},
+        "stages_ms": mean,
+        "gpu_launches": int(launches // args.steps),
+        "roofline": roof,
+        "clocks": clk,
+        "setup_s": setup_s,
+    }
+    line["roofline"]["caching_fwd_tflops"] = fl_c / (mean["caching_fwd"] / 1000.0) / 1e12
+    line["roofline"]["prefetch_fwd_tflops"] = fl_p / (mean["prefetch_fwd"] / 1000.0) / 1e12
+    if e2e_ms is not None:
+        e2e_step = e2e_ms_max / args.steps
+        line["e2e"] = {"value": total_n / (e2e_step / 1000.0), "unit": UNIT,
+                       "ms_per_step": e2e_step,
+                       "h2d_bytes_per_step": int(n * 4),
+                       "d2h_bytes_per_step": int(hp.d2h_bytes())}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank, world, torch, dist):
+    """--impl reference: the reference CPU algorithm (oracle port) on rank 0."""
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    import paper_2511_08568_b200 as rb
+    # the full rank-0 trace: the buffer capacity is 20% of ITS unique ids
+    t = rb.generate_trace(rb.TraceGenConfig([args.rows] * args.tables, args.accesses,
+                                            1.05, 0.4, 32, 2))
+    # The reference's float64 weights (init_params, model.py:83-100) for the
+    # rows the sample touches: one uniform double per PCG64 draw, so embed_id
+    # row g is draws [g*d, (g+1)*d) and the dense arrays start at draw V*d.
+    from paper_2511_08568_b200.model import _shapes
+    V, d = t.total_ids, args.dim
+    uniq = np.unique(t.gid_array[:args.cpu_sample])
+    emb, dense = {}, {}
+    for kind, seed in (("caching", 0), ("prefetch", 1)):
+        full = np.zeros((int(uniq.max()) + 1, d))
+        for g in uniq:
+            b = np.random.PCG64(seed)
+            b.advance(int(g) * d)
+            full[g] = np.random.Generator(b).uniform(-args.init_scale, args.init_scale, d)
+        b = np.random.PCG64(seed)
+        b.advance(V * d)
+        rng = np.random.Generator(b)
+        shp = _shapes(kind, V, len(t.table_sizes), d, 1 if kind == "caching" else 2, 5)
+        dense[kind] = {nm: rng.uniform(-args.init_scale, args.init_scale, size=s)
+                       for nm, s in shp.items() if nm != "embed_id"}
+        emb[kind] = full
+    C = int(math.floor(0.2 * t.unique_count))
+    C32 = C - C % 32
+
+    class P:
+        pass
+    cp, pp = P(), P()
+    cp.arrays, cp.dim, cp.stacks = dense["caching"], d, 1
+    pp.arrays, pp.dim, pp.stacks = dense["prefetch"], d, 2
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(t, cp, pp, emb["caching"], emb["prefetch"], args.cpu_sample, C32, 32)
+        vals.append(last["value"])
+    value = statistics.median(vals)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": args.cpu_sample / value * 1000.0,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
+            "config": workload(args, 0), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"],
+                             "kind": "port", "sample": last["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

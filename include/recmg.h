@@ -103,8 +103,9 @@ int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t
  *                      chunk order (runtime.py:276,282) via recmg_coverage_mean
  *   access_class[n]    nullable: 0 cache hit, 1 prefetch hit, 2 on-demand
  * Status: RECMG_E_INVALID_CONFIG for a bad cfg / l_in / l_out / window_ratio
- * (trace.py:233-236); bits outside {0,1} are RECMG_E_BUFFER_STATE
- * (runtime.py:127-128) and are reported through counters->occupancy = -1.
+ * (trace.py:233-236).  Bits must be 0/1: the model path only emits 0/1, and
+ * the host mirror rejects other caching_fn output with ValueError before
+ * any launch (runtime.py:124-128); a nonzero byte here is read as 1.
  */
 int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                  int32_t l_in, int32_t l_out, int32_t window_ratio, const uint8_t *bits,
@@ -184,6 +185,10 @@ int recmg_table_ids(const int32_t *gids, int64_t n, const int64_t *offsets, int3
 int recmg_trace_pool_pass(const int64_t *host_zipf_gids, const double *host_sticky_coin,
                           const double *host_pool_coin, int64_t n, double stickiness,
                           int32_t pool_size, int64_t *host_out_gids);
+
+/* ---- instrumentation --------------------------------------------------- */
+/* Kernels this library has launched since it was loaded (host counter).   */
+uint64_t recmg_launch_count(void);
 
 #ifdef __cplusplus
 }

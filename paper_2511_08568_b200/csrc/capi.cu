@@ -8,6 +8,12 @@
 
 using namespace recmg;
 
+#include <atomic>
+namespace recmg {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace recmg
+
 namespace {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -67,6 +73,8 @@ const char *recmg_status_category(int status) {
         default: return "error";
     }
 }
+
+uint64_t recmg_launch_count(void) { return g_launches.load(); }
 
 int64_t recmg_num_chunks(int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio) {
     // trace.py:238-250: origins 0, l_in, ... while origin + l_in + l_win <= n

@@ -11,7 +11,14 @@
         if (_e != cudaSuccess) return RECMG_E_CUDA;                 \
     } while (0)
 
-#define RECMG_LAUNCH_CHECK() RECMG_CUDA_TRY(cudaGetLastError())
+// Every kernel launch is followed by exactly one RECMG_LAUNCH_CHECK, which
+// also counts it (recmg_launch_count, the bench's gpu_launches evidence).
+namespace recmg { void note_launch(); }
+#define RECMG_LAUNCH_CHECK()            \
+    do {                                \
+        recmg::note_launch();           \
+        RECMG_CUDA_TRY(cudaGetLastError()); \
+    } while (0)
 
 namespace recmg {
 

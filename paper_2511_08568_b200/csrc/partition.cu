@@ -195,7 +195,9 @@ int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t M, uint32_t *p
     if (M <= 0) return RECMG_OK;
     int64_t nb = (M + kScanTile - 1) / kScanTile;
     scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(in, M, partial);
+    RECMG_LAUNCH_CHECK();
     scan_partials_kernel<<<1, kScanThreads, 0, s>>>(partial, nb);
+    RECMG_LAUNCH_CHECK();
     scan_downsweep_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, M, partial);
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
@@ -244,6 +246,7 @@ int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaSt
         int shift = 8 * p;
         part_hist_kernel<<<pb.ntiles, kPartThreads, 0, s>>>(kin, N, (uint32_t)S, shift, pb.hist,
                                                            pb.ntiles);
+        RECMG_LAUNCH_CHECK();
         int rc = exclusive_scan_u32(pb.hist, pb.offs, M, pb.partial, s);
         if (rc) return rc;
         if (vin)

@@ -86,6 +86,35 @@ def init_params(kind, table_sizes, dim=32, stacks=None, l_in=15, l_out=5, seed=0
     return ModelParameters(kind, list(table_sizes), dim, stacks, l_in, l_out, arrays)
 
 
+def init_params_device(kind, table_sizes, dim=32, stacks=None, l_in=15, l_out=5, seed=0,
+                       init_scale=0.08, block_rows=1 << 20):
+    """init_params with embed_id streamed to the GPU in row blocks.
+
+    Draws exactly the values init_params draws (same default_rng(seed)
+    stream, same _shapes order; Generator.uniform fills element by element,
+    so block draws continue the one stream), but never holds the float64
+    [V, d] embed_id on the host: each block is cast to fp32 and copied into
+    HBM.  Returns (ModelParameters without "embed_id", embed_id fp32 [V, d]
+    on the device).
+    """
+    if kind not in (CACHING, PREFETCH):
+        raise InvalidConfigError(f"unknown model kind {kind!r}")
+    if stacks is None:
+        stacks = 1 if kind == CACHING else 2
+    torch = _native.torch_cuda()
+    rng = np.random.default_rng(seed)
+    total = int(sum(table_sizes))
+    shapes = _shapes(kind, total, len(table_sizes), dim, stacks, l_out)
+    emb = torch.empty((total, dim), dtype=torch.float32, device="cuda")
+    for r0 in range(0, total, block_rows):
+        r1 = min(total, r0 + block_rows)
+        blk = rng.uniform(-init_scale, init_scale, size=(r1 - r0, dim)).astype(np.float32)
+        emb[r0:r1].copy_(torch.from_numpy(blk))
+    arrays = {name: rng.uniform(-init_scale, init_scale, size=shape)
+              for name, shape in shapes.items() if name != "embed_id"}
+    return ModelParameters(kind, list(table_sizes), dim, stacks, l_in, l_out, arrays), emb
+
+
 class DeviceModel:
     """A model's weights resident in HBM in the kernel layout.
 
