@@ -231,7 +231,7 @@ def main():
 
     for _ in range(args.warmup):
         hp.launch(n)
-    rep, lru = hp.report()
+    torch.cuda.synchronize()
 
     # ---- device-resident timing -------------------------------------------
     hp.enable_stage_timing(True)

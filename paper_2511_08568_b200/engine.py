@@ -33,6 +33,7 @@ class BufferReplay:
         self._ws = None
         self._ws_key = None
         self._cov = None
+        self.K = 0
         self.reserve(n, pf_stride)
         self.reset()
 
