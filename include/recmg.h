@@ -186,6 +186,13 @@ int recmg_trace_pool_pass(const int64_t *host_zipf_gids, const double *host_stic
                           const double *host_pool_coin, int64_t n, double stickiness,
                           int32_t pool_size, int64_t *host_out_gids);
 
+/* ---- diagnostics -------------------------------------------------------- */
+/* tcgen05 self-test GEMM: D[128 x N] (fp32, row-major) = A[128 x K] * B[N x K]^T
+ * with A, B fp16 row-major; A staged in shared memory (a_in_tmem = 0) or in
+ * tensor memory (1).  Pins the descriptor / TMEM layouts of the LSTM kernels. */
+int recmg_selftest_umma(const void *A, const void *B, float *D, int N, int K, int a_in_tmem,
+                        void *stream);
+
 /* ---- instrumentation --------------------------------------------------- */
 /* Kernels this library has launched since it was loaded (host counter).   */
 uint64_t recmg_launch_count(void);

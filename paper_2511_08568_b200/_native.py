@@ -38,7 +38,7 @@ EXPORTS = (
     "recmg_coverage_mean", "recmg_simulate_workspace_bytes", "recmg_simulate",
     "recmg_buffer_op", "recmg_model_dense_floats", "recmg_model_packed_bytes",
     "recmg_model_pack", "recmg_model_forward", "recmg_table_ids", "recmg_trace_pool_pass",
-    "recmg_launch_count",
+    "recmg_launch_count", "recmg_selftest_umma",
 )
 
 
@@ -93,6 +93,8 @@ def lib():
         "recmg_table_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp]),
         "recmg_trace_pool_pass": (ctypes.c_int, [vp, vp, vp, i64, ctypes.c_double, i32, vp]),
         "recmg_launch_count": (ctypes.c_uint64, []),
+        "recmg_selftest_umma": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
