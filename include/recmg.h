@@ -139,7 +139,13 @@ int recmg_buffer_op(const recmg_buffer_cfg *cfg, void *state, int32_t op, int64_
 
 /* ---- models  (neural/model.py) ----------------------------------------- */
 enum { RECMG_MODEL_CACHING = 0, RECMG_MODEL_PREFETCH = 1 };
-enum { RECMG_PREC_FP32 = 0 };  /* fp32 storage + fp32 math (logits within 1e-3) */
+enum {
+    RECMG_PREC_FP32 = 0, /* SIMT: fp32 weights, fp32 FMA, any dim <= 64            */
+    RECMG_PREC_TC32 = 1  /* tcgen05: every GEMM as the fp16 hi/lo 3-product split
+                            with fp32 accumulation in TMEM (fp32-class logits);
+                            dim 64, l_in/l_out <= 16, 1 (caching) / 2 (prefetch)
+                            stacks; token projection folded into per-id tables   */
+};
 
 typedef struct {
     int32_t kind;      /* ModelParameters.kind (model.py:28-38)   */
@@ -154,13 +160,21 @@ typedef struct {
 /* Floats of the raw dense blob: every array of _shapes (model.py:54-80)
  * except embed_id, row-major, concatenated in _shapes order.               */
 int64_t recmg_model_dense_floats(const recmg_model_shape *shape);
-/* Bytes of the packed (kernel-layout) dense weights.                       */
+/* Bytes of the packed (kernel-layout) weights for a precision; 0 if that
+ * precision does not support the shape.  TC32 includes the folded token
+ * tables (total_ids x 4*dim fp32 per layer-0 projection).                  */
 size_t recmg_model_packed_bytes(const recmg_model_shape *shape, int32_t precision);
 /* Re-lay the raw dense blob into the kernel layout (gate-interleaved LSTM
  * weights).  Ingests init_params / load_checkpoint arrays (model.py:83-100,
  * checkpoint.py:48-79) after a float64 -> float32 cast.                    */
 int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, void *packed,
                      int32_t precision, void *stream);
+/* TC32 packing also needs embed_id [total_ids x dim] fp32 (folded tables). */
+int recmg_model_pack_tc(const recmg_model_shape *shape, const float *dense_raw,
+                        const float *embed_id, void *packed, void *stream);
+/* Scratch bytes recmg_model_forward needs for `batch` chunks.              */
+size_t recmg_model_workspace_bytes(const recmg_model_shape *shape, int32_t precision,
+                                   int64_t batch);
 /*
  * forward_caching_batch (model.py:184-196) / forward_prefetch_batch
  * (model.py:199-212) over `batch` chunks:
@@ -173,7 +187,7 @@ int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, voi
 int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
                         const float *embed_id, const void *packed, const int32_t *gid,
                         const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
-                        int32_t *pf_gid, void *stream);
+                        int32_t *pf_gid, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- trace helpers ----------------------------------------------------- */
 /* tid[i] = table of gids[i] given table offsets[n_tables+1] (device), the

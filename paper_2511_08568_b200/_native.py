@@ -30,6 +30,7 @@ POLICY_LRU = 1
 OP_ADD, OP_POPULATE, OP_REFERENCE, OP_SET_PRIORITY, OP_QUERY = range(5)
 MODEL_CACHING, MODEL_PREFETCH = 0, 1
 PREC_FP32 = 0
+PREC_TC32 = 1
 
 # every symbol include/recmg.h declares (tests check the export table)
 EXPORTS = (
@@ -38,7 +39,8 @@ EXPORTS = (
     "recmg_coverage_mean", "recmg_simulate_workspace_bytes", "recmg_simulate",
     "recmg_buffer_op", "recmg_model_dense_floats", "recmg_model_packed_bytes",
     "recmg_model_pack", "recmg_model_forward", "recmg_table_ids", "recmg_trace_pool_pass",
-    "recmg_launch_count", "recmg_selftest_umma",
+    "recmg_launch_count", "recmg_selftest_umma", "recmg_model_pack_tc",
+    "recmg_model_workspace_bytes",
 )
 
 
@@ -89,7 +91,10 @@ def lib():
         "recmg_model_dense_floats": (i64, [shp]),
         "recmg_model_packed_bytes": (sz, [shp, i32]),
         "recmg_model_pack": (ctypes.c_int, [shp, vp, vp, i32, vp]),
-        "recmg_model_forward": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp]),
+        "recmg_model_forward": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp,
+                                               sz, vp]),
+        "recmg_model_pack_tc": (ctypes.c_int, [shp, vp, vp, vp, vp]),
+        "recmg_model_workspace_bytes": (sz, [shp, i32, i64]),
         "recmg_table_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp]),
         "recmg_trace_pool_pass": (ctypes.c_int, [vp, vp, vp, i64, ctypes.c_double, i32, vp]),
         "recmg_launch_count": (ctypes.c_uint64, []),

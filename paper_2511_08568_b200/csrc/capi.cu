@@ -2,6 +2,7 @@
 #include <string.h>
 
 #include "lstm.cuh"
+#include "lstm_tc.cuh"
 #include "model_layout.cuh"
 #include "partition.cuh"
 #include "replay.cuh"
@@ -255,9 +256,16 @@ int64_t recmg_model_dense_floats(const recmg_model_shape *shape) {
     return raw_layout(shape).total;
 }
 
+static size_t dense_bytes_aligned(const recmg_model_shape *shape) {
+    return align_up((size_t)packed_layout(shape).total * sizeof(float), 256);
+}
+
 size_t recmg_model_packed_bytes(const recmg_model_shape *shape, int32_t precision) {
-    if (!shape_ok(shape) || precision != RECMG_PREC_FP32) return 0;
-    return (size_t)packed_layout(shape).total * sizeof(float);
+    if (!shape_ok(shape)) return 0;
+    if (precision == RECMG_PREC_FP32) return (size_t)packed_layout(shape).total * sizeof(float);
+    if (precision == RECMG_PREC_TC32 && tc_supported(shape))
+        return dense_bytes_aligned(shape) + (size_t)tc_layout(shape).total;
+    return 0;
 }
 
 int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, void *packed,
@@ -267,13 +275,33 @@ int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, voi
     return model_pack(shape, dense_raw, packed, as_stream(stream));
 }
 
+int recmg_model_pack_tc(const recmg_model_shape *shape, const float *dense_raw,
+                        const float *embed_id, void *packed, void *stream) {
+    if (!tc_supported(shape) || !dense_raw || !embed_id || !packed) return RECMG_E_INVALID_CONFIG;
+    return model_pack_tc(shape, dense_raw, embed_id, packed,
+                         (char *)packed + dense_bytes_aligned(shape), as_stream(stream));
+}
+
+size_t recmg_model_workspace_bytes(const recmg_model_shape *shape, int32_t precision,
+                                   int64_t batch) {
+    if (precision == RECMG_PREC_TC32 && tc_supported(shape)) return tc_workspace_bytes(shape, batch);
+    return 0;
+}
+
 int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
                         const float *embed_id, const void *packed, const int32_t *gid,
                         const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
-                        int32_t *pf_gid, void *stream) {
-    if (!shape_ok(shape) || precision != RECMG_PREC_FP32 || batch < 0 || !logits)
-        return RECMG_E_INVALID_CONFIG;
-    if (batch > 0 && (!embed_id || !packed || !gid || !tid)) return RECMG_E_INVALID_CONFIG;
+                        int32_t *pf_gid, void *ws, size_t ws_bytes, void *stream) {
+    if (!shape_ok(shape) || batch < 0 || !logits) return RECMG_E_INVALID_CONFIG;
+    if (batch > 0 && (!packed || !gid || !tid)) return RECMG_E_INVALID_CONFIG;
+    if (precision == RECMG_PREC_TC32) {
+        if (!tc_supported(shape)) return RECMG_E_INVALID_CONFIG;
+        return model_forward_tc(shape, packed, (const char *)packed + dense_bytes_aligned(shape),
+                                gid, tid, batch, logits, bits, pf_gid, ws, ws_bytes,
+                                as_stream(stream));
+    }
+    if (precision != RECMG_PREC_FP32) return RECMG_E_INVALID_CONFIG;
+    if (batch > 0 && !embed_id) return RECMG_E_INVALID_CONFIG;
     return model_forward_fp32(shape, embed_id, packed, gid, tid, batch, logits, bits, pf_gid,
                               as_stream(stream));
 }

@@ -1,0 +1,767 @@
+// K1 / K2 on the 5th-gen tensor cores: fp32-parity LSTM + attention forwards
+// with every GEMM on tcgen05 (kind::f16, fp32 accumulation in TMEM).
+//
+// Precision: each GEMM is the 3-product split x*w ~= xh*wh + xh*wl + xl*wh
+// with xh = fp16(x), xl = fp16(x - xh) (same for w), accumulated in fp32;
+// that is ~22 significant bits per product, i.e. fp32-class logits (the
+// 1e-3 parity bar; tests/test_gpu_model.py).  Elementwise math stays fp32.
+//
+// Tile = 128 chunks = 128 TMEM lanes; 256 threads: warp w serves TMEM lane
+// quadrant (w & 3) and hidden units [32*(w>>2), +32), so every chunk row is
+// owned by two threads.  TMEM (512 columns):
+//   [0,256)   Z   gate pre-activations, gate-interleaved (col 4j+g)
+//   [256,320) Q   attention query / enc_pre of the previous step
+//   [320,384) C   comb accumulator (caching) / h1 operand (prefetch)
+//   [384,512) A   fp16 hi|lo operands (h, ctx / h0, ctx)
+// Weights live in shared memory as fp16 hi/lo B images in the no-swizzle
+// K-major core-matrix layout (umma.cuh), loaded per phase.  The layer-0
+// token projection x_t @ Wx + b is folded into per-id tables at pack time
+// (Pid = E_id @ Wx[:d], Ptab = E_tab @ Wx[d:2d] + b), so z starts as
+// Pid[gid] + Ptab[tid] written into Z with tcgen05.st.
+// Encoder states H_t and enc_pre_t = H_t @ att_enc go to a per-CTA L2
+// scratch for the attention of every decoder step (model.py:115-124).
+#include <vector>
+
+#include "lstm.cuh"
+#include "lstm_tc.cuh"
+#include "model_layout.cuh"
+#include "umma.cuh"
+
+namespace recmg {
+
+namespace {
+
+constexpr int kThreadsTC = 256;
+constexpr uint32_t COL_Z = 0, COL_Q = 256, COL_C = 320, COL_A = 384;
+// A operand sub-regions (32 columns = 64 fp16 each)
+constexpr uint32_t A_H_HI = COL_A + 0, A_H_LO = COL_A + 32, A_X_HI = COL_A + 64,
+                   A_X_LO = COL_A + 96;                  // caching: h, ctx
+constexpr uint32_t P_H0_HI = COL_A + 0, P_H0_LO = COL_A + 32, P_CTX_HI = COL_A + 64,
+                   P_CTX_LO = COL_A + 96, P_H1_HI = COL_C, P_H1_LO = COL_C + 32;  // prefetch
+
+__device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float ftanh(float x) {
+    return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
+}
+
+struct TcArgs {
+    recmg_model_shape m;
+    TcLayout tl;
+    PackedLayout pl;
+    const uint8_t *blob;   // TC blob (B images + P tables)
+    const float *dense;    // fp32 packed blob (biases, att_v, comb, head, slot_proj)
+    const int32_t *gid, *tid;
+    int64_t batch;
+    float *logits;
+    uint8_t *bits;
+    int32_t *pf_gid;
+    float *scratch;        // [gridDim.x][2][L][128][64]
+};
+
+// ---- per-thread helpers ------------------------------------------------------
+struct Ctx {
+    int tid, warp, lane, quad, half, row;
+    uint32_t tbase, lane_addr;  // tmem base, + lane quadrant
+};
+
+// all 256 threads: copy a phase's B images (bytes [off, off+len) of the blob) to smem
+__device__ __forceinline__ void load_phase(uint8_t *smem, const uint8_t *blob, int64_t off,
+                                           int64_t len, int tid) {
+    const int4 *src = reinterpret_cast<const int4 *>(blob + off);
+    int4 *dst = reinterpret_cast<int4 *>(smem);
+    for (int64_t i = tid; i < len / 16; i += kThreadsTC) dst[i] = __ldg(src + i);
+    umma::fence_proxy_async();
+    __syncthreads();
+}
+
+// the three split products for one B matrix: d (+)= a * b, K = 64 (4 k-steps)
+__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_saddr,
+                                     int N, bool acc) {
+    const uint32_t idesc = umma::idesc_f16(128, N);
+    const uint32_t lo_off = (uint32_t)N * 128u;  // hi image N*64*2 bytes, lo follows
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++)
+        umma::mma_ts(d, a_hi + 8 * ks, umma::make_desc(b_saddr + 256 * ks, 128, 1024), idesc,
+                     (acc || ks > 0) ? 1u : 0u);
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++)
+        umma::mma_ts(d, a_hi + 8 * ks, umma::make_desc(b_saddr + lo_off + 256 * ks, 128, 1024),
+                     idesc, 1u);
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++)
+        umma::mma_ts(d, a_lo + 8 * ks, umma::make_desc(b_saddr + 256 * ks, 128, 1024), idesc, 1u);
+}
+
+// sync point after threads wrote TMEM operands / before the MMA issue
+__device__ __forceinline__ void tmem_writes_done() {
+    umma::tmem_st_wait();
+    umma::fence_before();
+    __syncthreads();
+}
+
+__device__ __forceinline__ void wait_mma(uint64_t *mbar, uint32_t &phase) {
+    umma::mbar_wait(mbar, phase);
+    phase ^= 1u;
+    umma::fence_after();
+}
+
+// write 32 fp32 values (this thread's hidden units) as fp16 hi|lo into an A region
+__device__ __forceinline__ void store_operand(const Ctx &c, uint32_t col_hi, uint32_t col_lo,
+                                              const float (&v)[32]) {
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int m = 0; m < 16; m++) {
+        const __half2 h = __floats2half2_rn(v[2 * m], v[2 * m + 1]);
+        const float2 hf = __half22float2(h);
+        hi[m] = *reinterpret_cast<const uint32_t *>(&h);
+        lo[m] = umma::pack_half2(v[2 * m] - hf.x, v[2 * m + 1] - hf.y);
+    }
+    umma::tmem_st16(c.lane_addr + col_hi + 16 * c.half, hi);
+    umma::tmem_st16(c.lane_addr + col_lo + 16 * c.half, lo);
+}
+
+__device__ __forceinline__ void zero_operand(const Ctx &c, uint32_t col_hi, uint32_t col_lo) {
+    uint32_t z[16];
+#pragma unroll
+    for (int m = 0; m < 16; m++) z[m] = 0u;
+    umma::tmem_st16(c.lane_addr + col_hi + 16 * c.half, z);
+    umma::tmem_st16(c.lane_addr + col_lo + 16 * c.half, z);
+}
+
+// Z[my 128 columns] = Pid[g] + Ptab[t]  (layer-0 token projection + bias)
+__device__ __forceinline__ void init_z_from_tables(const Ctx &c, const float *pid,
+                                                   const float *ptab, int32_t g, int32_t tb) {
+    const float4 *a = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + 128 * c.half);
+    const float4 *b = reinterpret_cast<const float4 *>(ptab + (int64_t)tb * 256 + 128 * c.half);
+#pragma unroll
+    for (int blk = 0; blk < 8; blk++) {
+        uint32_t r[16];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float4 x = __ldg(a + blk * 4 + q), y = __ldg(b + blk * 4 + q);
+            r[4 * q + 0] = __float_as_uint(x.x + y.x);
+            r[4 * q + 1] = __float_as_uint(x.y + y.y);
+            r[4 * q + 2] = __float_as_uint(x.z + y.z);
+            r[4 * q + 3] = __float_as_uint(x.w + y.w);
+        }
+        umma::tmem_st16(c.lane_addr + COL_Z + 128 * c.half + 16 * blk, r);
+    }
+}
+
+// Z[my 128 columns] = row (same for every chunk: prefetch slot projection)
+__device__ __forceinline__ void init_z_from_row(const Ctx &c, const float *rowp) {
+    const float4 *a = reinterpret_cast<const float4 *>(rowp + 128 * c.half);
+#pragma unroll
+    for (int blk = 0; blk < 8; blk++) {
+        uint32_t r[16];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float4 x = __ldg(a + blk * 4 + q);
+            r[4 * q + 0] = __float_as_uint(x.x);
+            r[4 * q + 1] = __float_as_uint(x.y);
+            r[4 * q + 2] = __float_as_uint(x.z);
+            r[4 * q + 3] = __float_as_uint(x.w);
+        }
+        umma::tmem_st16(c.lane_addr + COL_Z + 128 * c.half + 16 * blk, r);
+    }
+}
+
+// LSTM cell on this thread's 32 hidden units (model.py:103-112):
+// z (+ bias) -> i,f,g,o -> c, h
+template <bool BIAS>
+__device__ __forceinline__ void cell(const Ctx &c, const float *bias, float (&cs)[32],
+                                     float (&h)[32]) {
+    const float4 *b4 = reinterpret_cast<const float4 *>(bias) + 32 * c.half;
+#pragma unroll
+    for (int blk = 0; blk < 8; blk += 2) {
+        float z0[16], z1[16];
+        umma::tmem_ld16(c.lane_addr + COL_Z + 128 * c.half + 16 * blk, z0);
+        umma::tmem_ld16(c.lane_addr + COL_Z + 128 * c.half + 16 * (blk + 1), z1);
+        umma::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int j = 4 * blk + u;  // hidden unit within my 32
+            const float *z = (u < 4) ? &z0[4 * u] : &z1[4 * (u - 4)];
+            float zi = z[0], zf = z[1], zg = z[2], zo = z[3];
+            if (BIAS) {
+                const float4 bb = __ldg(b4 + j);
+                zi += bb.x; zf += bb.y; zg += bb.z; zo += bb.w;
+            }
+            const float ig = fsig(zi), fg = fsig(zf), gg = ftanh(zg), og = fsig(zo);
+            cs[j] = fg * cs[j] + ig * gg;
+            h[j] = og * ftanh(cs[j]);
+        }
+    }
+}
+
+// read 32 columns [col + 32*half, +32) of this thread's lane
+__device__ __forceinline__ void read32(const Ctx &c, uint32_t col, float (&v)[32]) {
+    float a[16], b[16];
+    umma::tmem_ld16(c.lane_addr + col + 32 * c.half, a);
+    umma::tmem_ld16(c.lane_addr + col + 32 * c.half + 16, b);
+    umma::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; i++) { v[i] = a[i]; v[16 + i] = b[i]; }
+}
+
+__device__ __forceinline__ void store32(float *dst, const float (&v)[32]) {
+    float4 *d = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+    for (int i = 0; i < 8; i++) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
+// partial attention scores over this thread's 32 units (model.py:118-119)
+__device__ __forceinline__ void attn_scores(const Ctx &c, const float *Es, int npos,
+                                            const float (&q)[32], const float (&v)[32],
+                                            float *s_part, int L) {
+    for (int j = 0; j < npos; j++) {
+        const float4 *e = reinterpret_cast<const float4 *>(Es + ((int64_t)j * 128 + c.row) * 64 +
+                                                            32 * c.half);
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const float4 x = e[i];
+            s += v[4 * i + 0] * ftanh(x.x + q[4 * i + 0]);
+            s += v[4 * i + 1] * ftanh(x.y + q[4 * i + 1]);
+            s += v[4 * i + 2] * ftanh(x.z + q[4 * i + 2]);
+            s += v[4 * i + 3] * ftanh(x.w + q[4 * i + 3]);
+        }
+        s_part[(c.half * L + j) * 128 + c.row] = s;
+    }
+}
+
+// softmax over positions + context on this thread's 32 units (model.py:120-123)
+__device__ __forceinline__ void attn_context(const Ctx &c, const float *Hs, int npos,
+                                             const float *s_part, int L, float (&ctx)[32]) {
+    float mx = -INFINITY;
+    for (int j = 0; j < npos; j++)
+        mx = fmaxf(mx, s_part[j * 128 + c.row] + s_part[(L + j) * 128 + c.row]);
+#pragma unroll
+    for (int k = 0; k < 32; k++) ctx[k] = 0.0f;
+    float sum = 0.0f;
+    for (int j = 0; j < npos; j++) {
+        const float e = __expf(s_part[j * 128 + c.row] + s_part[(L + j) * 128 + c.row] - mx);
+        sum += e;
+        const float4 *hp = reinterpret_cast<const float4 *>(Hs + ((int64_t)j * 128 + c.row) * 64 +
+                                                             32 * c.half);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const float4 x = hp[i];
+            ctx[4 * i + 0] += e * x.x;
+            ctx[4 * i + 1] += e * x.y;
+            ctx[4 * i + 2] += e * x.z;
+            ctx[4 * i + 3] += e * x.w;
+        }
+    }
+    const float inv = __fdividef(1.0f, sum);
+#pragma unroll
+    for (int k = 0; k < 32; k++) ctx[k] *= inv;
+}
+
+// partial head: sum_k tanh(comb_k + b_k) * w_k over my 32 units (model.py:177-179)
+__device__ __forceinline__ float head_partial(const Ctx &c, uint32_t col, const float *comb_b,
+                                              const float *head_w) {
+    float v[32];
+    read32(c, col, v);
+    float s = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 32; k++)
+        s += ftanh(v[k] + __ldg(comb_b + 32 * c.half + k)) * __ldg(head_w + 32 * c.half + k);
+    return s;
+}
+
+__device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T, int t, float s,
+                                           bool caching) {
+    if (chunk >= a.batch) return;
+    a.logits[chunk * T + t] = s;
+    if (caching) {
+        if (a.bits) a.bits[chunk * T + t] = s >= 0.0f ? 1 : 0;   // runtime.py:192
+    } else if (a.pf_gid) {
+        const double po = 1.0 / (1.0 + exp(-(double)s));          // model.py:250-258
+        const int64_t V = a.m.total_ids;
+        double gg = floor(po * (double)(V - 1) + 0.5);
+        gg = fmin(fmax(gg, 0.0), (double)(V - 1));
+        a.pf_gid[chunk * T + t] = (int32_t)gg;
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_s;
+    __shared__ float lpart[2][128];
+    const bool caching = (KIND == RECMG_MODEL_CACHING);
+    const int L = a.m.l_in;
+    const int T = caching ? L : a.m.l_out;
+    float *s_part = reinterpret_cast<float *>(smem + a.tl.spart_off);
+
+    Ctx c;
+    c.tid = threadIdx.x;
+    c.warp = c.tid >> 5;
+    c.lane = c.tid & 31;
+    c.quad = c.warp & 3;
+    c.half = c.warp >> 2;
+    c.row = 32 * c.quad + c.lane;
+    if (c.tid == 0) umma::mbar_init(&mbar, 1);
+    if (c.warp == 0) umma::tmem_alloc<512>(&tmem_base_s);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    c.tbase = tmem_base_s;
+    c.lane_addr = c.tbase + ((uint32_t)(32 * c.quad) << 16);
+    uint32_t phase = 0;
+    const uint32_t sbase = umma::smem_u32(smem);
+    const TcLayout &tl = a.tl;
+    const PackedLayout &pl = a.pl;
+    const float *pid_enc = reinterpret_cast<const float *>(a.blob + tl.pid[0]);
+    const float *ptab_enc = reinterpret_cast<const float *>(a.blob + tl.ptab[0]);
+    const float *pid_dec = reinterpret_cast<const float *>(a.blob + tl.pid[1]);
+    const float *ptab_dec = reinterpret_cast<const float *>(a.blob + tl.ptab[1]);
+    float *Hs = a.scratch + (int64_t)blockIdx.x * 2 * L * 128 * 64;
+    float *Es = Hs + (int64_t)L * 128 * 64;
+    const float *att_v = a.dense + pl.att_v;
+    const float *comb_b = a.dense + pl.comb_b;
+    const float *head_w = a.dense + pl.head_w;
+    const float head_b = __ldg(a.dense + pl.head_b);
+    const int64_t n_tiles = (a.batch + 127) / 128;
+
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t chunk = tile * 128 + c.row;
+        const int64_t crow = chunk < a.batch ? chunk : a.batch - 1;  // clamp pad rows
+        const int32_t *gid = a.gid + crow * L;
+        const int32_t *tidp = a.tid + crow * L;
+        float cs0[32], cs1[32], h[32];
+
+        // ====================== encoder (model.py:131-145) ======================
+        load_phase(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid);
+#pragma unroll
+        for (int k = 0; k < 32; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
+        if (caching) {
+            zero_operand(c, A_H_HI, A_H_LO);
+        } else {
+            zero_operand(c, P_H0_HI, P_H0_LO);
+            zero_operand(c, P_H1_HI, P_H1_LO);
+        }
+        for (int t = 0; t <= L; t++) {
+            const bool last = (t == L);   // t == L: only enc_pre of the last state
+            if (!last) init_z_from_tables(c, pid_enc, ptab_enc, __ldg(gid + t), __ldg(tidp + t));
+            tmem_writes_done();
+            if (caching) {
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    if (!last) mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                                    sbase + tl.b_off[0], 256, true);      // Z += h Wh
+                    mma3(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                         sbase + tl.b_off[1], 64, false);                  // Q = h att_enc
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                if (t >= 1) {
+                    float ep[32];
+                    read32(c, COL_Q, ep);
+                    store32(Es + ((int64_t)(t - 1) * 128 + c.row) * 64 + 32 * c.half, ep);
+                }
+                if (!last) {
+                    cell<false>(c, nullptr, cs0, h);
+                    store_operand(c, A_H_HI, A_H_LO, h);
+                    store32(Hs + ((int64_t)t * 128 + c.row) * 64 + 32 * c.half, h);
+                }
+            } else {
+                if (!last) {
+                    // layer 0: Z = Pid + Ptab + h0 Wh0
+                    if (c.tid == 0) {
+                        umma::fence_after();
+                        mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                             sbase + tl.b_off[0], 256, true);
+                        umma::commit(&mbar);
+                    }
+                    wait_mma(&mbar, phase);
+                    cell<false>(c, nullptr, cs0, h);
+                    store_operand(c, P_H0_HI, P_H0_LO, h);
+                    tmem_writes_done();
+                }
+                // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell); Q = h1(t-1) att_enc
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    if (!last) {
+                        mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                             sbase + tl.b_off[1], 256, false);
+                        mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                             sbase + tl.b_off[2], 256, true);
+                    }
+                    mma3(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                         sbase + tl.b_off[3], 64, false);
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                if (t >= 1) {
+                    float ep[32];
+                    read32(c, COL_Q, ep);
+                    store32(Es + ((int64_t)(t - 1) * 128 + c.row) * 64 + 32 * c.half, ep);
+                }
+                if (!last) {
+                    cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
+                    store_operand(c, P_H1_HI, P_H1_LO, h);
+                    store32(Hs + ((int64_t)t * 128 + c.row) * 64 + 32 * c.half, h);
+                }
+            }
+        }
+        __syncthreads();  // H / enc_pre scratch complete (block-visible via L1/L2)
+
+        // ====================== decoder (model.py:156-181) ======================
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 32; k++) { v[k] = __ldg(att_v + 32 * c.half + k); cs0[k] = 0.0f; cs1[k] = 0.0f; }
+        load_phase(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
+        if (caching) {
+            zero_operand(c, A_H_HI, A_H_LO);
+            zero_operand(c, A_X_HI, A_X_LO);
+            for (int t = 0; t <= T; t++) {
+                const bool last = (t == T);   // t == T: only finish comb_{T-1}
+                if (!last) init_z_from_tables(c, pid_dec, ptab_dec, __ldg(gid + t), __ldg(tidp + t));
+                tmem_writes_done();
+                // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    if (!last) {
+                        mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                             sbase + tl.b_off[2], 256, true);
+                        mma3(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                             sbase + tl.b_off[3], 64, false);
+                    }
+                    if (t >= 1)
+                        mma3(c.tbase + COL_C, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                             sbase + tl.b_off[4], 64, true);
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                if (t >= 1) lpart[c.half][c.row] = head_partial(c, COL_C, comb_b, head_w);
+                if (!last) {
+                    float q[32];
+                    read32(c, COL_Q, q);
+                    attn_scores(c, Es, t + 1, q, v, s_part, L);   // causal: j <= t
+                }
+                __syncthreads();
+                if (t >= 1 && c.half == 0)
+                    emit_logit(a, chunk, T, t - 1, lpart[0][c.row] + lpart[1][c.row] + head_b, true);
+                if (last) break;
+                float ctx[32];
+                attn_context(c, Hs, t + 1, s_part, L, ctx);
+                store_operand(c, A_X_HI, A_X_LO, ctx);
+                tmem_writes_done();
+                // GEMM2 on ctx_t: Z += ctx Wc ; C = ctx Wcomb_c
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    mma3(c.tbase + COL_Z, c.tbase + A_X_HI, c.tbase + A_X_LO,
+                         sbase + tl.b_off[5], 256, true);
+                    mma3(c.tbase + COL_C, c.tbase + A_X_HI, c.tbase + A_X_LO,
+                         sbase + tl.b_off[6], 64, false);
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                cell<false>(c, nullptr, cs0, h);
+                store_operand(c, A_H_HI, A_H_LO, h);
+            }
+        } else {
+            zero_operand(c, P_H0_HI, P_H0_LO);
+            zero_operand(c, P_H1_HI, P_H1_LO);
+            zero_operand(c, P_CTX_HI, P_CTX_LO);
+            for (int t = 0; t <= T; t++) {
+                const bool last = (t == T);
+                // (DEC-A weights resident) Q = h1 att_dec ; Z[0:64) = h1 Wcomb_h + ctx Wcomb_c
+                tmem_writes_done();
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    if (!last)
+                        mma3(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                             sbase + tl.b_off[4], 64, false);
+                    if (t >= 1) {
+                        mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                             sbase + tl.b_off[5], 64, false);
+                        mma3(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
+                             sbase + tl.b_off[6], 64, true);
+                    }
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                if (t >= 1) lpart[c.half][c.row] = head_partial(c, COL_Z, comb_b, head_w);
+                if (!last) {
+                    float q[32];
+                    read32(c, COL_Q, q);
+                    attn_scores(c, Es, L, q, v, s_part, L);       // non-causal
+                }
+                __syncthreads();
+                if (t >= 1 && c.half == 0)
+                    emit_logit(a, chunk, T, t - 1, lpart[0][c.row] + lpart[1][c.row] + head_b, false);
+                if (last) break;
+                float ctx[32];
+                attn_context(c, Hs, L, s_part, L, ctx);
+                store_operand(c, P_CTX_HI, P_CTX_LO, ctx);
+                // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
+                init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
+                tmem_writes_done();
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    mma3(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
+                         sbase + tl.b_off[7], 256, true);
+                    mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                         sbase + tl.b_off[8], 256, true);
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                cell<false>(c, nullptr, cs0, h);
+                store_operand(c, P_H0_HI, P_H0_LO, h);
+                umma::tmem_st_wait();
+                // layer 1 (DEC-B weights): Z = h0 Wx1 + h1 Wh1 (+ b1)
+                load_phase(smem, a.blob, tl.phase_off[2], tl.phase_len[2], c.tid);
+                umma::fence_before();
+                __syncthreads();
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                         sbase + tl.b_off[9], 256, false);
+                    mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                         sbase + tl.b_off[10], 256, true);
+                    umma::commit(&mbar);
+                }
+                wait_mma(&mbar, phase);
+                cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
+                store_operand(c, P_H1_HI, P_H1_LO, h);
+                umma::tmem_st_wait();
+                load_phase(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
+            }
+        }
+        __syncthreads();
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (c.warp == 0) umma::tmem_free<512>(c.tbase);
+}
+
+// ---------------------------------------------------------------------------
+// packing: B images (fp16 hi/lo, core-matrix layout) and the folded token tables
+namespace {
+
+struct BSpec {
+    int64_t src;      // float offset in the raw blob of W[k0][0]
+    int64_t ld;       // row stride of W (floats)
+    int N;            // output columns
+    int gates;        // 1: B row n = 4j+g reads W column g*d+j ; 0: identity
+    int64_t dst;      // byte offset of the hi image in the TC blob
+};
+
+__global__ void bimage_kernel(const float *raw, uint8_t *out, BSpec s, int d) {
+    const int64_t total = (int64_t)s.N * 64;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(i / 64), k = (int)(i % 64);
+        const int col = s.gates ? ((n & 3) * d + (n >> 2)) : n;
+        const float w = raw[s.src + (int64_t)k * s.ld + col];
+        const __half hi = __float2half_rn(w);
+        const __half lo = __float2half_rn(w - __half2float(hi));
+        const uint32_t off = umma::kmajor_offset(n, k, 64);
+        *reinterpret_cast<__half *>(out + s.dst + off) = hi;
+        *reinterpret_cast<__half *>(out + s.dst + (int64_t)s.N * 128 + off) = lo;
+    }
+}
+
+// out[r][4j+g] = bias[g*d+j] + sum_k E[r][k] * W[k][g*d+j]   (fp32)
+__global__ void proj_table_kernel(const float *E, int64_t rows, int d, const float *W,
+                                  const float *bias, float *out) {
+    extern __shared__ float e_s[];  // [32][d]
+    const int n = threadIdx.x;       // 0..4d-1
+    const int j = n >> 2, g = n & 3;
+    const int col = g * d + j;
+    for (int64_t r0 = (int64_t)blockIdx.x * 32; r0 < rows; r0 += (int64_t)gridDim.x * 32) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 32 * d; i += blockDim.x) {
+            const int64_t r = r0 + i / d;
+            e_s[i] = r < rows ? E[r * d + (i % d)] : 0.0f;
+        }
+        __syncthreads();
+        float acc[32];
+        const float b = bias ? bias[col] : 0.0f;
+#pragma unroll
+        for (int q = 0; q < 32; q++) acc[q] = b;
+        for (int k = 0; k < d; k++) {
+            const float w = __ldg(W + (int64_t)k * 4 * d + col);
+#pragma unroll
+            for (int q = 0; q < 32; q++) acc[q] += e_s[q * d + k] * w;
+        }
+#pragma unroll
+        for (int q = 0; q < 32; q++)
+            if (r0 + q < rows) out[(r0 + q) * 4 * d + n] = acc[q];
+    }
+}
+
+}  // namespace
+
+bool tc_supported(const recmg_model_shape *m) {
+    return shape_ok(m) && m->dim == 64 && m->l_in <= 16 && m->l_out <= 16 &&
+           ((m->kind == RECMG_MODEL_CACHING && m->stacks == 1) ||
+            (m->kind == RECMG_MODEL_PREFETCH && m->stacks == 2));
+}
+
+TcLayout tc_layout(const recmg_model_shape *m) {
+    TcLayout t{};
+    const int64_t V = m->total_ids, T = m->n_tables;
+    int64_t o = 0;
+    auto img = [&](int N) { int64_t r = o; o += (int64_t)N * 256; return r; };  // hi+lo bytes
+    if (m->kind == RECMG_MODEL_CACHING) {
+        // ENC {Wh_e, att_enc} | DEC {Wh_d, att_dec, Wcomb_h, Wc_d, Wcomb_c}
+        t.phase_off[0] = o;
+        t.b_off[0] = img(256) - t.phase_off[0];
+        t.b_off[1] = img(64) - t.phase_off[0];
+        t.phase_len[0] = o - t.phase_off[0];
+        t.phase_off[1] = o;
+        t.b_off[2] = img(256) - t.phase_off[1];
+        t.b_off[3] = img(64) - t.phase_off[1];
+        t.b_off[4] = img(64) - t.phase_off[1];
+        t.b_off[5] = img(256) - t.phase_off[1];
+        t.b_off[6] = img(64) - t.phase_off[1];
+        t.phase_len[1] = o - t.phase_off[1];
+        t.nb = 7;
+    } else {
+        // ENC {Wh0, Wx1, Wh1, att_enc} | DEC-A {att_dec, Wcomb_h, Wcomb_c, Wctx0, Wh0}
+        // | DEC-B {Wx1, Wh1}
+        t.phase_off[0] = o;
+        t.b_off[0] = img(256) - t.phase_off[0];
+        t.b_off[1] = img(256) - t.phase_off[0];
+        t.b_off[2] = img(256) - t.phase_off[0];
+        t.b_off[3] = img(64) - t.phase_off[0];
+        t.phase_len[0] = o - t.phase_off[0];
+        t.phase_off[1] = o;
+        t.b_off[4] = img(64) - t.phase_off[1];
+        t.b_off[5] = img(64) - t.phase_off[1];
+        t.b_off[6] = img(64) - t.phase_off[1];
+        t.b_off[7] = img(256) - t.phase_off[1];
+        t.b_off[8] = img(256) - t.phase_off[1];
+        t.phase_len[1] = o - t.phase_off[1];
+        t.phase_off[2] = o;
+        t.b_off[9] = img(256) - t.phase_off[2];
+        t.b_off[10] = img(256) - t.phase_off[2];
+        t.phase_len[2] = o - t.phase_off[2];
+        t.nb = 11;
+    }
+    o = (o + 255) / 256 * 256;
+    const int ntab = m->kind == RECMG_MODEL_CACHING ? 2 : 1;
+    for (int i = 0; i < 2; i++) {
+        if (i < ntab) {
+            t.pid[i] = o; o += V * 256 * 4;
+            t.ptab[i] = o; o += T * 256 * 4;
+            o = (o + 255) / 256 * 256;
+        } else {
+            t.pid[i] = t.pid[0];
+            t.ptab[i] = t.ptab[0];
+        }
+    }
+    const size_t spart = (size_t)2 * m->l_in * 128 * 4;
+    t.spart_off = 176 * 1024;
+    size_t wmax = 0;
+    for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
+    t.smem_bytes = wmax > t.spart_off + spart ? wmax : t.spart_off + spart;
+    t.total = o;
+    return t;
+}
+
+int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *embed_id,
+                  void *packed_dense, void *tc_blob, cudaStream_t s) {
+    int rc = model_pack(m, raw, packed_dense, s);
+    if (rc) return rc;
+    const RawLayout r = raw_layout(m);
+    const TcLayout t = tc_layout(m);
+    const int d = m->dim;
+    uint8_t *out = (uint8_t *)tc_blob;
+    std::vector<BSpec> specs;
+    auto spec = [&](int phase, int b, int64_t src, int64_t ld, int N, int gates) {
+        BSpec x{src, ld, N, gates, t.phase_off[phase] + t.b_off[b]};
+        specs.push_back(x);
+    };
+    if (m->kind == RECMG_MODEL_CACHING) {
+        spec(0, 0, r.enc_wh[0], 4 * d, 256, 1);
+        spec(0, 1, r.att_enc, d, 64, 0);
+        spec(1, 2, r.dec_wh[0], 4 * d, 256, 1);
+        spec(1, 3, r.att_dec, d, 64, 0);
+        spec(1, 4, r.comb_w, d, 64, 0);                       // rows 0..d-1: h part
+        spec(1, 5, r.dec_wx[0] + 2 * d * 4 * d, 4 * d, 256, 1); // rows 2d..3d-1: ctx part
+        spec(1, 6, r.comb_w + d * d, d, 64, 0);               // rows d..2d-1: ctx part
+    } else {
+        spec(0, 0, r.enc_wh[0], 4 * d, 256, 1);
+        spec(0, 1, r.enc_wx[1], 4 * d, 256, 1);
+        spec(0, 2, r.enc_wh[1], 4 * d, 256, 1);
+        spec(0, 3, r.att_enc, d, 64, 0);
+        spec(1, 4, r.att_dec, d, 64, 0);
+        spec(1, 5, r.comb_w, d, 64, 0);
+        spec(1, 6, r.comb_w + d * d, d, 64, 0);
+        spec(1, 7, r.dec_wx[0] + 2 * d * 4 * d, 4 * d, 256, 1);
+        spec(1, 8, r.dec_wh[0], 4 * d, 256, 1);
+        spec(2, 9, r.dec_wx[1], 4 * d, 256, 1);
+        spec(2, 10, r.dec_wh[1], 4 * d, 256, 1);
+    }
+    for (const BSpec &x : specs) {
+        bimage_kernel<<<64, 256, 0, s>>>(raw, out, x, d);
+        RECMG_LAUNCH_CHECK();
+    }
+    // folded token tables: Pid = E_id @ Wx[0:d], Ptab = E_tab @ Wx[d:2d] + b
+    const int ntab = m->kind == RECMG_MODEL_CACHING ? 2 : 1;
+    for (int i = 0; i < ntab; i++) {
+        const int64_t wx = (i == 0) ? r.enc_wx[0] : r.dec_wx[0];
+        const int64_t bb = (i == 0) ? r.enc_b[0] : r.dec_b[0];
+        const int64_t blocks = imin64((m->total_ids + 31) / 32, 64 * kSmCount);
+        proj_table_kernel<<<(unsigned)blocks, 4 * d, 32 * d * 4, s>>>(
+            embed_id, m->total_ids, d, raw + wx, nullptr, (float *)(out + t.pid[i]));
+        RECMG_LAUNCH_CHECK();
+        proj_table_kernel<<<(unsigned)imin64((m->n_tables + 31) / 32, 64 * kSmCount), 4 * d,
+                            32 * d * 4, s>>>(raw + r.embed_table, m->n_tables, d,
+                                             raw + wx + (int64_t)d * 4 * d, raw + bb,
+                                             (float *)(out + t.ptab[i]));
+        RECMG_LAUNCH_CHECK();
+    }
+    return RECMG_OK;
+}
+
+int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
+                     const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
+                     uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s) {
+    if (batch <= 0) return RECMG_OK;
+    const int64_t n_tiles = (batch + 127) / 128;
+    const int grid = (int)imin64(n_tiles, kSmCount);
+    if (ws_bytes < tc_workspace_bytes(m, batch)) return RECMG_E_WORKSPACE;
+    TcArgs a;
+    a.m = *m;
+    a.tl = tc_layout(m);
+    a.pl = packed_layout(m);
+    a.blob = (const uint8_t *)tc_blob;
+    a.dense = (const float *)packed_dense;
+    a.gid = gid;
+    a.tid = tid;
+    a.batch = batch;
+    a.logits = logits;
+    a.bits = bits;
+    a.pf_gid = pf_gid;
+    a.scratch = (float *)ws;
+    const int smem = (int)a.tl.smem_bytes;
+    if (m->kind == RECMG_MODEL_CACHING) {
+        RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_CACHING>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        lstm_tc_kernel<RECMG_MODEL_CACHING><<<grid, kThreadsTC, smem, s>>>(a);
+    } else {
+        RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_PREFETCH>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        lstm_tc_kernel<RECMG_MODEL_PREFETCH><<<grid, kThreadsTC, smem, s>>>(a);
+    }
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+size_t tc_workspace_bytes(const recmg_model_shape *m, int64_t batch) {
+    const int64_t n_tiles = (batch + 127) / 128;
+    const int64_t grid = imin64(n_tiles > 0 ? n_tiles : 1, kSmCount);
+    return (size_t)grid * 2 * m->l_in * 128 * 64 * sizeof(float);
+}
+
+}  // namespace recmg

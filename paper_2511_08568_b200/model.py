@@ -116,13 +116,17 @@ def init_params_device(kind, table_sizes, dim=32, stacks=None, l_in=15, l_out=5,
 
 
 class DeviceModel:
-    """A model's weights resident in HBM in the kernel layout.
+    """A model's weights resident in HBM in a kernel layout.
 
-    embed_id is uploaded as fp32 [V, d]; every other array is cast to fp32,
-    concatenated in _shapes order and re-laid by ``recmg_model_pack``.
+    precision "tc32" (default when the shape allows: d = 64): every GEMM on
+    the tcgen05 tensor cores as the fp16 hi/lo 3-product split, fp32
+    accumulation (recmg_model_pack_tc / RECMG_PREC_TC32; csrc/lstm_tc.cu);
+    the layer-0 token projection is folded into per-id tables, so the
+    packed weights hold total_ids x 4d fp32 per projection.
+    precision "fp32": the SIMT kernel (csrc/lstm_simt.cu), any dim <= 64.
     """
 
-    def __init__(self, params: ModelParameters, embed_id=None):
+    def __init__(self, params: ModelParameters, embed_id=None, precision: str = "auto"):
         torch = _native.torch_cuda()
         L = _native.lib()
         self.params = params
@@ -135,6 +139,15 @@ class DeviceModel:
         if nf < 0:
             raise InvalidConfigError(f"unsupported model shape dim={params.dim} "
                                      f"stacks={params.stacks} l_in={params.l_in}")
+        tc_bytes = L.recmg_model_packed_bytes(ctypes.byref(self.shape), _native.PREC_TC32)
+        if precision == "auto":
+            precision = "tc32" if tc_bytes else "fp32"
+        if precision == "tc32" and not tc_bytes:
+            raise InvalidConfigError("tc32 needs dim 64, l_in/l_out <= 16 and the default stacks")
+        if precision not in ("tc32", "fp32"):
+            raise InvalidConfigError(f"unknown precision {precision!r}")
+        self.precision = precision
+        self.prec = _native.PREC_TC32 if precision == "tc32" else _native.PREC_FP32
         names = [n for n in _shapes(params.kind, params.total_ids, len(params.table_sizes),
                                     params.dim, params.stacks, params.l_out) if n != "embed_id"]
         raw = np.concatenate([np.asarray(params.arrays[n], dtype=np.float32).reshape(-1)
@@ -144,19 +157,34 @@ class DeviceModel:
         if embed_id is None:
             embed_id = torch.from_numpy(
                 np.ascontiguousarray(params.arrays["embed_id"], dtype=np.float32)).cuda()
-        self.embed_id = embed_id
         raw_d = torch.from_numpy(raw).cuda()
         self.packed = _native.device_bytes(
-            torch, L.recmg_model_packed_bytes(ctypes.byref(self.shape), _native.PREC_FP32))
-        _native.check(L.recmg_model_pack(ctypes.byref(self.shape), _native.ptr(raw_d),
-                                         _native.ptr(self.packed), _native.PREC_FP32,
-                                         _native.stream_handle(torch)), "model_pack")
+            torch, L.recmg_model_packed_bytes(ctypes.byref(self.shape), self.prec))
+        st = _native.stream_handle(torch)
+        if self.prec == _native.PREC_TC32:
+            _native.check(L.recmg_model_pack_tc(ctypes.byref(self.shape), _native.ptr(raw_d),
+                                                _native.ptr(embed_id), _native.ptr(self.packed),
+                                                st), "model_pack_tc")
+            self.embed_id = None            # folded into the packed tables
+        else:
+            _native.check(L.recmg_model_pack(ctypes.byref(self.shape), _native.ptr(raw_d),
+                                             _native.ptr(self.packed), _native.PREC_FP32, st),
+                          "model_pack")
+            self.embed_id = embed_id
         torch.cuda.current_stream().synchronize()
         self.offsets = torch.from_numpy(table_offsets(params.table_sizes)).cuda()
+        self._ws = None
 
     @property
     def out_len(self):
         return self.params.l_in if self.kind == CACHING else self.params.l_out
+
+    def workspace(self, B):
+        torch = _native.torch_cuda()
+        need = _native.lib().recmg_model_workspace_bytes(ctypes.byref(self.shape), self.prec, B)
+        if need and (self._ws is None or self._ws.numel() < need):
+            self._ws = _native.device_bytes(torch, need)
+        return self._ws
 
     def forward(self, gid, tid, logits=None, bits=None, pf_gid=None):
         """gid/tid: device int32 [B, l_in].  Returns logits [B, out_len] fp32."""
@@ -164,11 +192,12 @@ class DeviceModel:
         B = gid.shape[0]
         if logits is None:
             logits = torch.empty((B, self.out_len), dtype=torch.float32, device="cuda")
+        ws = self.workspace(B)
         _native.check(_native.lib().recmg_model_forward(
-            ctypes.byref(self.shape), _native.PREC_FP32, _native.ptr(self.embed_id),
+            ctypes.byref(self.shape), self.prec, _native.ptr(self.embed_id),
             _native.ptr(self.packed), _native.ptr(gid), _native.ptr(tid), B,
-            _native.ptr(logits), _native.ptr(bits), _native.ptr(pf_gid),
-            _native.stream_handle(torch)), "model_forward")
+            _native.ptr(logits), _native.ptr(bits), _native.ptr(pf_gid), _native.ptr(ws),
+            ws.numel() if ws is not None else 0, _native.stream_handle(torch)), "model_forward")
         return logits
 
     def table_ids(self, gid):
@@ -192,7 +221,7 @@ class ForwardResult:
         return self.value.shape
 
 
-def _forward_batch(params, gid, tid, kind):
+def _forward_batch(params, gid, tid, kind, precision="auto"):
     if params.kind != kind:
         raise InvalidConfigError(f"forward_{kind} needs a {kind} model")
     torch = _native.torch_cuda()
@@ -207,21 +236,21 @@ def _forward_batch(params, gid, tid, kind):
         raise IndexError("embedding id outside embed_id")          # numpy fancy-index error
     if tid.size and (tid.min() < 0 or tid.max() >= len(params.table_sizes)):
         raise IndexError("table id outside embed_table")
-    dm = DeviceModel(params)
+    dm = DeviceModel(params, precision=precision)
     g = torch.from_numpy(np.ascontiguousarray(gid, dtype=np.int32)).cuda()
     t = torch.from_numpy(np.ascontiguousarray(tid, dtype=np.int32)).cuda()
     logits = dm.forward(g, t)
     return ForwardResult(logits.cpu().numpy())
 
 
-def forward_caching_batch(params, gid, tid) -> ForwardResult:
+def forward_caching_batch(params, gid, tid, precision="auto") -> ForwardResult:
     """model.py:184-196 on the GPU."""
-    return _forward_batch(params, gid, tid, CACHING)
+    return _forward_batch(params, gid, tid, CACHING, precision)
 
 
-def forward_prefetch_batch(params, gid, tid) -> ForwardResult:
+def forward_prefetch_batch(params, gid, tid, precision="auto") -> ForwardResult:
     """model.py:199-212 on the GPU."""
-    return _forward_batch(params, gid, tid, PREFETCH)
+    return _forward_batch(params, gid, tid, PREFETCH, precision)
 
 
 def _check_inputs(params, inputs):

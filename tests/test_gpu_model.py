@@ -35,17 +35,18 @@ def test_models_vs_reference_fixture():
         assert np.abs(res.value - probs).max() < 1e-5
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tc32"])
 @pytest.mark.parametrize("scale", [0.08, 0.4, 0.6])
-def test_config1_shapes_vs_oracle(scale):
-    """d = 64, config-1 layout, 512 chunks of a config-1 style trace."""
-    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 512 * 15 + 30, 1.05, 0.4, 32, 0))
+def test_config1_shapes_vs_oracle(scale, precision):
+    """d = 64, config-1 layout, 300 chunks (a ragged tile) of a config-1 style trace."""
+    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 300 * 15 + 30, 1.05, 0.4, 32, 0))
     K = rb.num_chunks(len(t))
     gid = t.gid_array[:K * 15].reshape(K, 15)
     tid = t.table_ids[:K * 15].reshape(K, 15)
     cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=scale)
     pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=scale)
-    lc = rb.forward_caching_batch(cp, gid, tid).logits
-    lp = rb.forward_prefetch_batch(pp, gid, tid).logits
+    lc = rb.forward_caching_batch(cp, gid, tid, precision).logits
+    lp = rb.forward_prefetch_batch(pp, gid, tid, precision).logits
     rc = mo.caching_logits(cp.arrays, 64, 1, gid, tid)
     rp = mo.prefetch_logits(pp.arrays, 64, 2, 5, gid, tid)
     _check(lc, rc)
