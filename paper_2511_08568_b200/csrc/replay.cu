@@ -145,6 +145,57 @@ __device__ __forceinline__ void flush_counters(recmg_counters *ctr, unsigned lon
 }
 
 // ---------------------------------------------------------------------------
+// Per-warp shared-memory ring over one set's event segment, filled with
+// cp.async: 4 slots x 256 events, up to 4 blocks in flight, so the serial
+// consumer reads every window from shared memory instead of paying an L2/DRAM
+// round trip per 32-event batch (the replay of the hottest set is a single
+// dependency chain).
+constexpr int kRingBlk = 256;
+constexpr int kRingSlots = 4;
+
+struct EventRing {
+    uint32_t *buf;       // [kRingSlots * kRingBlk] shared
+    const uint32_t *ev;  // global segment base (= ev + lo)
+    int64_t n;           // segment length
+    int64_t nblk, issued;
+    int lane;
+
+    __device__ __forceinline__ void issue_next() {
+        const int64_t k = issued;
+        const uint32_t *src = ev + k * kRingBlk;
+        uint32_t *dst = buf + (k % kRingSlots) * kRingBlk;
+        const int cnt = (int)imin64(kRingBlk, n - k * kRingBlk);
+        for (int i = lane; i < cnt; i += 32) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(dst + i)),
+                         "l"(src + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        issued++;
+    }
+    __device__ __forceinline__ void init(uint32_t *b, const uint32_t *e, int64_t len, int l) {
+        buf = b; ev = e; n = len; lane = l; issued = 0;
+        nblk = (len + kRingBlk - 1) / kRingBlk;
+        while (issued < nblk && issued < kRingSlots) issue_next();
+    }
+    // make events [r, r + cnt) (relative) readable; refill freed slots
+    __device__ __forceinline__ void ensure(int64_t r, int cnt) {
+        const int64_t k0 = r / kRingBlk;
+        while (issued < nblk && issued < k0 + kRingSlots) issue_next();
+        const int64_t k1 = (r + cnt - 1) / kRingBlk;
+        const int64_t pending = issued - 1 - k1;   // groups allowed to stay in flight
+        if (pending <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else if (pending == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+        else asm volatile("cp.async.wait_group 3;" ::: "memory");
+        __syncwarp();
+    }
+    __device__ __forceinline__ uint32_t at(int64_t r) const {
+        return buf[((r / kRingBlk) % kRingSlots) * kRingBlk + (r % kRingBlk)];
+    }
+};
+
+// ---------------------------------------------------------------------------
 // Narrow sets: warp per set, W <= 32 ways in lanes.
 template <int POLICY, bool CLASS>
 __global__ void __launch_bounds__(kNarrowWarps * 32)
@@ -172,15 +223,14 @@ replay_narrow_kernel(ReplayArgs a) {
     seg_range(a, set, lo, hi);
     unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
 
+    __shared__ uint32_t ring_buf[kNarrowWarps][kRingSlots * kRingBlk];
+    EventRing ring;
+    ring.init(ring_buf[threadIdx.x >> 5], a.ev + lo, hi - lo, lane);
     for (int64_t pos = lo; pos < hi;) {
-        // keep ~1K events ahead warm in L1
-        if (((pos - lo) & 255) == 0) {
-            const uint32_t *pfa = a.ev + pos + 256 + lane * 8;
-            if (pfa < a.ev + hi) asm volatile("prefetch.global.L1 [%0];" ::"l"(pfa));
-        }
         const int nb = (int)imin64(32, hi - pos);
         const bool valid = lane < nb;
-        const uint32_t e = valid ? __ldg(a.ev + pos + lane) : 0u;
+        ring.ensure(pos - lo, nb);
+        const uint32_t e = valid ? ring.at(pos - lo + lane) : 0u;
         const int32_t g = (int32_t)ev_gid(e);
         const uint32_t ty = ev_type(e);
 
@@ -336,10 +386,14 @@ replay_wide_kernel(ReplayArgs a) {
     const unsigned lt = (1u << lane) - 1u;
     int64_t free_hint = 0;
 
+    __shared__ uint32_t ring_buf[kRingSlots * kRingBlk];
+    EventRing ring;
+    ring.init(ring_buf, a.ev + lo, hi - lo, lane);
     for (int64_t pos = lo; pos < hi;) {
         const int nb = (int)imin64(32, hi - pos);
         const bool valid = lane < nb;
-        const uint32_t e = valid ? __ldg(a.ev + pos + lane) : 0u;
+        ring.ensure(pos - lo, nb);
+        const uint32_t e = valid ? ring.at(pos - lo + lane) : 0u;
         const int32_t g = (int32_t)ev_gid(e);
         const uint32_t ty = ev_type(e);
         const bool real = valid && (uint32_t)g != kGidMask;
