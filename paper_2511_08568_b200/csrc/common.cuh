@@ -23,6 +23,7 @@ namespace recmg { void note_launch(); }
 namespace recmg {
 
 constexpr int kSmCount = 148;  // B200: 2 dies x 74 SMs
+constexpr int64_t kSmemMaxWays = 4096;  // sets up to this many ways replay in shared memory
 
 // Event word: [type:2][gid:30]
 enum : uint32_t { EV_SERVE = 0u, EV_UPD0 = 1u, EV_UPD1 = 2u, EV_PREFETCH = 3u };
@@ -48,7 +49,7 @@ __host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) {
 
 struct Geometry {
     int64_t S, W;  // sets, ways per set
-    bool wide;     // W > 32: CTA-per-set kernel with id->slot map
+    bool wide;     // W > kSmemMaxWays: global-memory ways + id->slot map
 };
 
 inline bool geometry_of(const recmg_buffer_cfg *cfg, Geometry *g) {
@@ -58,7 +59,7 @@ inline bool geometry_of(const recmg_buffer_cfg *cfg, Geometry *g) {
     if (cfg->ways > 0 && cfg->capacity % cfg->ways != 0) return false;
     g->S = cfg->ways > 0 ? cfg->capacity / cfg->ways : 1;
     g->W = cfg->ways > 0 ? cfg->ways : cfg->capacity;
-    g->wide = g->W > 32;
+    g->wide = g->W > kSmemMaxWays;
     return true;
 }
 

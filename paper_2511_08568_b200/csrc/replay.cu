@@ -196,105 +196,172 @@ struct EventRing {
 };
 
 // ---------------------------------------------------------------------------
-// Narrow sets: warp per set, W <= 32 ways in lanes.
+// Sets of up to kSmemMaxWays ways: one warp per set, the set's ways and an
+// open-addressing gid -> way hash index live in shared memory.  Per batch of
+// 32 events: one hash probe per lane (membership), one ballot for the first
+// residency-changing miss, __match_any_sync groups the hit-run by way and the
+// group leader applies the run's effect on its way (S: tag clear / hit
+// class, U/P: last write wins), then the miss is resolved serially.
+constexpr uint64_t kHtEmpty = ~0ull;
+
+struct SetView {
+    uint32_t *ring;
+    int32_t *tags;
+    int64_t *meta;
+    uint64_t *ht;
+    uint32_t hmask;
+    int hbits;
+};
+
+__device__ __forceinline__ uint32_t ht_home(uint32_t g, int bits) {
+    return (g * 0x9E3779B1u) >> (32 - bits);
+}
+
+__device__ __forceinline__ int ht_find(const SetView &v, uint32_t g) {
+    uint32_t p = ht_home(g, v.hbits);
+    while (true) {
+        const uint64_t x = v.ht[p];
+        if (x == kHtEmpty) return -1;
+        if ((uint32_t)(x >> 32) == g) return (int)(uint32_t)x;
+        p = (p + 1) & v.hmask;
+    }
+}
+
+__device__ __forceinline__ void ht_insert(const SetView &v, uint32_t g, uint32_t way) {
+    uint32_t p = ht_home(g, v.hbits);
+    while (v.ht[p] != kHtEmpty) p = (p + 1) & v.hmask;
+    v.ht[p] = ((uint64_t)g << 32) | way;
+}
+
+// linear-probing delete with backward shift (no tombstones)
+__device__ __forceinline__ void ht_erase(const SetView &v, uint32_t g) {
+    uint32_t i = ht_home(g, v.hbits);
+    while ((uint32_t)(v.ht[i] >> 32) != g) i = (i + 1) & v.hmask;
+    uint32_t j = i;
+    while (true) {
+        j = (j + 1) & v.hmask;
+        const uint64_t x = v.ht[j];
+        if (x == kHtEmpty) break;
+        const uint32_t k = ht_home((uint32_t)(x >> 32), v.hbits);
+        const bool stay = (i <= j) ? (i < k && k <= j) : (i < k || k <= j);
+        if (!stay) {
+            v.ht[i] = x;
+            i = j;
+        }
+    }
+    v.ht[i] = kHtEmpty;
+}
+
 template <int POLICY, bool CLASS>
-__global__ void __launch_bounds__(kNarrowWarps * 32)
-replay_narrow_kernel(ReplayArgs a) {
+__global__ void __launch_bounds__(256)
+replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes_per_warp) {
+    extern __shared__ __align__(16) uint8_t dsm[];
     const unsigned FULL = 0xFFFFFFFFu;
-    const int lane = threadIdx.x & 31;
-    const int64_t set = (int64_t)blockIdx.x * kNarrowWarps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t set = (int64_t)blockIdx.x * warps_per_cta + warp;
     if (set >= a.S) return;
     const int W = (int)a.W;
-    const unsigned wayMask = (W == 32) ? FULL : ((1u << W) - 1u);
     const int64_t sbase = set * a.W;
-
-    // way state in registers; lanes >= W hold -2 (never resident, never free)
-    int32_t tag = -2;
-    int64_t meta = 0;
-    if (lane < W) {
-        tag = a.st.tags[sbase + lane];
-        meta = a.st.meta[sbase + lane];
-    }
-    int32_t prio = (int32_t)(meta & 0xFFFFFFFF);
-    bool flag = (meta >> 32) & 1;
-    const int64_t clock_base = a.st.header[0];
+    uint8_t *base = dsm + (size_t)warp * bytes_per_warp;
+    SetView v;
+    v.ring = reinterpret_cast<uint32_t *>(base);
+    v.tags = reinterpret_cast<int32_t *>(base + kRingSlots * kRingBlk * 4);
+    v.meta = reinterpret_cast<int64_t *>(base + kRingSlots * kRingBlk * 4 + 4 * Wp);
+    v.ht = reinterpret_cast<uint64_t *>(base + kRingSlots * kRingBlk * 4 + 12 * Wp);
+    v.hbits = hbits;
+    v.hmask = (1u << hbits) - 1u;
 
     int64_t lo, hi;
     seg_range(a, set, lo, hi);
-    unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
-
-    __shared__ uint32_t ring_buf[kNarrowWarps][kRingSlots * kRingBlk];
     EventRing ring;
-    ring.init(ring_buf[threadIdx.x >> 5], a.ev + lo, hi - lo, lane);
+    ring.init(v.ring, a.ev + lo, hi - lo, lane);
+
+    for (uint32_t i = lane; i <= v.hmask; i += 32) v.ht[i] = kHtEmpty;
+    int cnt = 0;
+    for (int w = lane; w < Wp; w += 32) {
+        const int32_t t = w < W ? a.st.tags[sbase + w] : -2;
+        v.tags[w] = t;
+        v.meta[w] = w < W ? a.st.meta[sbase + w] : 0;
+        cnt += t >= 0;
+    }
+    __syncwarp();
+    for (int w = lane; w < W; w += 32) {
+        const int32_t t = v.tags[w];
+        if (t < 0) continue;
+        uint32_t p = ht_home((uint32_t)t, hbits);
+        const unsigned long long entry = ((unsigned long long)(uint32_t)t << 32) | (uint32_t)w;
+        while (atomicCAS((unsigned long long *)&v.ht[p], kHtEmpty, entry) != kHtEmpty)
+            p = (p + 1) & v.hmask;
+    }
+    int count = (int)__reduce_add_sync(FULL, (unsigned)cnt);
+    __syncwarp();
+    const int64_t clock_base = a.st.header[0];
+    unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    int64_t free_hint = 0;
+
     for (int64_t pos = lo; pos < hi;) {
         const int nb = (int)imin64(32, hi - pos);
         const bool valid = lane < nb;
         ring.ensure(pos - lo, nb);
         const uint32_t e = valid ? ring.at(pos - lo + lane) : 0u;
-        const int32_t g = (int32_t)ev_gid(e);
+        const uint32_t g = ev_gid(e);
         const uint32_t ty = ev_type(e);
-
-        // membership: event lanes learn their way; way lanes learn their events
-        int myway = -1;
-        unsigned myev = 0;
-#pragma unroll
-        for (int w = 0; w < 32; w++) {
-            const int32_t tw = __shfl_sync(FULL, tag, w);
-            const bool hit = valid && (g == tw);
-            const unsigned b = __ballot_sync(FULL, hit);
-            if (hit) myway = w;
-            if (lane == w) myev = b;
-        }
-        const bool member = myway >= 0;
+        const bool real = valid && g != kGidMask;   // kGidMask = empty prefetch slot
+        const int way = real ? ht_find(v, g) : -1;
+        const bool member = way >= 0;
         unsigned missmask;
-        const bool real = valid && (uint32_t)g != kGidMask;  // kGidMask = empty prefetch slot
         if (POLICY == RECMG_POLICY_PRIORITY)
             missmask = __ballot_sync(FULL, real && !member && (ty == EV_SERVE || ty == EV_PREFETCH));
         else
             missmask = __ballot_sync(FULL, real && !member);
         const int cut = missmask ? (__ffs(missmask) - 1) : nb;
-        const unsigned below = (cut >= 32) ? FULL : ((1u << cut) - 1u);
-
+        const bool inrun = member && lane < cut;
+        const unsigned peers = __match_any_sync(FULL, inrun ? (unsigned)way : (0x80000000u | lane));
+        const int leader = 31 - __clz(peers);
         if (POLICY == RECMG_POLICY_PRIORITY) {
-            const unsigned Smask = __ballot_sync(FULL, valid && ty == EV_SERVE);
-            const unsigned UPmask = __ballot_sync(FULL, valid && ty != EV_SERVE);
-            const unsigned U1mask = __ballot_sync(FULL, valid && ty == EV_UPD1);
-            const unsigned m = myev & below;
-            const unsigned sm = m & Smask;
-            const bool pf_first = (sm != 0) && flag;
-            if (sm) {
-                const unsigned c = __popc(sm);
-                if (flag) { ph += 1; ch += c - 1; flag = false; }
-                else ch += c;
-            }
-            const unsigned upm = m & UPmask;
-            if (upm) {
-                const int last = 31 - __clz(upm);
-                prio = a.es + (((U1mask >> last) & 1u) ? 1 : 0);
+            const unsigned Smask = __ballot_sync(FULL, inrun && ty == EV_SERVE);
+            const unsigned UPmask = __ballot_sync(FULL, inrun && ty != EV_SERVE);
+            const unsigned U1mask = __ballot_sync(FULL, inrun && ty == EV_UPD1);
+            bool flag0 = false;
+            if (inrun && lane == leader) {
+                const int64_t m0 = v.meta[way];
+                flag0 = (m0 >> 32) & 1;
+                const unsigned sp = peers & Smask, up = peers & UPmask;
+                int32_t pr = (int32_t)(m0 & 0xFFFFFFFF);
+                bool f = flag0;
+                if (sp) {
+                    const unsigned c = __popc(sp);
+                    if (f) { ph += 1; ch += c - 1; f = false; }
+                    else ch += c;
+                }
+                if (up) {
+                    const int last = 31 - __clz(up);
+                    pr = a.es + (((U1mask >> last) & 1u) ? 1 : 0);
+                }
+                if (sp || up) v.meta[way] = (int64_t)(uint32_t)pr | ((int64_t)f << 32);
             }
             if (CLASS) {
-                const int first_s = sm ? (__ffs(sm) - 1) : -1;
-                const int fs = __shfl_sync(FULL, first_s, member ? myway : 0);
-                const bool pff = __shfl_sync(FULL, pf_first, member ? myway : 0);
-                if (lane < cut && member && ty == EV_SERVE)
-                    write_class(a, pos + lane, (pff && fs == lane) ? 1 : 0);
+                const bool f0 = __shfl_sync(FULL, flag0, leader);
+                if (inrun && ty == EV_SERVE) {
+                    const bool first = ((peers & Smask) & lt) == 0;
+                    write_class(a, pos + lane, (f0 && first) ? 1 : 0);
+                }
             }
         } else {
-            const unsigned m = myev & below;
-            if (m) {
-                lhits += __popc(m);
-                meta = clock_base + pos + (31 - __clz(m));
+            if (inrun && lane == leader) {
+                v.meta[way] = clock_base + pos + leader;
+                lhits += __popc(peers);
             }
             if (a.per_access_hit && lane < cut)
                 a.per_access_hit[a.vals ? a.vals[pos + lane] : pos + lane] = 1;
         }
+        __syncwarp();
 
         if (cut < nb) {
-            // the first residency-changing event: resolve it serially
             const uint32_t ec = __shfl_sync(FULL, e, cut);
-            const int32_t gc = (int32_t)ev_gid(ec);
+            const uint32_t gc = ev_gid(ec);
             const uint32_t tc = ev_type(ec);
-            const unsigned resident = __ballot_sync(FULL, tag >= 0);
             if (POLICY == RECMG_POLICY_PRIORITY) {
                 if (tc == EV_SERVE) {
                     od++;
@@ -302,61 +369,84 @@ replay_narrow_kernel(ReplayArgs a) {
                 } else {
                     ins++;
                 }
-                if (__popc(resident) == W) {
-                    // populate(): argmin (priority, gid), age all p>0
-                    const unsigned key = (tag >= 0) ? (unsigned)prio : 0xFFFFFFFFu;
-                    const unsigned minp = __reduce_min_sync(FULL, key);
-                    const unsigned gk = (tag >= 0 && (unsigned)prio == minp) ? (unsigned)tag : 0xFFFFFFFFu;
-                    const unsigned ming = __reduce_min_sync(FULL, gk);
-                    if (tag >= 0 && prio > 0) prio--;
-                    if (tag >= 0 && (unsigned)tag == ming) { tag = -1; flag = false; }
-                    nev++;
-                }
-                const unsigned freem = __ballot_sync(FULL, tag == -1) & wayMask;
-                if (lane == __ffs(freem) - 1) {
-                    tag = gc;
-                    prio = a.es;
-                    flag = (tc == EV_PREFETCH);
-                }
             } else {
                 od++;
                 if (a.per_access_hit && lane == 0)
                     a.per_access_hit[a.vals ? a.vals[pos + cut] : pos + cut] = 0;
-                if (__popc(resident) == W) {
-                    // evict the least recently used way (unique clocks)
-                    const long long key = (tag >= 0) ? (long long)meta : LLONG_MAX;
-                    long long mn = key;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
-                    if (tag >= 0 && key == mn) tag = -1;
-                    nev++;
-                }
-                const unsigned freem = __ballot_sync(FULL, tag == -1) & wayMask;
-                if (lane == __ffs(freem) - 1) {
-                    tag = gc;
-                    meta = clock_base + pos + cut;
-                }
             }
+            int target;
+            if (count >= W) {
+                // populate(): victim = argmin (priority, gid) [LRU: min clock]
+                unsigned long long best = ~0ull;
+                int bslot = -1;
+                for (int w = lane; w < W; w += 32) {
+                    const int32_t t = v.tags[w];
+                    if (t < 0) continue;
+                    const int64_t m = v.meta[w];
+                    const unsigned long long key = (POLICY == RECMG_POLICY_PRIORITY)
+                        ? (((unsigned long long)(uint32_t)m << 32) | (uint32_t)t)
+                        : (unsigned long long)m;
+                    if (key < best) { best = key; bslot = w; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+                    const int os = __shfl_xor_sync(FULL, bslot, o);
+                    if (ob < best) { best = ob; bslot = os; }
+                }
+                if (POLICY == RECMG_POLICY_PRIORITY) {
+                    for (int w = lane; w < W; w += 32) {
+                        if (v.tags[w] < 0) continue;
+                        const int64_t m = v.meta[w];
+                        if ((int32_t)(m & 0xFFFFFFFF) > 0) v.meta[w] = m - 1;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    ht_erase(v, (uint32_t)v.tags[bslot]);
+                    v.tags[bslot] = -1;
+                }
+                count--;
+                nev++;
+                target = bslot;
+            } else {
+                // first free way at or after the hint (ways below it are occupied:
+                // inside a launch a way is only freed by an eviction, refilled at once)
+                int found = -1;
+                for (int64_t b = free_hint; b < Wp && found < 0; b += 32) {
+                    const int w = (int)b + lane;
+                    const unsigned fm = __ballot_sync(FULL, w < W && v.tags[w] == -1);
+                    if (fm) found = (int)b + __ffs(fm) - 1;
+                }
+                target = found;
+                free_hint = found + 1;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                v.tags[target] = (int32_t)gc;
+                v.meta[target] = (POLICY == RECMG_POLICY_PRIORITY)
+                    ? ((int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32))
+                    : (clock_base + pos + cut);
+                ht_insert(v, gc, (uint32_t)target);
+            }
+            count++;
+            __syncwarp();
             pos += cut + 1;
         } else {
             pos += nb;
         }
     }
 
-    // write back
-    if (lane < W) {
-        a.st.tags[sbase + lane] = tag;
-        if (POLICY == RECMG_POLICY_PRIORITY)
-            a.st.meta[sbase + lane] = (int64_t)(uint32_t)prio | ((int64_t)flag << 32);
-        else
-            a.st.meta[sbase + lane] = meta;
+    // write back the set
+    for (int w = lane; w < W; w += 32) {
+        a.st.tags[sbase + w] = v.tags[w];
+        a.st.meta[sbase + w] = v.meta[w];
     }
-    const unsigned occ = __popc(__ballot_sync(FULL, tag >= 0));
-    if (lane == 0) a.st.count[set] = (int32_t)occ;
+    if (lane == 0) a.st.count[set] = count;
     if (POLICY == RECMG_POLICY_PRIORITY) {
         ch = __reduce_add_sync(FULL, (unsigned)ch);
         ph = __reduce_add_sync(FULL, (unsigned)ph);
-        if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, occ);
+        if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
     } else {
         lhits = __reduce_add_sync(FULL, (unsigned)lhits);
         if (lane == 0 && a.hits_misses) {
@@ -367,7 +457,7 @@ replay_narrow_kernel(ReplayArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Wide sets: one warp per set, W > 32 ways in global memory.
+// Wide sets: one warp per set, W > kSmemMaxWays ways in global memory.
 template <int POLICY, bool CLASS>
 __global__ void __launch_bounds__(32)
 replay_wide_kernel(ReplayArgs a) {
@@ -646,15 +736,31 @@ __global__ void buffer_op_kernel(StateView st, int64_t S, int64_t W, int32_t op,
 // ---------------------------------------------------------------------------
 int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_t nsets,
                   cudaStream_t s) {
+    (void)narrow;
     if (nsets <= 0) return RECMG_OK;
-    if (narrow) {
-        unsigned grid = (unsigned)((nsets + kNarrowWarps - 1) / kNarrowWarps);
+    if (a.W <= kSmemMaxWays) {
+        const int Wp = (int)((a.W + 31) / 32 * 32);
+        int hbits = 6;
+        while ((1 << hbits) < (Wp <= 256 ? 4 * Wp : 2 * Wp)) hbits++;
+        const int bytes = kRingSlots * kRingBlk * 4 + 12 * Wp + 8 * (1 << hbits);
+        int wpc = 98304 / bytes;
+        wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
+        const size_t smem = (size_t)wpc * bytes;
+        const unsigned grid = (unsigned)((nsets + wpc - 1) / wpc);
+#define RECMG_SMEM_LAUNCH(P, C)                                                            \
+    do {                                                                                    \
+        RECMG_CUDA_TRY(cudaFuncSetAttribute(replay_smem_kernel<P, C>,                       \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                            (int)smem));                                    \
+        replay_smem_kernel<P, C><<<grid, 32 * wpc, smem, s>>>(a, wpc, Wp, hbits, bytes);    \
+    } while (0)
         if (policy == RECMG_POLICY_PRIORITY) {
-            if (cls) replay_narrow_kernel<RECMG_POLICY_PRIORITY, true><<<grid, kNarrowWarps * 32, 0, s>>>(a);
-            else replay_narrow_kernel<RECMG_POLICY_PRIORITY, false><<<grid, kNarrowWarps * 32, 0, s>>>(a);
+            if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, true);
+            else RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, false);
         } else {
-            replay_narrow_kernel<RECMG_POLICY_LRU, false><<<grid, kNarrowWarps * 32, 0, s>>>(a);
+            RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU, false);
         }
+#undef RECMG_SMEM_LAUNCH
     } else {
         if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) replay_wide_kernel<RECMG_POLICY_PRIORITY, true><<<(unsigned)nsets, 32, 0, s>>>(a);

@@ -4,7 +4,6 @@
 
 namespace recmg {
 
-constexpr int kNarrowWarps = 4;  // sets per CTA in the narrow kernel
 
 struct ReplayArgs;
 
