@@ -31,13 +31,17 @@ namespace recmg {
 
 namespace {
 
-constexpr int kThreadsTC = 256;
 constexpr uint32_t COL_Z = 0, COL_Q = 256, COL_C = 320, COL_A = 384;
 // A operand sub-regions (32 columns = 64 fp16 each)
 constexpr uint32_t A_H_HI = COL_A + 0, A_H_LO = COL_A + 32, A_X_HI = COL_A + 64,
                    A_X_LO = COL_A + 96;                  // caching: h, ctx
 constexpr uint32_t P_H0_HI = COL_A + 0, P_H0_LO = COL_A + 32, P_CTX_HI = COL_A + 64,
                    P_CTX_LO = COL_A + 96, P_H1_HI = COL_C, P_H1_LO = COL_C + 32;  // prefetch
+
+// threads per chunk row: the caching model runs 2 (256 threads, 32 hidden
+// units each), the prefetch model 4 (512 threads, 16 units each) -- measured
+template <int KIND> struct PartsOf { static constexpr int value = 2; };
+template <> struct PartsOf<RECMG_MODEL_PREFETCH> { static constexpr int value = 4; };
 
 __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float ftanh(float x) {
@@ -48,28 +52,33 @@ struct TcArgs {
     recmg_model_shape m;
     TcLayout tl;
     PackedLayout pl;
-    const uint8_t *blob;   // TC blob (B images + P tables)
+    const uint8_t *blob;   // TC blob (B images + folded tables)
     const float *dense;    // fp32 packed blob (biases, att_v, comb, head, slot_proj)
     const int32_t *gid, *tid;
     int64_t batch;
     float *logits;
     uint8_t *bits;
     int32_t *pf_gid;
-    float *scratch;        // [gridDim.x][2][L][128][64]
+    float *scratch;        // [gridDim.x][2][L][16][128] float4
 };
 
 // ---- per-thread helpers ------------------------------------------------------
+template <int PARTS>
 struct Ctx {
-    int tid, warp, lane, quad, half, row;
+    static constexpr int U = 64 / PARTS;       // hidden units per thread
+    static constexpr int NQ = U / 4;           // float4 per scratch position
+    static constexpr int NT = 128 * PARTS;     // threads
+    int tid, warp, lane, quad, part, row;
     uint32_t tbase, lane_addr;  // tmem base, + lane quadrant
 };
 
-// all 256 threads: copy a phase's B images (bytes [off, off+len) of the blob) to smem
+// all threads: copy a phase's B images (bytes [off, off+len) of the blob) to smem
+template <int NT>
 __device__ __forceinline__ void load_phase(uint8_t *smem, const uint8_t *blob, int64_t off,
                                            int64_t len, int tid) {
     const int4 *src = reinterpret_cast<const int4 *>(blob + off);
     int4 *dst = reinterpret_cast<int4 *>(smem);
-    for (int64_t i = tid; i < len / 16; i += kThreadsTC) dst[i] = __ldg(src + i);
+    for (int64_t i = tid; i < len / 16; i += NT) dst[i] = __ldg(src + i);
     umma::fence_proxy_async();
     __syncthreads();
 }
@@ -105,54 +114,75 @@ __device__ __forceinline__ void wait_mma(uint64_t *mbar, uint32_t &phase) {
     umma::fence_after();
 }
 
-// write 32 fp32 values (this thread's hidden units) as fp16 hi|lo into an A region
-__device__ __forceinline__ void store_operand(const Ctx &c, uint32_t col_hi, uint32_t col_lo,
-                                              const float (&v)[32]) {
-    uint32_t hi[16], lo[16];
+template <int N>
+__device__ __forceinline__ void st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
+    if constexpr (N == 16) umma::tmem_st16(taddr, r);
+    else umma::tmem_st8(taddr, r);
+}
+
+// this thread's U units as fp16 hi|lo into an A operand region (U/2 columns each)
+template <int PARTS>
+__device__ __forceinline__ void store_operand(const Ctx<PARTS> &c, uint32_t col_hi,
+                                              uint32_t col_lo, const float (&v)[Ctx<PARTS>::U]) {
+    constexpr int H = Ctx<PARTS>::U / 2;
+    uint32_t hi[H], lo[H];
 #pragma unroll
-    for (int m = 0; m < 16; m++) {
+    for (int m = 0; m < H; m++) {
         const __half2 h = __floats2half2_rn(v[2 * m], v[2 * m + 1]);
         const float2 hf = __half22float2(h);
         hi[m] = *reinterpret_cast<const uint32_t *>(&h);
         lo[m] = umma::pack_half2(v[2 * m] - hf.x, v[2 * m + 1] - hf.y);
     }
-    umma::tmem_st16(c.lane_addr + col_hi + 16 * c.half, hi);
-    umma::tmem_st16(c.lane_addr + col_lo + 16 * c.half, lo);
+    st_cols<H>(c.lane_addr + col_hi + H * c.part, hi);
+    st_cols<H>(c.lane_addr + col_lo + H * c.part, lo);
 }
 
-__device__ __forceinline__ void zero_operand(const Ctx &c, uint32_t col_hi, uint32_t col_lo) {
-    uint32_t z[16];
+template <int PARTS>
+__device__ __forceinline__ void zero_operand(const Ctx<PARTS> &c, uint32_t col_hi, uint32_t col_lo) {
+    constexpr int H = Ctx<PARTS>::U / 2;
+    uint32_t z[H];
 #pragma unroll
-    for (int m = 0; m < 16; m++) z[m] = 0u;
-    umma::tmem_st16(c.lane_addr + col_hi + 16 * c.half, z);
-    umma::tmem_st16(c.lane_addr + col_lo + 16 * c.half, z);
+    for (int m = 0; m < H; m++) z[m] = 0u;
+    st_cols<H>(c.lane_addr + col_hi + H * c.part, z);
+    st_cols<H>(c.lane_addr + col_lo + H * c.part, z);
 }
 
-// Z[my 128 columns] = Pid[g] + Ptab[t]  (layer-0 token projection + bias)
-__device__ __forceinline__ void init_z_from_tables(const Ctx &c, const float *pid,
+// Z[my 4U gate columns] = Pid[g] + Ptab[t]  (layer-0 token projection + bias)
+template <int PARTS>
+__device__ __forceinline__ void init_z_from_tables(const Ctx<PARTS> &c, const float *pid,
                                                    const float *ptab, int32_t g, int32_t tb) {
-    const float4 *a = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + 128 * c.half);
-    const float4 *b = reinterpret_cast<const float4 *>(ptab + (int64_t)tb * 256 + 128 * c.half);
+    constexpr int NC = 4 * Ctx<PARTS>::U;     // columns
+    const float4 *a = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + NC * c.part);
+    const float4 *b = reinterpret_cast<const float4 *>(ptab + (int64_t)tb * 256 + NC * c.part);
 #pragma unroll
-    for (int blk = 0; blk < 8; blk++) {
-        uint32_t r[16];
+    for (int half = 0; half < NC / 64; half++) {
+        float4 x[16];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const float4 x = __ldg(a + blk * 4 + q), y = __ldg(b + blk * 4 + q);
-            r[4 * q + 0] = __float_as_uint(x.x + y.x);
-            r[4 * q + 1] = __float_as_uint(x.y + y.y);
-            r[4 * q + 2] = __float_as_uint(x.z + y.z);
-            r[4 * q + 3] = __float_as_uint(x.w + y.w);
+        for (int q = 0; q < 16; q++) x[q] = __ldg(a + half * 16 + q);
+#pragma unroll
+        for (int blk = 0; blk < 4; blk++) {
+            uint32_t r[16];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const float4 y = __ldg(b + half * 16 + blk * 4 + q);
+                const float4 u = x[blk * 4 + q];
+                r[4 * q + 0] = __float_as_uint(u.x + y.x);
+                r[4 * q + 1] = __float_as_uint(u.y + y.y);
+                r[4 * q + 2] = __float_as_uint(u.z + y.z);
+                r[4 * q + 3] = __float_as_uint(u.w + y.w);
+            }
+            umma::tmem_st16(c.lane_addr + COL_Z + NC * c.part + 64 * half + 16 * blk, r);
         }
-        umma::tmem_st16(c.lane_addr + COL_Z + 128 * c.half + 16 * blk, r);
     }
 }
 
-// Z[my 128 columns] = row (same for every chunk: prefetch slot projection)
-__device__ __forceinline__ void init_z_from_row(const Ctx &c, const float *rowp) {
-    const float4 *a = reinterpret_cast<const float4 *>(rowp + 128 * c.half);
+// Z[my 4U columns] = row (same for every chunk: prefetch slot projection)
+template <int PARTS>
+__device__ __forceinline__ void init_z_from_row(const Ctx<PARTS> &c, const float *rowp) {
+    constexpr int NC = 4 * Ctx<PARTS>::U;
+    const float4 *a = reinterpret_cast<const float4 *>(rowp + NC * c.part);
 #pragma unroll
-    for (int blk = 0; blk < 8; blk++) {
+    for (int blk = 0; blk < NC / 16; blk++) {
         uint32_t r[16];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -162,25 +192,25 @@ __device__ __forceinline__ void init_z_from_row(const Ctx &c, const float *rowp)
             r[4 * q + 2] = __float_as_uint(x.z);
             r[4 * q + 3] = __float_as_uint(x.w);
         }
-        umma::tmem_st16(c.lane_addr + COL_Z + 128 * c.half + 16 * blk, r);
+        umma::tmem_st16(c.lane_addr + COL_Z + NC * c.part + 16 * blk, r);
     }
 }
 
-// LSTM cell on this thread's 32 hidden units (model.py:103-112):
-// z (+ bias) -> i,f,g,o -> c, h
-template <bool BIAS>
-__device__ __forceinline__ void cell(const Ctx &c, const float *bias, float (&cs)[32],
-                                     float (&h)[32]) {
-    const float4 *b4 = reinterpret_cast<const float4 *>(bias) + 32 * c.half;
+// LSTM cell on this thread's U hidden units (model.py:103-112)
+template <bool BIAS, int PARTS>
+__device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
+                                     float (&cs)[Ctx<PARTS>::U], float (&h)[Ctx<PARTS>::U]) {
+    constexpr int U = Ctx<PARTS>::U;
+    const float4 *b4 = reinterpret_cast<const float4 *>(bias) + U * c.part;
 #pragma unroll
-    for (int blk = 0; blk < 8; blk += 2) {
+    for (int blk = 0; blk < U / 4; blk += 2) {
         float z0[16], z1[16];
-        umma::tmem_ld16(c.lane_addr + COL_Z + 128 * c.half + 16 * blk, z0);
-        umma::tmem_ld16(c.lane_addr + COL_Z + 128 * c.half + 16 * (blk + 1), z1);
+        umma::tmem_ld16(c.lane_addr + COL_Z + 4 * U * c.part + 16 * blk, z0);
+        umma::tmem_ld16(c.lane_addr + COL_Z + 4 * U * c.part + 16 * (blk + 1), z1);
         umma::tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < 8; u++) {
-            const int j = 4 * blk + u;  // hidden unit within my 32
+            const int j = 4 * blk + u;
             const float *z = (u < 4) ? &z0[4 * u] : &z1[4 * (u - 4)];
             float zi = z[0], zf = z[1], zg = z[2], zo = z[3];
             if (BIAS) {
@@ -194,79 +224,141 @@ __device__ __forceinline__ void cell(const Ctx &c, const float *bias, float (&cs
     }
 }
 
-// read 32 columns [col + 32*half, +32) of this thread's lane
-__device__ __forceinline__ void read32(const Ctx &c, uint32_t col, float (&v)[32]) {
-    float a[16], b[16];
-    umma::tmem_ld16(c.lane_addr + col + 32 * c.half, a);
-    umma::tmem_ld16(c.lane_addr + col + 32 * c.half + 16, b);
+// U columns [col + U*part, +U) of this thread's lane
+template <int PARTS>
+__device__ __forceinline__ void readU(const Ctx<PARTS> &c, uint32_t col,
+                                      float (&v)[Ctx<PARTS>::U]) {
+    constexpr int U = Ctx<PARTS>::U;
+#pragma unroll
+    for (int k = 0; k < U / 16; k++) {
+        float t[16];
+        umma::tmem_ld16(c.lane_addr + col + U * c.part + 16 * k, t);
+#pragma unroll
+        for (int i = 0; i < 16; i++) v[16 * k + i] = t[i];
+    }
     umma::tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 16; i++) { v[i] = a[i]; v[16 + i] = b[i]; }
 }
 
-__device__ __forceinline__ void store32(float *dst, const float (&v)[32]) {
-    float4 *d = reinterpret_cast<float4 *>(dst);
-#pragma unroll
-    for (int i = 0; i < 8; i++) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+// scratch position j of this thread: NQ float4 at [(j*16 + NQ*part + u)*128 + row];
+// consecutive rows of a warp are consecutive float4 -> fully coalesced
+template <int PARTS>
+__device__ __forceinline__ float4 *scratch_at(float *base, const Ctx<PARTS> &c, int j, int u) {
+    return reinterpret_cast<float4 *>(base) +
+           ((int64_t)(j * 16 + Ctx<PARTS>::NQ * c.part + u) * 128 + c.row);
 }
 
-// partial attention scores over this thread's 32 units (model.py:118-119)
-__device__ __forceinline__ void attn_scores(const Ctx &c, const float *Es, int npos,
-                                            const float (&q)[32], const float (&v)[32],
+template <int PARTS>
+__device__ __forceinline__ void storeU(float *base, const Ctx<PARTS> &c, int j,
+                                       const float (&v)[Ctx<PARTS>::U]) {
+#pragma unroll
+    for (int u = 0; u < Ctx<PARTS>::NQ; u++)
+        *scratch_at(base, c, j, u) = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+}
+
+template <int NQ>
+__device__ __forceinline__ float score_part(const float4 (&e)[NQ], const float (&q)[4 * NQ],
+                                            const float4 *v4) {
+    float s = 0.0f;
+#pragma unroll
+    for (int u = 0; u < NQ; u++) {
+        const float4 v = __ldg(v4 + u);
+        s += v.x * ftanh(e[u].x + q[4 * u + 0]);
+        s += v.y * ftanh(e[u].y + q[4 * u + 1]);
+        s += v.z * ftanh(e[u].z + q[4 * u + 2]);
+        s += v.w * ftanh(e[u].w + q[4 * u + 3]);
+    }
+    return s;
+}
+
+// partial attention scores over this thread's units (model.py:118-119),
+// two positions per iteration so 2*NQ loads are in flight
+template <int PARTS>
+__device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int npos,
+                                            const float (&q)[Ctx<PARTS>::U], const float *vp,
                                             float *s_part, int L) {
-    for (int j = 0; j < npos; j++) {
-        const float4 *e = reinterpret_cast<const float4 *>(Es + ((int64_t)j * 128 + c.row) * 64 +
-                                                            32 * c.half);
-        float s = 0.0f;
+    constexpr int NQ = Ctx<PARTS>::NQ;
+    const float4 *v4 = reinterpret_cast<const float4 *>(vp) + NQ * c.part;
+    int j = 0;
+    for (; j + 2 <= npos; j += 2) {
+        float4 e0[NQ], e1[NQ];
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const float4 x = e[i];
-            s += v[4 * i + 0] * ftanh(x.x + q[4 * i + 0]);
-            s += v[4 * i + 1] * ftanh(x.y + q[4 * i + 1]);
-            s += v[4 * i + 2] * ftanh(x.z + q[4 * i + 2]);
-            s += v[4 * i + 3] * ftanh(x.w + q[4 * i + 3]);
-        }
-        s_part[(c.half * L + j) * 128 + c.row] = s;
+        for (int u = 0; u < NQ; u++) { e0[u] = *scratch_at(Es, c, j, u); e1[u] = *scratch_at(Es, c, j + 1, u); }
+        s_part[(c.part * L + j) * 128 + c.row] = score_part<NQ>(e0, q, v4);
+        s_part[(c.part * L + j + 1) * 128 + c.row] = score_part<NQ>(e1, q, v4);
+    }
+    if (j < npos) {
+        float4 e0[NQ];
+#pragma unroll
+        for (int u = 0; u < NQ; u++) e0[u] = *scratch_at(Es, c, j, u);
+        s_part[(c.part * L + j) * 128 + c.row] = score_part<NQ>(e0, q, v4);
     }
 }
 
-// softmax over positions + context on this thread's 32 units (model.py:120-123)
-__device__ __forceinline__ void attn_context(const Ctx &c, const float *Hs, int npos,
-                                             const float *s_part, int L, float (&ctx)[32]) {
+template <int PARTS>
+__device__ __forceinline__ float full_score(const float *s_part, int L, int j, int row) {
+    float s = 0.0f;
+#pragma unroll
+    for (int p = 0; p < PARTS; p++) s += s_part[(p * L + j) * 128 + row];
+    return s;
+}
+
+template <int NQ>
+__device__ __forceinline__ void acc_ctx(float (&ctx)[4 * NQ], float e, const float4 (&h)[NQ]) {
+#pragma unroll
+    for (int u = 0; u < NQ; u++) {
+        ctx[4 * u + 0] += e * h[u].x;
+        ctx[4 * u + 1] += e * h[u].y;
+        ctx[4 * u + 2] += e * h[u].z;
+        ctx[4 * u + 3] += e * h[u].w;
+    }
+}
+
+// softmax over positions + context on this thread's units (model.py:120-123)
+template <int PARTS>
+__device__ __forceinline__ void attn_context(const Ctx<PARTS> &c, float *Hs, int npos,
+                                             const float *s_part, int L,
+                                             float (&ctx)[Ctx<PARTS>::U]) {
+    constexpr int NQ = Ctx<PARTS>::NQ;
     float mx = -INFINITY;
-    for (int j = 0; j < npos; j++)
-        mx = fmaxf(mx, s_part[j * 128 + c.row] + s_part[(L + j) * 128 + c.row]);
+    for (int j = 0; j < npos; j++) mx = fmaxf(mx, full_score<PARTS>(s_part, L, j, c.row));
 #pragma unroll
-    for (int k = 0; k < 32; k++) ctx[k] = 0.0f;
+    for (int k = 0; k < 4 * NQ; k++) ctx[k] = 0.0f;
     float sum = 0.0f;
-    for (int j = 0; j < npos; j++) {
-        const float e = __expf(s_part[j * 128 + c.row] + s_part[(L + j) * 128 + c.row] - mx);
-        sum += e;
-        const float4 *hp = reinterpret_cast<const float4 *>(Hs + ((int64_t)j * 128 + c.row) * 64 +
-                                                             32 * c.half);
+    int j = 0;
+    for (; j + 2 <= npos; j += 2) {
+        float4 h0[NQ], h1[NQ];
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const float4 x = hp[i];
-            ctx[4 * i + 0] += e * x.x;
-            ctx[4 * i + 1] += e * x.y;
-            ctx[4 * i + 2] += e * x.z;
-            ctx[4 * i + 3] += e * x.w;
-        }
+        for (int u = 0; u < NQ; u++) { h0[u] = *scratch_at(Hs, c, j, u); h1[u] = *scratch_at(Hs, c, j + 1, u); }
+        const float e0 = __expf(full_score<PARTS>(s_part, L, j, c.row) - mx);
+        const float e1 = __expf(full_score<PARTS>(s_part, L, j + 1, c.row) - mx);
+        sum += e0 + e1;
+        acc_ctx<NQ>(ctx, e0, h0);
+        acc_ctx<NQ>(ctx, e1, h1);
+    }
+    if (j < npos) {
+        float4 h0[NQ];
+#pragma unroll
+        for (int u = 0; u < NQ; u++) h0[u] = *scratch_at(Hs, c, j, u);
+        const float e0 = __expf(full_score<PARTS>(s_part, L, j, c.row) - mx);
+        sum += e0;
+        acc_ctx<NQ>(ctx, e0, h0);
     }
     const float inv = __fdividef(1.0f, sum);
 #pragma unroll
-    for (int k = 0; k < 32; k++) ctx[k] *= inv;
+    for (int k = 0; k < 4 * NQ; k++) ctx[k] *= inv;
 }
 
-// partial head: sum_k tanh(comb_k + b_k) * w_k over my 32 units (model.py:177-179)
-__device__ __forceinline__ float head_partial(const Ctx &c, uint32_t col, const float *comb_b,
-                                              const float *head_w) {
-    float v[32];
-    read32(c, col, v);
+// partial head: sum_k tanh(comb_k + b_k) * w_k over my units (model.py:177-179)
+template <int PARTS>
+__device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
+                                              const float *comb_b, const float *head_w) {
+    constexpr int U = Ctx<PARTS>::U;
+    float v[U];
+    readU(c, col, v);
     float s = 0.0f;
 #pragma unroll
-    for (int k = 0; k < 32; k++)
-        s += ftanh(v[k] + __ldg(comb_b + 32 * c.half + k)) * __ldg(head_w + 32 * c.half + k);
+    for (int k = 0; k < U; k++)
+        s += ftanh(v[k] + __ldg(comb_b + U * c.part + k)) * __ldg(head_w + U * c.part + k);
     return s;
 }
 
@@ -289,22 +381,26 @@ __device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T
 
 // ---------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
+__global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(TcArgs a) {
+    constexpr int PARTS = PartsOf<KIND>::value;
+    using C = Ctx<PARTS>;
+    constexpr int U = C::U;
+    constexpr int NT = C::NT;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_s;
-    __shared__ float lpart[2][128];
+    __shared__ float lpart[PARTS][128];
     const bool caching = (KIND == RECMG_MODEL_CACHING);
     const int L = a.m.l_in;
     const int T = caching ? L : a.m.l_out;
     float *s_part = reinterpret_cast<float *>(smem + a.tl.spart_off);
 
-    Ctx c;
+    C c;
     c.tid = threadIdx.x;
     c.warp = c.tid >> 5;
     c.lane = c.tid & 31;
     c.quad = c.warp & 3;
-    c.half = c.warp >> 2;
+    c.part = c.warp >> 2;
     c.row = 32 * c.quad + c.lane;
     if (c.tid == 0) umma::mbar_init(&mbar, 1);
     if (c.warp == 0) umma::tmem_alloc<512>(&tmem_base_s);
@@ -334,12 +430,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
         const int64_t crow = chunk < a.batch ? chunk : a.batch - 1;  // clamp pad rows
         const int32_t *gid = a.gid + crow * L;
         const int32_t *tidp = a.tid + crow * L;
-        float cs0[32], cs1[32], h[32];
+        float cs0[U], cs1[U], h[U];
 
         // ====================== encoder (model.py:131-145) ======================
-        load_phase(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid);
+        load_phase<NT>(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid);
 #pragma unroll
-        for (int k = 0; k < 32; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
+        for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
         if (caching) {
             zero_operand(c, A_H_HI, A_H_LO);
         } else {
@@ -361,14 +457,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
                 }
                 wait_mma(&mbar, phase);
                 if (t >= 1) {
-                    float ep[32];
-                    read32(c, COL_Q, ep);
-                    store32(Es + ((int64_t)(t - 1) * 128 + c.row) * 64 + 32 * c.half, ep);
+                    float ep[U];
+                    readU(c, COL_Q, ep);
+                    storeU(Es, c, t - 1, ep);
                 }
                 if (!last) {
                     cell<false>(c, nullptr, cs0, h);
                     store_operand(c, A_H_HI, A_H_LO, h);
-                    store32(Hs + ((int64_t)t * 128 + c.row) * 64 + 32 * c.half, h);
+                    storeU(Hs, c, t, h);
                 }
             } else {
                 if (!last) {
@@ -399,24 +495,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
                 }
                 wait_mma(&mbar, phase);
                 if (t >= 1) {
-                    float ep[32];
-                    read32(c, COL_Q, ep);
-                    store32(Es + ((int64_t)(t - 1) * 128 + c.row) * 64 + 32 * c.half, ep);
+                    float ep[U];
+                    readU(c, COL_Q, ep);
+                    storeU(Es, c, t - 1, ep);
                 }
                 if (!last) {
                     cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
                     store_operand(c, P_H1_HI, P_H1_LO, h);
-                    store32(Hs + ((int64_t)t * 128 + c.row) * 64 + 32 * c.half, h);
+                    storeU(Hs, c, t, h);
                 }
             }
         }
-        __syncthreads();  // H / enc_pre scratch complete (block-visible via L1/L2)
+        __syncthreads();  // scratch rows are read back by the same threads that wrote them
 
         // ====================== decoder (model.py:156-181) ======================
-        float v[32];
 #pragma unroll
-        for (int k = 0; k < 32; k++) { v[k] = __ldg(att_v + 32 * c.half + k); cs0[k] = 0.0f; cs1[k] = 0.0f; }
-        load_phase(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
+        for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
+        load_phase<NT>(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
+        float lsum;
         if (caching) {
             zero_operand(c, A_H_HI, A_H_LO);
             zero_operand(c, A_X_HI, A_X_LO);
@@ -439,17 +535,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
-                if (t >= 1) lpart[c.half][c.row] = head_partial(c, COL_C, comb_b, head_w);
+                if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_C, comb_b, head_w);
                 if (!last) {
-                    float q[32];
-                    read32(c, COL_Q, q);
-                    attn_scores(c, Es, t + 1, q, v, s_part, L);   // causal: j <= t
+                    float q[U];
+                    readU(c, COL_Q, q);
+                    attn_scores(c, Es, t + 1, q, att_v, s_part, L);   // causal: j <= t
                 }
                 __syncthreads();
-                if (t >= 1 && c.half == 0)
-                    emit_logit(a, chunk, T, t - 1, lpart[0][c.row] + lpart[1][c.row] + head_b, true);
+                if (t >= 1 && c.part == 0) {
+                    lsum = head_b;
+#pragma unroll
+                    for (int p = 0; p < PARTS; p++) lsum += lpart[p][c.row];
+                    emit_logit(a, chunk, T, t - 1, lsum, true);
+                }
                 if (last) break;
-                float ctx[32];
+                float ctx[U];
                 attn_context(c, Hs, t + 1, s_part, L, ctx);
                 store_operand(c, A_X_HI, A_X_LO, ctx);
                 tmem_writes_done();
@@ -488,17 +588,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
-                if (t >= 1) lpart[c.half][c.row] = head_partial(c, COL_Z, comb_b, head_w);
+                if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_Z, comb_b, head_w);
                 if (!last) {
-                    float q[32];
-                    read32(c, COL_Q, q);
-                    attn_scores(c, Es, L, q, v, s_part, L);       // non-causal
+                    float q[U];
+                    readU(c, COL_Q, q);
+                    attn_scores(c, Es, L, q, att_v, s_part, L);       // non-causal
                 }
                 __syncthreads();
-                if (t >= 1 && c.half == 0)
-                    emit_logit(a, chunk, T, t - 1, lpart[0][c.row] + lpart[1][c.row] + head_b, false);
+                if (t >= 1 && c.part == 0) {
+                    lsum = head_b;
+#pragma unroll
+                    for (int p = 0; p < PARTS; p++) lsum += lpart[p][c.row];
+                    emit_logit(a, chunk, T, t - 1, lsum, false);
+                }
                 if (last) break;
-                float ctx[32];
+                float ctx[U];
                 attn_context(c, Hs, L, s_part, L, ctx);
                 store_operand(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
@@ -517,7 +621,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
                 store_operand(c, P_H0_HI, P_H0_LO, h);
                 umma::tmem_st_wait();
                 // layer 1 (DEC-B weights): Z = h0 Wx1 + h1 Wh1 (+ b1)
-                load_phase(smem, a.blob, tl.phase_off[2], tl.phase_len[2], c.tid);
+                load_phase<NT>(smem, a.blob, tl.phase_off[2], tl.phase_len[2], c.tid);
                 umma::fence_before();
                 __syncthreads();
                 if (c.tid == 0) {
@@ -532,7 +636,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lstm_tc_kernel(TcArgs a) {
                 cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
                 store_operand(c, P_H1_HI, P_H1_LO, h);
                 umma::tmem_st_wait();
-                load_phase(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
+                load_phase<NT>(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
             }
         }
         __syncthreads();
@@ -659,7 +763,7 @@ TcLayout tc_layout(const recmg_model_shape *m) {
             t.ptab[i] = t.ptab[0];
         }
     }
-    const size_t spart = (size_t)2 * m->l_in * 128 * 4;
+    const size_t spart = (size_t)(m->kind == RECMG_MODEL_CACHING ? 2 : 4) * m->l_in * 128 * 4;
     t.spart_off = 176 * 1024;
     size_t wmax = 0;
     for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
@@ -748,11 +852,11 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
     if (m->kind == RECMG_MODEL_CACHING) {
         RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_CACHING>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        lstm_tc_kernel<RECMG_MODEL_CACHING><<<grid, kThreadsTC, smem, s>>>(a);
+        lstm_tc_kernel<RECMG_MODEL_CACHING><<<grid, 128 * PartsOf<RECMG_MODEL_CACHING>::value, smem, s>>>(a);
     } else {
         RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_PREFETCH>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        lstm_tc_kernel<RECMG_MODEL_PREFETCH><<<grid, kThreadsTC, smem, s>>>(a);
+        lstm_tc_kernel<RECMG_MODEL_PREFETCH><<<grid, 128 * PartsOf<RECMG_MODEL_PREFETCH>::value, smem, s>>>(a);
     }
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
