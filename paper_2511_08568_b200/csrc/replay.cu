@@ -39,9 +39,16 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
             if (r < l_in) {
                 e = ev_make(EV_SERVE, (uint32_t)gids[k * l_in + r]);
             } else if (r < 2 * l_in) {
+                // keep-bit update; inside one chunk's update block nothing changes
+                // residency, so only the LAST update of an id can matter
+                // (runtime.py:126-130): earlier duplicates become empty events
                 int64_t j = r - l_in;
+                const int32_t gj = gids[k * l_in + j];
+                bool later = false;
+                for (int64_t q = j + 1; q < l_in; q++) later |= (gids[k * l_in + q] == gj);
                 uint32_t b = bits ? (uint32_t)bits[k * l_in + j] : 0u;
-                e = ev_make(b ? EV_UPD1 : EV_UPD0, (uint32_t)gids[k * l_in + j]);
+                e = later ? ev_make(EV_UPD0, kGidMask)
+                          : ev_make(b ? EV_UPD1 : EV_UPD0, (uint32_t)gj);
             } else {
                 // -1 pads a row: that entry and everything after it is empty
                 const int32_t *row = pf + k * pf_stride;
@@ -300,23 +307,11 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
     const unsigned lt = (1u << lane) - 1u;
     int64_t free_hint = 0;
 
-    for (int64_t pos = lo; pos < hi;) {
-        const int nb = (int)imin64(32, hi - pos);
-        const bool valid = lane < nb;
-        ring.ensure(pos - lo, nb);
-        const uint32_t e = valid ? ring.at(pos - lo + lane) : 0u;
-        const uint32_t g = ev_gid(e);
+    // Apply the hit-run part held by one 32-event half (events base+lane,
+    // lane < n_run): group by way, the group leader updates its way.
+    auto apply_run = [&](int64_t base, uint32_t e, int way, int n_run) {
         const uint32_t ty = ev_type(e);
-        const bool real = valid && g != kGidMask;   // kGidMask = empty prefetch slot
-        const int way = real ? ht_find(v, g) : -1;
-        const bool member = way >= 0;
-        unsigned missmask;
-        if (POLICY == RECMG_POLICY_PRIORITY)
-            missmask = __ballot_sync(FULL, real && !member && (ty == EV_SERVE || ty == EV_PREFETCH));
-        else
-            missmask = __ballot_sync(FULL, real && !member);
-        const int cut = missmask ? (__ffs(missmask) - 1) : nb;
-        const bool inrun = member && lane < cut;
+        const bool inrun = way >= 0 && lane < n_run;
         const unsigned peers = __match_any_sync(FULL, inrun ? (unsigned)way : (0x80000000u | lane));
         const int leader = 31 - __clz(peers);
         if (POLICY == RECMG_POLICY_PRIORITY) {
@@ -345,21 +340,48 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 const bool f0 = __shfl_sync(FULL, flag0, leader);
                 if (inrun && ty == EV_SERVE) {
                     const bool first = ((peers & Smask) & lt) == 0;
-                    write_class(a, pos + lane, (f0 && first) ? 1 : 0);
+                    write_class(a, base + lane, (f0 && first) ? 1 : 0);
                 }
             }
         } else {
             if (inrun && lane == leader) {
-                v.meta[way] = clock_base + pos + leader;
+                v.meta[way] = clock_base + base + leader;
                 lhits += __popc(peers);
             }
-            if (a.per_access_hit && lane < cut)
-                a.per_access_hit[a.vals ? a.vals[pos + lane] : pos + lane] = 1;
+            if (a.per_access_hit && lane < n_run)
+                a.per_access_hit[a.vals ? a.vals[base + lane] : base + lane] = 1;
         }
         __syncwarp();
+    };
+
+    for (int64_t pos = lo; pos < hi;) {
+        // 64 events per step (two per lane): membership of both halves against
+        // the same tag set, one cut, the run applied half by half
+        const int nb = (int)imin64(64, hi - pos);
+        ring.ensure(pos - lo, nb);
+        const bool v0 = lane < nb, v1 = lane + 32 < nb;
+        const uint32_t e0 = v0 ? ring.at(pos - lo + lane) : 0u;
+        const uint32_t e1 = v1 ? ring.at(pos - lo + 32 + lane) : 0u;
+        const uint32_t g0 = ev_gid(e0), g1 = ev_gid(e1);
+        const bool real0 = v0 && g0 != kGidMask, real1 = v1 && g1 != kGidMask;
+        const int way0 = real0 ? ht_find(v, g0) : -1;
+        const int way1 = real1 ? ht_find(v, g1) : -1;
+        unsigned miss0, miss1;
+        if (POLICY == RECMG_POLICY_PRIORITY) {
+            const uint32_t t0 = ev_type(e0), t1 = ev_type(e1);
+            miss0 = __ballot_sync(FULL, real0 && way0 < 0 && (t0 == EV_SERVE || t0 == EV_PREFETCH));
+            miss1 = __ballot_sync(FULL, real1 && way1 < 0 && (t1 == EV_SERVE || t1 == EV_PREFETCH));
+        } else {
+            miss0 = __ballot_sync(FULL, real0 && way0 < 0);
+            miss1 = __ballot_sync(FULL, real1 && way1 < 0);
+        }
+        const int cut = miss0 ? (__ffs(miss0) - 1) : (miss1 ? 32 + __ffs(miss1) - 1 : nb);
+        apply_run(pos, e0, way0, cut < 32 ? cut : 32);
+        if (cut > 32) apply_run(pos + 32, e1, way1, cut - 32);
+        const uint32_t e = cut < 32 ? e0 : e1;
 
         if (cut < nb) {
-            const uint32_t ec = __shfl_sync(FULL, e, cut);
+            const uint32_t ec = __shfl_sync(FULL, e, cut & 31);
             const uint32_t gc = ev_gid(ec);
             const uint32_t tc = ev_type(ec);
             if (POLICY == RECMG_POLICY_PRIORITY) {
