@@ -259,8 +259,9 @@ def main():
     dev_ms = start.elapsed_time(end)
     stage_ms = {s: [] for s in HotPath.STAGES}
     for evs in stage_events:
-        for j, s in enumerate(HotPath.STAGES):
-            stage_ms[s].append(evs[j][0].elapsed_time(evs[j][1]))
+        hp.events = evs
+        for s_, v_ in hp.stage_times().items():
+            stage_ms[s_].append(v_)
     rep, lru = hp.report()
     hp.events = None
 

@@ -113,6 +113,18 @@ int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
                  uint8_t *cov_num, uint8_t *cov_den, uint8_t *access_class, void *ws,
                  size_t ws_bytes, void *stream);
 
+/* The same replay over chunks [k_begin, k_end) only (k_end = -1: all), with
+ * the tail accesses appended when with_tail (requires k_end = last chunk).
+ * Consecutive ranges on one state reproduce recmg_replay exactly, so a trace
+ * can be replayed piece by piece while later pieces are still being scored.
+ * bits / pf / cov_* / access_class are indexed globally (chunk k, access i). */
+int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                        int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
+                        int64_t k_end, int32_t with_tail, const uint8_t *bits, const int32_t *pf,
+                        int32_t pf_stride, recmg_counters *counters, uint8_t *cov_num,
+                        uint8_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
+                        void *stream);
+
 /* Host: sequential float64 mean of num/den in chunk order (runtime.py:276,282). */
 double recmg_coverage_mean(const uint8_t *host_num, const uint8_t *host_den, int64_t K);
 
@@ -188,6 +200,11 @@ int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
                         const float *embed_id, const void *packed, const int32_t *gid,
                         const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
                         int32_t *pf_gid, void *ws, size_t ws_bytes, void *stream);
+
+/* Upper bound on the CTAs (= SMs) the TC32 forwards occupy (default 148);
+ * returns the previous value.  Leaving a few SMs to the replay lets a
+ * pipelined replay of earlier chunks run beside the forwards.              */
+int recmg_set_model_sm_budget(int n);
 
 /* ---- trace helpers ----------------------------------------------------- */
 /* tid[i] = table of gids[i] given table offsets[n_tables+1] (device), the

@@ -40,7 +40,7 @@ EXPORTS = (
     "recmg_buffer_op", "recmg_model_dense_floats", "recmg_model_packed_bytes",
     "recmg_model_pack", "recmg_model_forward", "recmg_table_ids", "recmg_trace_pool_pass",
     "recmg_launch_count", "recmg_selftest_umma", "recmg_model_pack_tc",
-    "recmg_model_workspace_bytes",
+    "recmg_model_workspace_bytes", "recmg_replay_chunks", "recmg_set_model_sm_budget",
 )
 
 
@@ -85,6 +85,9 @@ def lib():
         "recmg_replay": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp, vp,
                                         vp, vp, vp, sz, vp]),
         "recmg_coverage_mean": (ctypes.c_double, [vp, vp, i64]),
+        "recmg_replay_chunks": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64, i32,
+                                               vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
+        "recmg_set_model_sm_budget": (ctypes.c_int, [ctypes.c_int]),
         "recmg_simulate_workspace_bytes": (ctypes.c_int, [cfgp, i64, ctypes.POINTER(sz)]),
         "recmg_simulate": (ctypes.c_int, [cfgp, vp, vp, i64, vp, vp, vp, sz, vp]),
         "recmg_buffer_op": (ctypes.c_int, [cfgp, vp, i32, i64, i64, i32, vp, vp]),

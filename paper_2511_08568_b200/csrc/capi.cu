@@ -21,28 +21,87 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 
 struct ReplayPlan {
     Geometry g;
-    int64_t K = 0, Ec = 0, E = 0;
+    int64_t K = 0, Ec = 0, E = 0;   // E: events of this call's chunk range (+ tail)
+    int64_t k0 = 0, nk = 0;
+    bool tail = true;
     bool vals = false;
     uint32_t *ev = nullptr, *vv = nullptr;
     PartitionBuffers pb;
 };
 
 bool plan_replay(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in, int32_t l_out,
-                 int32_t window_ratio, int32_t pf_stride, bool with_class, Arena &a,
-                 ReplayPlan &p) {
+                 int32_t window_ratio, int32_t pf_stride, bool with_class, int64_t k_begin,
+                 int64_t k_end, bool with_tail, Arena &a, ReplayPlan &p) {
     if (!geometry_of(cfg, &p.g)) return false;
     if (cfg->policy != RECMG_POLICY_PRIORITY || cfg->eviction_speed < 1) return false;
     if (n < 0 || l_in < 1 || l_out < 1 || window_ratio < 1 || pf_stride < 0) return false;
     if ((int64_t)window_ratio * l_out > 255) return false;  // uint8 coverage counts
     p.K = recmg_num_chunks(n, l_in, l_out, window_ratio);
+    if (k_begin < 0) k_begin = 0;
+    if (k_end < 0 || k_end > p.K) k_end = p.K;
+    if (k_begin > k_end) return false;
+    if (with_tail && k_end != p.K) return false;   // the tail follows the last chunk
+    p.k0 = k_begin;
+    p.nk = k_end - k_begin;
+    p.tail = with_tail;
     p.Ec = 2 * (int64_t)l_in + pf_stride;
-    p.E = p.K * p.Ec + (n - p.K * l_in);
-    if (p.E >= ((int64_t)1 << 32)) return false;
+    p.E = p.nk * p.Ec + (with_tail ? (n - p.K * l_in) : 0);
+    if (p.K * p.Ec + n >= ((int64_t)1 << 32)) return false;
     p.vals = with_class && p.g.S > 1;
     p.ev = a.take<uint32_t>((size_t)p.E);
     p.vv = p.vals ? a.take<uint32_t>((size_t)p.E) : nullptr;
     if (p.g.S > 1) partition_plan(a, p.pb, p.E, p.g.S, p.vals);
     return true;
+}
+
+int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                 int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
+                 int64_t k_end, int with_tail, const uint8_t *bits, const int32_t *pf,
+                 int32_t pf_stride, recmg_counters *counters, uint8_t *cov_num,
+                 uint8_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
+                 cudaStream_t s) {
+    if (!pf) pf_stride = 0;
+    Arena a{(char *)ws, ws_bytes, 0};
+    ReplayPlan p;
+    if (!state || !counters || (n > 0 && !gids)) return RECMG_E_INVALID_CONFIG;
+    if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, access_class != nullptr,
+                     k_begin, k_end, with_tail != 0, a, p))
+        return RECMG_E_INVALID_CONFIG;
+    if (p.nk > 0) {
+        prefetch_stats_kernel<<<(unsigned)((p.nk + 255) / 256), 256, 0, s>>>(
+            gids, p.k0, p.nk, l_in, window_ratio * l_out, pf, pf_stride, cov_num, cov_den,
+            counters);
+        RECMG_LAUNCH_CHECK();
+    }
+    if (p.E == 0) return RECMG_OK;
+    if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
+    StateView st = state_view(state, cfg, p.g);
+    build_events_kernel<<<(unsigned)imin64((p.E + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
+        gids, n, l_in, bits, pf, pf_stride, p.K, p.k0, p.nk, p.tail ? 1 : 0, p.ev, p.vv);
+    RECMG_LAUNCH_CHECK();
+    uint32_t *ev = p.ev, *vv = p.vv;
+    ReplayArgs ra;
+    memset(&ra, 0, sizeof(ra));
+    if (p.g.S > 1) {
+        int rc = partition_run(p.pb, ev, vv, s);
+        if (rc) return rc;
+        ra.seg_start = p.pb.seg_start;
+        ra.seg_end = p.pb.seg_end;
+    }
+    ra.ev = ev;
+    ra.vals = vv;
+    ra.E = p.E;
+    ra.S = p.g.S;
+    ra.W = p.g.W;
+    ra.es = cfg->eviction_speed;
+    ra.l_in = l_in;
+    ra.Ec = p.Ec;
+    ra.K = p.K;
+    ra.ev_base = p.k0 * p.Ec;
+    ra.st = st;
+    ra.ctr = counters;
+    ra.access_class = access_class;
+    return launch_replay(RECMG_POLICY_PRIORITY, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
 }
 
 }  // namespace
@@ -110,7 +169,7 @@ int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t
                                  size_t *bytes) {
     Arena a{nullptr, 0, 0};
     ReplayPlan p;
-    if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, true, a, p))
+    if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, true, 0, -1, true, a, p))
         return RECMG_E_INVALID_CONFIG;
     *bytes = a.used + 256;
     return RECMG_OK;
@@ -121,48 +180,20 @@ int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
                  const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
                  uint8_t *cov_num, uint8_t *cov_den, uint8_t *access_class, void *ws,
                  size_t ws_bytes, void *stream) {
-    cudaStream_t s = as_stream(stream);
-    if (!pf) pf_stride = 0;
-    Arena a{(char *)ws, ws_bytes, 0};
-    ReplayPlan p;
-    if (!state || !counters || (n > 0 && !gids)) return RECMG_E_INVALID_CONFIG;
-    if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, access_class != nullptr, a, p))
-        return RECMG_E_INVALID_CONFIG;
-    if (p.E == 0) return RECMG_OK;
-    if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
-    StateView st = state_view(state, cfg, p.g);
+    return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, 0, -1, 1, bits, pf,
+                        pf_stride, counters, cov_num, cov_den, access_class, ws, ws_bytes,
+                        as_stream(stream));
+}
 
-    if (p.K > 0) {
-        prefetch_stats_kernel<<<(unsigned)((p.K + 255) / 256), 256, 0, s>>>(
-            gids, p.K, l_in, window_ratio * l_out, pf, pf_stride, cov_num, cov_den, counters);
-        RECMG_LAUNCH_CHECK();
-    }
-    if (p.E == 0) return RECMG_OK;
-    build_events_kernel<<<(unsigned)imin64((p.E + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
-        gids, n, l_in, bits, pf, pf_stride, p.K, p.ev, p.vv);
-    RECMG_LAUNCH_CHECK();
-    uint32_t *ev = p.ev, *vv = p.vv;
-    ReplayArgs ra;
-    memset(&ra, 0, sizeof(ra));
-    if (p.g.S > 1) {
-        int rc = partition_run(p.pb, ev, vv, s);
-        if (rc) return rc;
-        ra.seg_start = p.pb.seg_start;
-        ra.seg_end = p.pb.seg_end;
-    }
-    ra.ev = ev;
-    ra.vals = vv;
-    ra.E = p.E;
-    ra.S = p.g.S;
-    ra.W = p.g.W;
-    ra.es = cfg->eviction_speed;
-    ra.l_in = l_in;
-    ra.Ec = p.Ec;
-    ra.K = p.K;
-    ra.st = st;
-    ra.ctr = counters;
-    ra.access_class = access_class;
-    return launch_replay(RECMG_POLICY_PRIORITY, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
+int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                        int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
+                        int64_t k_end, int32_t with_tail, const uint8_t *bits, const int32_t *pf,
+                        int32_t pf_stride, recmg_counters *counters, uint8_t *cov_num,
+                        uint8_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
+                        void *stream) {
+    return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, k_begin, k_end,
+                        with_tail, bits, pf, pf_stride, counters, cov_num, cov_den,
+                        access_class, ws, ws_bytes, as_stream(stream));
 }
 
 double recmg_coverage_mean(const uint8_t *num, const uint8_t *den, int64_t K) {
@@ -305,6 +336,8 @@ int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
     return model_forward_fp32(shape, embed_id, packed, gid, tid, batch, logits, bits, pf_gid,
                               as_stream(stream));
 }
+
+int recmg_set_model_sm_budget(int n) { return set_model_sm_budget(n); }
 
 // ---- trace helpers -----------------------------------------------------------
 __global__ void table_ids_kernel(const int32_t *gids, int64_t n, const int64_t *offsets,

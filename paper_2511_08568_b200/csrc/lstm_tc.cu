@@ -60,6 +60,7 @@ struct TcArgs {
     uint8_t *bits;
     int32_t *pf_gid;
     float *scratch;        // [gridDim.x][2][L][16][128] float4
+    int *tile_counter;     // dynamic tile scheduler (zeroed before the launch)
 };
 
 // ---- per-thread helpers ------------------------------------------------------
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_s;
     __shared__ float lpart[PARTS][128];
+    __shared__ int s_tile;
     const bool caching = (KIND == RECMG_MODEL_CACHING);
     const int L = a.m.l_in;
     const int T = caching ? L : a.m.l_out;
@@ -425,7 +427,11 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     const float head_b = __ldg(a.dense + pl.head_b);
     const int64_t n_tiles = (a.batch + 127) / 128;
 
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    // dynamic tile scheduler: a CTA that starts late (its SM busy with a
+    // co-scheduled replay CTA) simply takes fewer tiles
+    if (c.tid == 0) s_tile = atomicAdd(a.tile_counter, 1);
+    __syncthreads();
+    for (int64_t tile = s_tile; tile < n_tiles;) {
         const int64_t chunk = tile * 128 + c.row;
         const int64_t crow = chunk < a.batch ? chunk : a.batch - 1;  // clamp pad rows
         const int32_t *gid = a.gid + crow * L;
@@ -640,6 +646,9 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             }
         }
         __syncthreads();
+        if (c.tid == 0) s_tile = atomicAdd(a.tile_counter, 1);
+        __syncthreads();
+        tile = s_tile;
     }
     umma::fence_before();
     __syncthreads();
@@ -828,12 +837,20 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
     return RECMG_OK;
 }
 
+static int g_model_sm_budget = kSmCount;
+
+int set_model_sm_budget(int n) {
+    const int prev = g_model_sm_budget;
+    g_model_sm_budget = n < 1 ? 1 : (n > kSmCount ? kSmCount : n);
+    return prev;
+}
+
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s) {
     if (batch <= 0) return RECMG_OK;
     const int64_t n_tiles = (batch + 127) / 128;
-    const int grid = (int)imin64(n_tiles, kSmCount);
+    const int grid = (int)imin64(n_tiles, g_model_sm_budget);
     if (ws_bytes < tc_workspace_bytes(m, batch)) return RECMG_E_WORKSPACE;
     TcArgs a;
     a.m = *m;
@@ -847,7 +864,9 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
     a.logits = logits;
     a.bits = bits;
     a.pf_gid = pf_gid;
-    a.scratch = (float *)ws;
+    a.tile_counter = (int *)ws;
+    a.scratch = (float *)((char *)ws + 256);
+    RECMG_CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), s));
     const int smem = (int)a.tl.smem_bytes;
     if (m->kind == RECMG_MODEL_CACHING) {
         RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_CACHING>,
@@ -865,7 +884,7 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
 size_t tc_workspace_bytes(const recmg_model_shape *m, int64_t batch) {
     const int64_t n_tiles = (batch + 127) / 128;
     const int64_t grid = imin64(n_tiles > 0 ? n_tiles : 1, kSmCount);
-    return (size_t)grid * 2 * m->l_in * 128 * 64 * sizeof(float);
+    return 256 + (size_t)grid * 2 * m->l_in * 128 * 64 * sizeof(float);
 }
 
 }  // namespace recmg

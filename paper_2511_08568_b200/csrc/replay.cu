@@ -27,15 +27,19 @@ namespace recmg {
 __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n, int32_t l_in,
                                     const uint8_t *__restrict__ bits,
                                     const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
+                                    int64_t k0, int64_t nk, int with_tail,
                                     uint32_t *__restrict__ ev, uint32_t *__restrict__ vals) {
+    // events of chunks [k0, k0+nk) (+ the tail when with_tail, i.e. k0+nk == K);
+    // local event i has global position k0*Ec + i
     const int64_t Ec = 2 * (int64_t)l_in + pf_stride;
-    const int64_t chunk_ev = K * Ec;
-    const int64_t E = chunk_ev + (n - K * l_in);
+    const int64_t chunk_ev = nk * Ec;
+    const int64_t E = chunk_ev + (with_tail ? (n - K * l_in) : 0);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
          i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t e;
         if (i < chunk_ev) {
-            int64_t k = i / Ec, r = i - k * Ec;
+            int64_t kk = i / Ec, r = i - kk * Ec;
+            const int64_t k = k0 + kk;
             if (r < l_in) {
                 e = ev_make(EV_SERVE, (uint32_t)gids[k * l_in + r]);
             } else if (r < 2 * l_in) {
@@ -61,7 +65,7 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
             e = ev_make(EV_SERVE, (uint32_t)gids[K * l_in + (i - chunk_ev)]);
         }
         ev[i] = e;
-        if (vals) vals[i] = (uint32_t)i;
+        if (vals) vals[i] = (uint32_t)(k0 * Ec + i);
     }
 }
 
@@ -78,12 +82,13 @@ __device__ __forceinline__ int64_t access_of_event(int64_t pos, int64_t Ec, int6
 
 // ---------------------------------------------------------------------------
 // prefetch statistics, one thread per chunk  (runtime.py:272-276)
-__global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t K, int32_t l_in,
-                                      int32_t l_win, const int32_t *__restrict__ pf,
+__global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t k0, int64_t nk,
+                                      int32_t l_in, int32_t l_win, const int32_t *__restrict__ pf,
                                       int32_t pf_stride, uint8_t *__restrict__ cov_num,
                                       uint8_t *__restrict__ cov_den,
                                       recmg_counters *__restrict__ ctr) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t K = k0 + nk;
     int64_t issued = 0, useful = 0;
     if (k < K) {
         const int32_t *w = gids + k * l_in + l_in;
@@ -135,7 +140,7 @@ __device__ __forceinline__ void seg_range(const ReplayArgs &a, int64_t set, int6
 }
 
 __device__ __forceinline__ void write_class(const ReplayArgs &a, int64_t pos, uint8_t c) {
-    int64_t orig = a.vals ? (int64_t)a.vals[pos] : pos;
+    int64_t orig = a.vals ? (int64_t)a.vals[pos] : a.ev_base + pos;
     a.access_class[access_of_event(orig, a.Ec, a.K, a.l_in)] = c;
 }
 
@@ -765,8 +770,9 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         int hbits = 6;
         while ((1 << hbits) < (Wp <= 256 ? 4 * Wp : 2 * Wp)) hbits++;
         const int bytes = kRingSlots * kRingBlk * 4 + 12 * Wp + 8 * (1 << hbits);
-        int wpc = 98304 / bytes;
-        wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
+        // one warp (one set) per CTA: a few KB of shared memory, so replay
+        // CTAs co-reside with other kernels' CTAs (pipelined with the forwards)
+        const int wpc = 1;
         const size_t smem = (size_t)wpc * bytes;
         const unsigned grid = (unsigned)((nsets + wpc - 1) / wpc);
 #define RECMG_SMEM_LAUNCH(P, C)                                                            \

@@ -10,9 +10,10 @@ struct ReplayArgs;
 __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n, int32_t l_in,
                                     const uint8_t *__restrict__ bits,
                                     const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
+                                    int64_t k0, int64_t nk, int with_tail,
                                     uint32_t *__restrict__ ev, uint32_t *__restrict__ vals);
-__global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t K, int32_t l_in,
-                                      int32_t l_win, const int32_t *__restrict__ pf,
+__global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t k0, int64_t nk,
+                                      int32_t l_in, int32_t l_win, const int32_t *__restrict__ pf,
                                       int32_t pf_stride, uint8_t *__restrict__ cov_num,
                                       uint8_t *__restrict__ cov_den,
                                       recmg_counters *__restrict__ ctr);
@@ -30,6 +31,7 @@ struct ReplayArgs {
     int32_t es;
     int32_t l_in;
     int64_t Ec, K;
+    int64_t ev_base;           // global position of local event 0 (chunk-range replays)
     StateView st;
     recmg_counters *ctr;
     uint8_t *access_class;

@@ -69,6 +69,20 @@ class BufferReplay:
             _native.ptr(access_class), _native.ptr(self._ws), self._ws.numel(),
             _native.stream_handle(self.torch)), "replay")
 
+    def run_chunks(self, gids, k0, k1, with_tail, bits=None, pf=None):
+        """Replay chunks [k0, k1) (+ tail) of the trace on the current state
+        (recmg_replay_chunks); consecutive ranges == one run()."""
+        n = gids.numel()
+        stride = int(pf.shape[1]) if pf is not None else 0
+        self.reserve(n, stride)
+        self.K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
+        _native.check(_native.lib().recmg_replay_chunks(
+            ctypes.byref(self.cfg), _native.ptr(self.state), _native.ptr(gids), n, self.l_in,
+            self.l_out, self.window_ratio, int(k0), int(k1), 1 if with_tail else 0,
+            _native.ptr(bits), _native.ptr(pf), stride, _native.ptr(self.counters),
+            _native.ptr(self._cov[0]), _native.ptr(self._cov[1]), None, _native.ptr(self._ws),
+            self._ws.numel(), _native.stream_handle(self.torch)), "replay_chunks")
+
     def cov_host(self):
         """(num, den) uint8 arrays of the last run, copied to the host."""
         c = self._cov[:, :self.K].cpu().numpy()

@@ -32,7 +32,13 @@ class HotPath:
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
                  n_max: int, ways: int | None = 32, eviction_speed: int = 4,
                  lru_capacity: int | None = None, lru_ways: int | None = 32, l_in: int = 15,
-                 l_out: int = 5, window_ratio: int = 3):
+                 l_out: int = 5, window_ratio: int = 3, pieces: int = 4, model_sms: int = 146):
+        """pieces > 1 pipelines the replay: chunks are scored in `pieces`
+        ranges on the main stream while earlier ranges replay on a side stream
+        (recmg_replay_chunks continues the buffer state, so the result is the
+        same as one replay); the LRU comparator runs on a third stream from
+        the start.  The TC forwards then use `model_sms` SMs, leaving the rest
+        to the replay CTAs."""
         torch = _native.torch_cuda()
         self.torch = torch
         self.table_sizes = [int(s) for s in table_sizes]
@@ -61,59 +67,95 @@ class HotPath:
         self.lru = None
         if lru_capacity:
             self.lru = LruSim(lru_capacity, self.total_ids, lru_ways, self.n_max)
+        self.pieces = max(1, int(pieces))
+        self.model_sms = int(model_sms) if self.pieces > 1 else 148
+        self.s_replay = torch.cuda.Stream()
+        self.s_lru = torch.cuda.Stream()
         self.events = None
+        self.stage_ms = {}
 
     def enable_stage_timing(self, on=True):
-        t = self.torch
-        self.events = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True))
-                       for _ in self.STAGES] if on else None
-        self.stage_ms = {s: [] for s in self.STAGES}
+        self.events = {} if on else None
 
-    def _mark(self, i, end):
-        if self.events is not None:
-            self.events[i][1 if end else 0].record()
-
-    def collect_stage_times(self):
+    def _ev(self, key, stream):
         if self.events is None:
             return
-        for i, s in enumerate(self.STAGES):
-            a, b = self.events[i]
-            self.stage_ms[s].append(a.elapsed_time(b))
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        self.events.setdefault(key, []).append(e)
+
+    def stage_times(self):
+        """ms per stage of the last launch (sum over pieces; stages overlap)."""
+        out = {}
+        for s in self.STAGES:
+            ev = self.events.get(s, []) if self.events else []
+            out[s] = sum(ev[i].elapsed_time(ev[i + 1]) for i in range(0, len(ev) - 1, 2))
+        return out
+
+    def _piece_bounds(self, K):
+        if self.pieces <= 1 or K < 128 * self.pieces:
+            return [(0, K)]
+        step = (K // self.pieces + 127) // 128 * 128
+        b = list(range(0, K, step)) + [K]
+        return [(b[i], b[i + 1]) for i in range(len(b) - 1)]
 
     def launch(self, n: int):
         """Stream-ordered launches over self.gids[:n] (device-resident)."""
+        torch = self.torch
         L = _native.lib()
         K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
         g = self.gids[:n]
-        bits = pf = None
-        self.buffer.reset()
+        main = torch.cuda.current_stream()
+        ready = torch.cuda.Event()
+        ready.record(main)
+        # K4: the LRU comparator depends only on the ids
         if self.lru is not None:
-            self.lru.reset()
-        self._mark(0, False)
-        if K and (self.caching is not None or self.prefetch is not None):
-            gk = g[:K * self.l_in].view(K, self.l_in)
-            tk = self.tid[:K * self.l_in].view(K, self.l_in)
-            _native.check(L.recmg_table_ids(_native.ptr(gk), K * self.l_in,
-                                            _native.ptr(self.offsets), len(self.table_sizes),
-                                            _native.ptr(tk), _native.stream_handle(self.torch)))
-        self._mark(0, True)
-        self._mark(1, False)
-        if K and self.caching is not None:
-            bits = self.bits[:K]
-            self.caching.forward(gk, tk, logits=self.clog[:K], bits=bits)
-        self._mark(1, True)
-        self._mark(2, False)
-        if K and self.prefetch is not None:
-            pf = self.pf[:K]
-            self.prefetch.forward(gk, tk, logits=self.plog[:K], pf_gid=pf)
-        self._mark(2, True)
-        self._mark(3, False)
-        self.buffer.run(g, bits, pf)
-        self._mark(3, True)
-        self._mark(4, False)
+            self.s_lru.wait_event(ready)
+            with torch.cuda.stream(self.s_lru):
+                self._ev("lru", self.s_lru)
+                self.lru.reset()
+                self.lru.run(g)
+                self._ev("lru", self.s_lru)
+        prev = L.recmg_set_model_sm_budget(self.model_sms)
+        try:
+            self._ev("table_ids", main)
+            if K and (self.caching is not None or self.prefetch is not None):
+                gk = g[:K * self.l_in].view(K, self.l_in)
+                tk = self.tid[:K * self.l_in].view(K, self.l_in)
+                _native.check(L.recmg_table_ids(_native.ptr(gk), K * self.l_in,
+                                                _native.ptr(self.offsets), len(self.table_sizes),
+                                                _native.ptr(tk), _native.stream_handle(torch)))
+            self._ev("table_ids", main)
+            self.s_replay.wait_event(ready)
+            with torch.cuda.stream(self.s_replay):
+                self.buffer.reset()
+            bits = self.bits[:K] if (K and self.caching is not None) else None
+            pf = self.pf[:K] if (K and self.prefetch is not None) else None
+            pieces = self._piece_bounds(K) if K else [(0, 0)]
+            for i, (k0, k1) in enumerate(pieces):
+                if k1 > k0:
+                    if self.caching is not None:
+                        self._ev("caching_fwd", main)
+                        self.caching.forward(gk[k0:k1], tk[k0:k1], logits=self.clog[k0:k1],
+                                             bits=self.bits[k0:k1])
+                        self._ev("caching_fwd", main)
+                    if self.prefetch is not None:
+                        self._ev("prefetch_fwd", main)
+                        self.prefetch.forward(gk[k0:k1], tk[k0:k1], logits=self.plog[k0:k1],
+                                              pf_gid=self.pf[k0:k1])
+                        self._ev("prefetch_fwd", main)
+                scored = torch.cuda.Event()
+                scored.record(main)
+                self.s_replay.wait_event(scored)
+                with torch.cuda.stream(self.s_replay):
+                    self._ev("replay", self.s_replay)
+                    self.buffer.run_chunks(g, k0, k1, i == len(pieces) - 1, bits, pf)
+                    self._ev("replay", self.s_replay)
+        finally:
+            L.recmg_set_model_sm_budget(prev)
+        main.wait_stream(self.s_replay)
         if self.lru is not None:
-            self.lru.run(g)
-        self._mark(4, True)
+            main.wait_stream(self.s_lru)
         self.K = K
         self.n = n
 

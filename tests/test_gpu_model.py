@@ -129,3 +129,25 @@ def test_replay_with_gpu_models_end_to_end():
     assert (rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_useful) == \
         (ref["cache_hits"], ref["prefetch_hits"], ref["on_demand"], ref["prefetch_useful"])
     assert rep.coverage == cov
+
+
+def test_hotpath_pipelined_equals_single_replay():
+    """HotPath with the replay pipelined in chunk pieces on a side stream (and
+    the LRU on a third) reports exactly what one replay reports."""
+    from paper_2511_08568_b200.pipeline import HotPath
+    t = rb.generate_trace(rb.TraceGenConfig([5000] * 16, 300_000, 1.05, 0.4, 32, 4))
+    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=0.4)
+    C = int(0.2 * t.unique_count)
+    C32 = C - C % 32
+    reps = []
+    for pieces in (1, 4, 7):
+        hp = HotPath(cp, pp, t.table_sizes, C32, len(t), ways=32, lru_capacity=C32,
+                     lru_ways=32, pieces=pieces)
+        reps.append(hp.replay_host(t.gid_array.astype(np.int32)))
+    assert reps[0] == reps[1] == reps[2]
+    rep, (h, m) = reps[0]
+    assert rep.total == len(t) and h + m == len(t)
+    ref = rb.replay(t, rb.BufferConfig(C32, 4, 32), cp, pp)
+    assert ref == rep and ref.evictions == rep.evictions
+    assert m == rb.simulate(t, rb.CacheConfig(C32, rb.Policy.LRU, 32), per_access=False).misses
