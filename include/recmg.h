@@ -225,6 +225,12 @@ int recmg_selftest_umma(const void *A, const void *B, float *D, int N, int K, in
                         void *stream);
 
 /* ---- instrumentation --------------------------------------------------- */
+/* TC32 forward with per-CTA phase cycle counters (prof: device int64
+ * [148][16]); diagnostic build of the same kernel (scripts/tc_phases.py).   */
+int recmg_model_forward_profile(const recmg_model_shape *shape, const void *packed,
+                                const int32_t *gid, const int32_t *tid, int64_t batch,
+                                float *logits, void *ws, size_t ws_bytes, long long *prof,
+                                void *stream);
 /* Kernels this library has launched since it was loaded (host counter).   */
 uint64_t recmg_launch_count(void);
 

@@ -339,6 +339,16 @@ int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
 
 int recmg_set_model_sm_budget(int n) { return set_model_sm_budget(n); }
 
+int recmg_model_forward_profile(const recmg_model_shape *shape, const void *packed,
+                                const int32_t *gid, const int32_t *tid, int64_t batch,
+                                float *logits, void *ws, size_t ws_bytes, long long *prof,
+                                void *stream) {
+    if (!tc_supported(shape) || !prof) return RECMG_E_INVALID_CONFIG;
+    return model_forward_tc(shape, packed, (const char *)packed + dense_bytes_aligned(shape), gid,
+                            tid, batch, logits, nullptr, nullptr, ws, ws_bytes,
+                            as_stream(stream), prof);
+}
+
 // ---- trace helpers -----------------------------------------------------------
 __global__ void table_ids_kernel(const int32_t *gids, int64_t n, const int64_t *offsets,
                                  int32_t n_tables, int32_t *tid) {

@@ -61,6 +61,41 @@ struct TcArgs {
     int32_t *pf_gid;
     float *scratch;        // [gridDim.x][2][L][16][128] float4
     int *tile_counter;     // dynamic tile scheduler (zeroed before the launch)
+    long long *prof;       // PROF builds: per-CTA cycles per phase [grid][16]
+};
+
+// Phase cycle accounting (thread 0's timeline = the CTA's critical path);
+// compiled only into the diagnostic recmg_model_forward_profile variant.
+template <bool PROF>
+struct PhaseClock {
+    long long acc[16];
+    long long last;
+    int cur;
+    __device__ __forceinline__ void start() {
+        if constexpr (PROF) {
+#pragma unroll
+            for (int i = 0; i < 16; i++) acc[i] = 0;
+            last = clock64();
+            cur = 15;
+        }
+    }
+    __device__ __forceinline__ void mark(int next) {
+        if constexpr (PROF) {
+            const long long t = clock64();
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (i == cur) acc[i] += t - last;
+            last = t;
+            cur = next;
+        }
+    }
+    __device__ __forceinline__ void flush(long long *out) {
+        if constexpr (PROF) {
+            mark(15);
+#pragma unroll
+            for (int i = 0; i < 16; i++) out[i] = acc[i];
+        }
+    }
 };
 
 // ---- per-thread helpers ------------------------------------------------------
@@ -381,8 +416,13 @@ __device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T
 }  // namespace
 
 // ---------------------------------------------------------------------------
-template <int KIND>
+// phases: 0 enc table init+sync, 1 enc MMA wait, 2 enc epilogue, 3 dec init+sync,
+// 4 dec MMA1 wait, 5 dec head+scores+sync, 6 dec softmax/ctx+sync, 7 dec MMA2 wait,
+// 8 dec cell, 9 weight loads, 10 prefetch layer-1 MMA wait, 11 prefetch layer-1 cell
+template <int KIND, bool PROF>
 __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(TcArgs a) {
+    PhaseClock<PROF> pc;
+    pc.start();
     constexpr int PARTS = PartsOf<KIND>::value;
     using C = Ctx<PARTS>;
     constexpr int U = C::U;
@@ -439,6 +479,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         float cs0[U], cs1[U], h[U];
 
         // ====================== encoder (model.py:131-145) ======================
+        pc.mark(9);
         load_phase<NT>(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid);
 #pragma unroll
         for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
@@ -450,8 +491,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         }
         for (int t = 0; t <= L; t++) {
             const bool last = (t == L);   // t == L: only enc_pre of the last state
+            pc.mark(0);
             if (!last) init_z_from_tables(c, pid_enc, ptab_enc, __ldg(gid + t), __ldg(tidp + t));
             tmem_writes_done();
+            pc.mark(1);
             if (caching) {
                 if (c.tid == 0) {
                     umma::fence_after();
@@ -462,6 +505,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                pc.mark(2);
                 if (t >= 1) {
                     float ep[U];
                     readU(c, COL_Q, ep);
@@ -517,6 +561,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         // ====================== decoder (model.py:156-181) ======================
 #pragma unroll
         for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
+        pc.mark(9);
         load_phase<NT>(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
         float lsum;
         if (caching) {
@@ -524,8 +569,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             zero_operand(c, A_X_HI, A_X_LO);
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);   // t == T: only finish comb_{T-1}
+                pc.mark(3);
                 if (!last) init_z_from_tables(c, pid_dec, ptab_dec, __ldg(gid + t), __ldg(tidp + t));
                 tmem_writes_done();
+                pc.mark(4);
                 // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
                 if (c.tid == 0) {
                     umma::fence_after();
@@ -541,6 +588,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                pc.mark(5);
                 if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_C, comb_b, head_w);
                 if (!last) {
                     float q[U];
@@ -555,10 +603,12 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     emit_logit(a, chunk, T, t - 1, lsum, true);
                 }
                 if (last) break;
+                pc.mark(6);
                 float ctx[U];
                 attn_context(c, Hs, t + 1, s_part, L, ctx);
                 store_operand(c, A_X_HI, A_X_LO, ctx);
                 tmem_writes_done();
+                pc.mark(7);
                 // GEMM2 on ctx_t: Z += ctx Wc ; C = ctx Wcomb_c
                 if (c.tid == 0) {
                     umma::fence_after();
@@ -569,6 +619,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
                 store_operand(c, A_H_HI, A_H_LO, h);
             }
@@ -579,7 +630,9 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);
                 // (DEC-A weights resident) Q = h1 att_dec ; Z[0:64) = h1 Wcomb_h + ctx Wcomb_c
+                pc.mark(3);
                 tmem_writes_done();
+                pc.mark(4);
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last)
@@ -594,6 +647,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                pc.mark(5);
                 if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_Z, comb_b, head_w);
                 if (!last) {
                     float q[U];
@@ -608,12 +662,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     emit_logit(a, chunk, T, t - 1, lsum, false);
                 }
                 if (last) break;
+                pc.mark(6);
                 float ctx[U];
                 attn_context(c, Hs, L, s_part, L, ctx);
                 store_operand(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
                 init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
                 tmem_writes_done();
+                pc.mark(7);
                 if (c.tid == 0) {
                     umma::fence_after();
                     mma3(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
@@ -623,10 +679,12 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
                 store_operand(c, P_H0_HI, P_H0_LO, h);
                 umma::tmem_st_wait();
                 // layer 1 (DEC-B weights): Z = h0 Wx1 + h1 Wh1 (+ b1)
+                pc.mark(9);
                 load_phase<NT>(smem, a.blob, tl.phase_off[2], tl.phase_len[2], c.tid);
                 umma::fence_before();
                 __syncthreads();
@@ -638,10 +696,13 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                          sbase + tl.b_off[10], 256, true);
                     umma::commit(&mbar);
                 }
+                pc.mark(10);
                 wait_mma(&mbar, phase);
+                pc.mark(11);
                 cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
                 store_operand(c, P_H1_HI, P_H1_LO, h);
                 umma::tmem_st_wait();
+                pc.mark(9);
                 load_phase<NT>(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
             }
         }
@@ -650,6 +711,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         __syncthreads();
         tile = s_tile;
     }
+    if (PROF && c.tid == 0) pc.flush(a.prof + blockIdx.x * 16);
     umma::fence_before();
     __syncthreads();
     if (c.warp == 0) umma::tmem_free<512>(c.tbase);
@@ -847,7 +909,8 @@ int set_model_sm_budget(int n) {
 
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
-                     uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s) {
+                     uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,
+                     long long *prof) {
     if (batch <= 0) return RECMG_OK;
     const int64_t n_tiles = (batch + 127) / 128;
     const int grid = (int)imin64(n_tiles, g_model_sm_budget);
@@ -867,16 +930,22 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
     a.tile_counter = (int *)ws;
     a.scratch = (float *)((char *)ws + 256);
     RECMG_CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), s));
+    a.prof = prof;
     const int smem = (int)a.tl.smem_bytes;
+#define RECMG_TC_LAUNCH(K, P)                                                                 \
+    do {                                                                                      \
+        RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<K, P>,                             \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+        lstm_tc_kernel<K, P><<<grid, 128 * PartsOf<K>::value, smem, s>>>(a);                   \
+    } while (0)
     if (m->kind == RECMG_MODEL_CACHING) {
-        RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_CACHING>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        lstm_tc_kernel<RECMG_MODEL_CACHING><<<grid, 128 * PartsOf<RECMG_MODEL_CACHING>::value, smem, s>>>(a);
+        if (prof) RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, true);
+        else RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, false);
     } else {
-        RECMG_CUDA_TRY(cudaFuncSetAttribute(lstm_tc_kernel<RECMG_MODEL_PREFETCH>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        lstm_tc_kernel<RECMG_MODEL_PREFETCH><<<grid, 128 * PartsOf<RECMG_MODEL_PREFETCH>::value, smem, s>>>(a);
+        if (prof) RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, true);
+        else RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, false);
     }
+#undef RECMG_TC_LAUNCH
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
 }
