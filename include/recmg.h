@@ -181,9 +181,13 @@ size_t recmg_model_packed_bytes(const recmg_model_shape *shape, int32_t precisio
  * checkpoint.py:48-79) after a float64 -> float32 cast.                    */
 int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, void *packed,
                      int32_t precision, void *stream);
-/* TC32 packing also needs embed_id [total_ids x dim] fp32 (folded tables). */
+/* TC32 packing also needs embed_id [total_ids x dim] fp32 and the table
+ * offsets [n_tables+1] int64 (device): the layer-0 token projection
+ * [E_id[r]; E_tab[tab(r)]] @ Wx + b is folded into one row per id r.  The
+ * TC32 forward then ignores embed_id and tid.                              */
 int recmg_model_pack_tc(const recmg_model_shape *shape, const float *dense_raw,
-                        const float *embed_id, void *packed, void *stream);
+                        const float *embed_id, const int64_t *table_offsets, void *packed,
+                        void *stream);
 /* Scratch bytes recmg_model_forward needs for `batch` chunks.              */
 size_t recmg_model_workspace_bytes(const recmg_model_shape *shape, int32_t precision,
                                    int64_t batch);

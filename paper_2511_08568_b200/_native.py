@@ -98,7 +98,7 @@ def lib():
         "recmg_model_pack": (ctypes.c_int, [shp, vp, vp, i32, vp]),
         "recmg_model_forward": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp,
                                                sz, vp]),
-        "recmg_model_pack_tc": (ctypes.c_int, [shp, vp, vp, vp, vp]),
+        "recmg_model_pack_tc": (ctypes.c_int, [shp, vp, vp, vp, vp, vp]),
         "recmg_model_workspace_bytes": (sz, [shp, i32, i64]),
         "recmg_table_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp]),
         "recmg_trace_pool_pass": (ctypes.c_int, [vp, vp, vp, i64, ctypes.c_double, i32, vp]),

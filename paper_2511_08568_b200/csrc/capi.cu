@@ -307,9 +307,11 @@ int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, voi
 }
 
 int recmg_model_pack_tc(const recmg_model_shape *shape, const float *dense_raw,
-                        const float *embed_id, void *packed, void *stream) {
-    if (!tc_supported(shape) || !dense_raw || !embed_id || !packed) return RECMG_E_INVALID_CONFIG;
-    return model_pack_tc(shape, dense_raw, embed_id, packed,
+                        const float *embed_id, const int64_t *table_offsets, void *packed,
+                        void *stream) {
+    if (!tc_supported(shape) || !dense_raw || !embed_id || !table_offsets || !packed)
+        return RECMG_E_INVALID_CONFIG;
+    return model_pack_tc(shape, dense_raw, embed_id, table_offsets, packed,
                          (char *)packed + dense_bytes_aligned(shape), as_stream(stream));
 }
 

@@ -183,13 +183,11 @@ __device__ __forceinline__ void zero_operand(const Ctx<PARTS> &c, uint32_t col_h
     st_cols<H>(c.lane_addr + col_lo + H * c.part, z);
 }
 
-// Z[my 4U gate columns] = Pid[g] + Ptab[t]  (layer-0 token projection + bias)
+// Z[my 4U gate columns] = P[g]  (layer-0 token projection + bias, folded per id)
 template <int PARTS>
-__device__ __forceinline__ void init_z_from_tables(const Ctx<PARTS> &c, const float *pid,
-                                                   const float *ptab, int32_t g, int32_t tb) {
+__device__ __forceinline__ void init_z_from_table(const Ctx<PARTS> &c, const float *pid, int32_t g) {
     constexpr int NC = 4 * Ctx<PARTS>::U;     // columns
     const float4 *a = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + NC * c.part);
-    const float4 *b = reinterpret_cast<const float4 *>(ptab + (int64_t)tb * 256 + NC * c.part);
 #pragma unroll
     for (int half = 0; half < NC / 64; half++) {
         float4 x[16];
@@ -200,12 +198,11 @@ __device__ __forceinline__ void init_z_from_tables(const Ctx<PARTS> &c, const fl
             uint32_t r[16];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                const float4 y = __ldg(b + half * 16 + blk * 4 + q);
                 const float4 u = x[blk * 4 + q];
-                r[4 * q + 0] = __float_as_uint(u.x + y.x);
-                r[4 * q + 1] = __float_as_uint(u.y + y.y);
-                r[4 * q + 2] = __float_as_uint(u.z + y.z);
-                r[4 * q + 3] = __float_as_uint(u.w + y.w);
+                r[4 * q + 0] = __float_as_uint(u.x);
+                r[4 * q + 1] = __float_as_uint(u.y);
+                r[4 * q + 2] = __float_as_uint(u.z);
+                r[4 * q + 3] = __float_as_uint(u.w);
             }
             umma::tmem_st16(c.lane_addr + COL_Z + NC * c.part + 64 * half + 16 * blk, r);
         }
@@ -456,9 +453,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     const TcLayout &tl = a.tl;
     const PackedLayout &pl = a.pl;
     const float *pid_enc = reinterpret_cast<const float *>(a.blob + tl.pid[0]);
-    const float *ptab_enc = reinterpret_cast<const float *>(a.blob + tl.ptab[0]);
     const float *pid_dec = reinterpret_cast<const float *>(a.blob + tl.pid[1]);
-    const float *ptab_dec = reinterpret_cast<const float *>(a.blob + tl.ptab[1]);
     float *Hs = a.scratch + (int64_t)blockIdx.x * 2 * L * 128 * 64;
     float *Es = Hs + (int64_t)L * 128 * 64;
     const float *att_v = a.dense + pl.att_v;
@@ -475,7 +470,6 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         const int64_t chunk = tile * 128 + c.row;
         const int64_t crow = chunk < a.batch ? chunk : a.batch - 1;  // clamp pad rows
         const int32_t *gid = a.gid + crow * L;
-        const int32_t *tidp = a.tid + crow * L;
         float cs0[U], cs1[U], h[U];
 
         // ====================== encoder (model.py:131-145) ======================
@@ -492,7 +486,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         for (int t = 0; t <= L; t++) {
             const bool last = (t == L);   // t == L: only enc_pre of the last state
             pc.mark(0);
-            if (!last) init_z_from_tables(c, pid_enc, ptab_enc, __ldg(gid + t), __ldg(tidp + t));
+            if (!last) init_z_from_table(c, pid_enc, __ldg(gid + t));
             tmem_writes_done();
             pc.mark(1);
             if (caching) {
@@ -570,7 +564,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);   // t == T: only finish comb_{T-1}
                 pc.mark(3);
-                if (!last) init_z_from_tables(c, pid_dec, ptab_dec, __ldg(gid + t), __ldg(tidp + t));
+                if (!last) init_z_from_table(c, pid_dec, __ldg(gid + t));
                 tmem_writes_done();
                 pc.mark(4);
                 // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
@@ -744,10 +738,14 @@ __global__ void bimage_kernel(const float *raw, uint8_t *out, BSpec s, int d) {
     }
 }
 
-// out[r][4j+g] = bias[g*d+j] + sum_k E[r][k] * W[k][g*d+j]   (fp32)
-__global__ void proj_table_kernel(const float *E, int64_t rows, int d, const float *W,
-                                  const float *bias, float *out) {
-    extern __shared__ float e_s[];  // [32][d]
+// out[r][4j+g] = bias[g*d+j] + sum_k E[r][k] W[k][g*d+j]
+//                             + sum_k Et[tab(r)][k] Wt[k][g*d+j]      (fp32)
+// i.e. the whole layer-0 token projection [E_id[r]; E_tab[tab(r)]] @ Wx + b
+// of model.py:105,148-153 for every id r, tab(r) = searchsorted(offsets, r).
+__global__ void proj_fold_kernel(const float *E, int64_t rows, int d, const float *W,
+                                 const float *Et, const float *Wt, const int64_t *offsets,
+                                 int n_tables, const float *bias, float *out) {
+    extern __shared__ float e_s[];  // [32][2d]
     const int n = threadIdx.x;       // 0..4d-1
     const int j = n >> 2, g = n & 3;
     const int col = g * d + j;
@@ -755,17 +753,29 @@ __global__ void proj_table_kernel(const float *E, int64_t rows, int d, const flo
         __syncthreads();
         for (int i = threadIdx.x; i < 32 * d; i += blockDim.x) {
             const int64_t r = r0 + i / d;
-            e_s[i] = r < rows ? E[r * d + (i % d)] : 0.0f;
+            float e = 0.0f, et = 0.0f;
+            if (r < rows) {
+                e = E[r * d + (i % d)];
+                int lo = 0, hi = n_tables;   // offsets[lo] <= r < offsets[hi]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (offsets[mid] <= r) lo = mid; else hi = mid;
+                }
+                et = Et[(int64_t)lo * d + (i % d)];
+            }
+            e_s[(i / d) * 2 * d + (i % d)] = e;
+            e_s[(i / d) * 2 * d + d + (i % d)] = et;
         }
         __syncthreads();
         float acc[32];
-        const float b = bias ? bias[col] : 0.0f;
+        const float b = bias[col];
 #pragma unroll
         for (int q = 0; q < 32; q++) acc[q] = b;
         for (int k = 0; k < d; k++) {
             const float w = __ldg(W + (int64_t)k * 4 * d + col);
+            const float wt = __ldg(Wt + (int64_t)k * 4 * d + col);
 #pragma unroll
-            for (int q = 0; q < 32; q++) acc[q] += e_s[q * d + k] * w;
+            for (int q = 0; q < 32; q++) acc[q] += e_s[q * 2 * d + k] * w + e_s[q * 2 * d + d + k] * wt;
         }
 #pragma unroll
         for (int q = 0; q < 32; q++)
@@ -827,13 +837,12 @@ TcLayout tc_layout(const recmg_model_shape *m) {
     for (int i = 0; i < 2; i++) {
         if (i < ntab) {
             t.pid[i] = o; o += V * 256 * 4;
-            t.ptab[i] = o; o += T * 256 * 4;
             o = (o + 255) / 256 * 256;
         } else {
             t.pid[i] = t.pid[0];
-            t.ptab[i] = t.ptab[0];
         }
     }
+    (void)T;
     const size_t spart = (size_t)(m->kind == RECMG_MODEL_CACHING ? 2 : 4) * m->l_in * 128 * 4;
     t.spart_off = 176 * 1024;
     size_t wmax = 0;
@@ -844,7 +853,7 @@ TcLayout tc_layout(const recmg_model_shape *m) {
 }
 
 int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *embed_id,
-                  void *packed_dense, void *tc_blob, cudaStream_t s) {
+                  const int64_t *offsets, void *packed_dense, void *tc_blob, cudaStream_t s) {
     int rc = model_pack(m, raw, packed_dense, s);
     if (rc) return rc;
     const RawLayout r = raw_layout(m);
@@ -881,19 +890,16 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
         bimage_kernel<<<64, 256, 0, s>>>(raw, out, x, d);
         RECMG_LAUNCH_CHECK();
     }
-    // folded token tables: Pid = E_id @ Wx[0:d], Ptab = E_tab @ Wx[d:2d] + b
+    // folded token tables: P[r] = [E_id[r]; E_tab[tab(r)]] @ Wx[0:2d] + b
     const int ntab = m->kind == RECMG_MODEL_CACHING ? 2 : 1;
     for (int i = 0; i < ntab; i++) {
         const int64_t wx = (i == 0) ? r.enc_wx[0] : r.dec_wx[0];
         const int64_t bb = (i == 0) ? r.enc_b[0] : r.dec_b[0];
         const int64_t blocks = imin64((m->total_ids + 31) / 32, 64 * kSmCount);
-        proj_table_kernel<<<(unsigned)blocks, 4 * d, 32 * d * 4, s>>>(
-            embed_id, m->total_ids, d, raw + wx, nullptr, (float *)(out + t.pid[i]));
-        RECMG_LAUNCH_CHECK();
-        proj_table_kernel<<<(unsigned)imin64((m->n_tables + 31) / 32, 64 * kSmCount), 4 * d,
-                            32 * d * 4, s>>>(raw + r.embed_table, m->n_tables, d,
-                                             raw + wx + (int64_t)d * 4 * d, raw + bb,
-                                             (float *)(out + t.ptab[i]));
+        proj_fold_kernel<<<(unsigned)blocks, 4 * d, 2 * 32 * d * 4, s>>>(
+            embed_id, m->total_ids, d, raw + wx, raw + r.embed_table,
+            raw + wx + (int64_t)d * 4 * d, offsets, m->n_tables, raw + bb,
+            (float *)(out + t.pid[i]));
         RECMG_LAUNCH_CHECK();
     }
     return RECMG_OK;

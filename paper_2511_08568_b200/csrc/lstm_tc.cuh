@@ -8,7 +8,7 @@ struct TcLayout {              // byte offsets into the TC blob
     int64_t phase_off[3], phase_len[3];  // B-image groups loaded together into smem
     int64_t b_off[16];                   // B image (hi, then lo) offset within its phase
     int nb;
-    int64_t pid[2], ptab[2];             // folded token tables (enc, dec) [rows][256] fp32
+    int64_t pid[2];                      // folded token tables (enc, dec) [ids][256] fp32
     size_t spart_off, smem_bytes;
     int64_t total;
 };
@@ -16,7 +16,7 @@ struct TcLayout {              // byte offsets into the TC blob
 bool tc_supported(const recmg_model_shape *m);
 TcLayout tc_layout(const recmg_model_shape *m);
 int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *embed_id,
-                  void *packed_dense, void *tc_blob, cudaStream_t s);
+                  const int64_t *offsets, void *packed_dense, void *tc_blob, cudaStream_t s);
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,

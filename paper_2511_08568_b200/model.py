@@ -158,13 +158,14 @@ class DeviceModel:
             embed_id = torch.from_numpy(
                 np.ascontiguousarray(params.arrays["embed_id"], dtype=np.float32)).cuda()
         raw_d = torch.from_numpy(raw).cuda()
+        self.offsets = torch.from_numpy(table_offsets(params.table_sizes)).cuda()
         self.packed = _native.device_bytes(
             torch, L.recmg_model_packed_bytes(ctypes.byref(self.shape), self.prec))
         st = _native.stream_handle(torch)
         if self.prec == _native.PREC_TC32:
             _native.check(L.recmg_model_pack_tc(ctypes.byref(self.shape), _native.ptr(raw_d),
-                                                _native.ptr(embed_id), _native.ptr(self.packed),
-                                                st), "model_pack_tc")
+                                                _native.ptr(embed_id), _native.ptr(self.offsets),
+                                                _native.ptr(self.packed), st), "model_pack_tc")
             self.embed_id = None            # folded into the packed tables
         else:
             _native.check(L.recmg_model_pack(ctypes.byref(self.shape), _native.ptr(raw_d),
@@ -172,7 +173,6 @@ class DeviceModel:
                           "model_pack")
             self.embed_id = embed_id
         torch.cuda.current_stream().synchronize()
-        self.offsets = torch.from_numpy(table_offsets(params.table_sizes)).cuda()
         self._ws = None
 
     @property
