@@ -291,16 +291,17 @@ __device__ __forceinline__ void storeU(float *base, const Ctx<PARTS> &c, int j,
 template <int NQ>
 __device__ __forceinline__ float score_part(const float4 (&e)[NQ], const float (&q)[4 * NQ],
                                             const float4 *v4) {
-    float s = 0.0f;
+    // four independent accumulators: the dot is a latency chain otherwise
+    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
 #pragma unroll
     for (int u = 0; u < NQ; u++) {
         const float4 v = __ldg(v4 + u);
-        s += v.x * ftanh(e[u].x + q[4 * u + 0]);
-        s += v.y * ftanh(e[u].y + q[4 * u + 1]);
-        s += v.z * ftanh(e[u].z + q[4 * u + 2]);
-        s += v.w * ftanh(e[u].w + q[4 * u + 3]);
+        s0 += v.x * ftanh(e[u].x + q[4 * u + 0]);
+        s1 += v.y * ftanh(e[u].y + q[4 * u + 1]);
+        s2 += v.z * ftanh(e[u].z + q[4 * u + 2]);
+        s3 += v.w * ftanh(e[u].w + q[4 * u + 3]);
     }
-    return s;
+    return (s0 + s1) + (s2 + s3);
 }
 
 // partial attention scores over this thread's units (model.py:118-119),
@@ -388,11 +389,11 @@ __device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
     constexpr int U = Ctx<PARTS>::U;
     float v[U];
     readU(c, col, v);
-    float s = 0.0f;
+    float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
     for (int k = 0; k < U; k++)
-        s += ftanh(v[k] + __ldg(comb_b + U * c.part + k)) * __ldg(head_w + U * c.part + k);
-    return s;
+        s[k & 3] += ftanh(v[k] + __ldg(comb_b + U * c.part + k)) * __ldg(head_w + U * c.part + k);
+    return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
 __device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T, int t, float s,
@@ -843,7 +844,7 @@ TcLayout tc_layout(const recmg_model_shape *m) {
         }
     }
     (void)T;
-    const size_t spart = (size_t)(m->kind == RECMG_MODEL_CACHING ? 2 : 4) * m->l_in * 128 * 4;
+    const size_t spart = (size_t)(m->kind == RECMG_MODEL_CACHING ? PartsOf<RECMG_MODEL_CACHING>::value : PartsOf<RECMG_MODEL_PREFETCH>::value) * m->l_in * 128 * 4;
     t.spart_off = 176 * 1024;
     size_t wmax = 0;
     for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
