@@ -47,7 +47,7 @@ UNIT = "accesses/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="recmg", choices=["recmg", "reference"])
     ap.add_argument("--accesses", type=int, default=25_000_000)
@@ -59,6 +59,10 @@ def parse():
                     help="accesses in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-rows", action="store_true",
+                    help="skip the K5/K6 host-row gather + EmbeddingBag measurement")
+    ap.add_argument("--row-dim", type=int, default=128)
+    ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
     return ap.parse_args()
 
 
@@ -183,6 +187,57 @@ def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways):
             "model_s": t1 - t0, "replay_s": t2 - t1}
 
 
+def measure_rows(args, hp, n, torch):
+    """K5 refresh (rows of slots changed by the replay, PCIe zero-copy) and K6
+    EmbeddingBag(sum) over the whole trace in bags of --pool accesses, after a
+    full replay.  Rows: N(0,1) fp32 [V, row_dim] in pinned host memory."""
+    from paper_2511_08568_b200.engine import RowStore
+    V = hp.total_ids
+    D = args.row_dim
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(123)
+    host = torch.empty((V, D), dtype=torch.float32, pin_memory=True)
+    blk = 1 << 20
+    for r0 in range(0, V, blk):
+        r1 = min(V, r0 + blk)
+        host[r0:r1].copy_(torch.randn((r1 - r0, D), device="cuda", generator=gen))
+    torch.cuda.synchronize()
+    # PCIe H2D peak on this box: pinned cudaMemcpy of 1 GiB, best of 5
+    src = host.view(-1)[: (1 << 28)]
+    dst = torch.empty_like(src, device="cuda")
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); dst.copy_(src, non_blocking=True); e1.record(); torch.cuda.synchronize()
+        best = max(best, src.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del dst
+    rows = RowStore(hp.buffer, host)
+    P = args.pool
+    n_bags = n // P
+    offsets = torch.arange(0, (n_bags + 1) * P, P, dtype=torch.int64, device="cuda")
+    out = torch.empty((n_bags, D), dtype=torch.float32, device="cuda")
+    hp.launch(n)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    rows.refresh()
+    e[1].record()
+    rows.pool(hp.gids[:n_bags * P], offsets, out)
+    e[2].record()
+    torch.cuda.synchronize()
+    copied = int(rows.copied.item())
+    hb, hh = (int(x) for x in rows.src.cpu().numpy())
+    t_ref, t_pool = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])
+    pool_bytes = (hb + hh) * D * 4 + n_bags * D * 4 + n * 4
+    return {"dim": D, "pooling_factor": P, "rows_host_gb": V * D * 4 / 1e9,
+            "refresh_ms": t_ref, "rows_copied": copied,
+            "refresh_pcie_gbs": copied * D * 4 / (t_ref / 1e3) / 1e9,
+            "pcie_h2d_peak_gbs": best, "pcie_peak_source": "pinned cudaMemcpy H2D 1 GiB, best of 5",
+            "pool_ms": t_pool, "bags": n_bags, "rows_from_hbm": hb, "rows_from_host": hh,
+            "pool_gbs": pool_bytes / (t_pool / 1e3) / 1e9,
+            "note": "K5/K6 run after the timed replay; not part of `value`"}
+
+
 def build_state(args, rank, torch):
     import paper_2511_08568_b200 as rb
     from paper_2511_08568_b200.model import DeviceModel, init_params_device
@@ -279,6 +334,11 @@ def main():
         e2e_ms = (time.perf_counter() - t0) * 1000.0
         assert rep_e == rep and lru_e == lru, "e2e replay disagrees with device replay"
 
+    # ---- K5/K6: host-row gathers + EmbeddingBag (config 2 rows) -------------
+    rows_line = None
+    if not args.no_rows:
+        rows_line = measure_rows(args, hp, n, torch)
+
     # ---- reduce over ranks ---------------------------------------------------
     vals = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device="cuda")
     ctr = torch.tensor([rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
@@ -301,7 +361,10 @@ def main():
     mean = {s: (sum(v) / len(v) if v else 0.0) for s, v in stage_ms.items()}
     fl_c = caching_flops(15, args.dim) * K
     fl_p = prefetch_flops(15, 5, args.dim) * K
-    dominant = max(("caching_fwd", "prefetch_fwd", "replay", "lru"), key=lambda s: mean[s])
+    # The replay and the LRU run on side streams under the forwards (HotPath
+    # pipelining), so the critical path is the two LSTM forwards: the dominant
+    # kernel is the longer forward.  Every kernel's own figure is listed too.
+    dominant = max(("caching_fwd", "prefetch_fwd"), key=lambda s: mean[s])
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -309,23 +372,23 @@ def main():
     except (OSError, ValueError):
         pass
     prof = load_profile_traffic() or {}
-    if dominant in ("caching_fwd", "prefetch_fwd"):
-        fl = fl_c if dominant == "caching_fwd" else fl_p
-        achieved = fl / (mean[dominant] / 1000.0) / 1e12
-        peak = peaks.get("bf16_tflops_sustained", 1400.0)
-        roof = {"kernel": dominant, "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)",
-                "algorithmic_flop_per_launch": fl,
-                "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch")}
-    else:
-        ev_n = K * (2 * 15 + 5) + (n - K * 15)
-        byts = ev_n * 4 + n * 1
-        achieved = byts / (mean[dominant] / 1000.0) / 1e9
-        peak = peaks.get("hbm_gbs", 6538.6)
-        roof = {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak,
-                "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch")}
+    fl = fl_c if dominant == "caching_fwd" else fl_p
+    achieved = fl / (mean[dominant] / 1000.0) / 1e12
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    ev_n = K * (2 * 15 + 5) + (n - K * 15)
+    roof = {"kernel": dominant, "bound": "tensor", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)",
+            "algorithmic_flop_per_launch": fl,
+            "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch"),
+            "kernels": {
+                "caching_fwd": {"ms": mean["caching_fwd"], "tflops": fl_c / (mean["caching_fwd"] / 1e3) / 1e12},
+                "prefetch_fwd": {"ms": mean["prefetch_fwd"], "tflops": fl_p / (mean["prefetch_fwd"] / 1e3) / 1e12},
+                "replay": {"ms": mean["replay"], "gbs": (ev_n * 4 + n) / (mean["replay"] / 1e3) / 1e9,
+                           "bound": "hbm (7.33 B/access algorithmic); dependency-chain bound",
+                           "overlapped": True},
+                "lru": {"ms": mean["lru"], "gbs": (n * 5) / (mean["lru"] / 1e3) / 1e9,
+                        "overlapped": True}}}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -343,14 +406,14 @@ def main():
         "clocks": clk,
         "setup_s": setup_s,
     }
-    line["roofline"]["caching_fwd_tflops"] = fl_c / (mean["caching_fwd"] / 1000.0) / 1e12
-    line["roofline"]["prefetch_fwd_tflops"] = fl_p / (mean["prefetch_fwd"] / 1000.0) / 1e12
     if e2e_ms is not None:
         e2e_step = e2e_ms_max / args.steps
         line["e2e"] = {"value": total_n / (e2e_step / 1000.0), "unit": UNIT,
                        "ms_per_step": e2e_step,
                        "h2d_bytes_per_step": int(n * 4),
                        "d2h_bytes_per_step": int(hp.d2h_bytes())}
+    if rows_line is not None:
+        line["rows"] = rows_line
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32)
     print(json.dumps(line), flush=True)

@@ -149,6 +149,24 @@ enum {
 int recmg_buffer_op(const recmg_buffer_cfg *cfg, void *state, int32_t op, int64_t gid,
                     int64_t arg, int32_t flag, int64_t *result, void *stream);
 
+/* ---- embedding rows: host gathers (K5) and EmbeddingBag pooling (K6) ---- */
+/* Not in the reference; parity = torch embedding_bag(sum).
+ * host_rows: [total_ids x dim] fp32 in pinned, mapped host memory (UVA);
+ * buf_rows: [capacity x dim] fp32 in HBM, row = buffer slot (set*ways+way);
+ * loaded: int32 [capacity], the id whose row each slot holds (-1 = none).  */
+/* Copy the row of every slot whose occupant changed since the last refresh
+ * (zero-copy PCIe reads); *copied (device int64) += rows copied.  ways <= 32. */
+int recmg_rows_refresh(const recmg_buffer_cfg *cfg, const void *state, int32_t *loaded,
+                       const float *host_rows, int32_t dim, float *buf_rows, int64_t *copied,
+                       void *stream);
+/* out[b] = sum of the rows of gids[bag_offsets[b] .. bag_offsets[b+1]) in
+ * order; each row read from its HBM slot when resident, else from host
+ * memory.  src_counts (device int64[2], nullable) += {from HBM, from host}. */
+int recmg_embedding_bag(const recmg_buffer_cfg *cfg, const void *state, const int32_t *gids,
+                        const int64_t *bag_offsets, int64_t n_bags, const float *buf_rows,
+                        const float *host_rows, int32_t dim, float *out, int64_t *src_counts,
+                        void *stream);
+
 /* ---- models  (neural/model.py) ----------------------------------------- */
 enum { RECMG_MODEL_CACHING = 0, RECMG_MODEL_PREFETCH = 1 };
 enum {

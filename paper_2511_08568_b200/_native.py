@@ -41,7 +41,7 @@ EXPORTS = (
     "recmg_model_pack", "recmg_model_forward", "recmg_table_ids", "recmg_trace_pool_pass",
     "recmg_launch_count", "recmg_selftest_umma", "recmg_model_pack_tc",
     "recmg_model_workspace_bytes", "recmg_replay_chunks", "recmg_set_model_sm_budget",
-    "recmg_model_forward_profile",
+    "recmg_model_forward_profile", "recmg_rows_refresh", "recmg_embedding_bag",
 )
 
 
@@ -89,6 +89,8 @@ def lib():
         "recmg_replay_chunks": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64, i32,
                                                vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
         "recmg_set_model_sm_budget": (ctypes.c_int, [ctypes.c_int]),
+        "recmg_rows_refresh": (ctypes.c_int, [cfgp, vp, vp, vp, i32, vp, vp, vp]),
+        "recmg_embedding_bag": (ctypes.c_int, [cfgp, vp, vp, vp, i64, vp, vp, i32, vp, vp, vp]),
         "recmg_model_forward_profile": (ctypes.c_int, [shp, vp, vp, vp, i64, vp, vp, sz, vp, vp]),
         "recmg_simulate_workspace_bytes": (ctypes.c_int, [cfgp, i64, ctypes.POINTER(sz)]),
         "recmg_simulate": (ctypes.c_int, [cfgp, vp, vp, i64, vp, vp, vp, sz, vp]),

@@ -146,6 +146,48 @@ class LruSim:
         return h, m
 
 
+class RowStore:
+    """Embedding rows of the buffered tables: all rows in pinned, mapped host
+    memory (read by the GPU over PCIe through UVA), one HBM row per buffer
+    slot.  refresh() (K5) copies the rows of slots whose occupant changed in
+    the last replay; pool() (K6) is EmbeddingBag(sum) reading resident rows
+    from HBM and the rest from host memory."""
+
+    def __init__(self, replay: "BufferReplay", host_rows):
+        torch = _native.torch_cuda()
+        self.torch = torch
+        if not host_rows.is_pinned():
+            raise ValueError("host_rows must be pinned (torch.Tensor.pin_memory())")
+        if host_rows.dtype != torch.float32 or host_rows.dim() != 2:
+            raise ValueError("host_rows must be float32 [total_ids, dim]")
+        self.replay = replay
+        self.host = host_rows
+        self.dim = int(host_rows.shape[1])
+        cap = int(replay.cfg.capacity)
+        self.buf = torch.zeros((cap, self.dim), dtype=torch.float32, device="cuda")
+        self.loaded = torch.full((cap,), -1, dtype=torch.int32, device="cuda")
+        self.copied = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.src = torch.zeros(2, dtype=torch.int64, device="cuda")
+
+    def refresh(self):
+        _native.check(_native.lib().recmg_rows_refresh(
+            ctypes.byref(self.replay.cfg), _native.ptr(self.replay.state),
+            _native.ptr(self.loaded), ctypes.c_void_p(self.host.data_ptr()), self.dim,
+            _native.ptr(self.buf), _native.ptr(self.copied),
+            _native.stream_handle(self.torch)), "rows_refresh")
+
+    def pool(self, gids, offsets, out=None):
+        n_bags = offsets.numel() - 1
+        if out is None:
+            out = self.torch.empty((n_bags, self.dim), dtype=self.torch.float32, device="cuda")
+        _native.check(_native.lib().recmg_embedding_bag(
+            ctypes.byref(self.replay.cfg), _native.ptr(self.replay.state), _native.ptr(gids),
+            _native.ptr(offsets), n_bags, _native.ptr(self.buf),
+            ctypes.c_void_p(self.host.data_ptr()), self.dim, _native.ptr(out),
+            _native.ptr(self.src), _native.stream_handle(self.torch)), "embedding_bag")
+        return out
+
+
 def to_device_gids(torch, gids: np.ndarray):
     g = np.asarray(gids)
     if g.size and (g.min() < 0 or g.max() >= (1 << 30) - 1):

@@ -1,0 +1,50 @@
+"""K5 host-row gathers + K6 EmbeddingBag vs torch.nn.functional.embedding_bag
+on the CPU (the reference has no row data; parity unpinned by
+the reference, oracle = torch embedding_bag(mode='sum'))."""
+import numpy as np
+import pytest
+
+import paper_2511_08568_b200 as rb
+from paper_2511_08568_b200.engine import BufferReplay, RowStore, to_device_gids
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dim,ways,bag", [(128, 32, 2), (16, 8, 5), (64, 32, 1), (256, 4, 3)])
+def test_gather_and_pool_vs_torch(dim, ways, bag):
+    import torch
+    import torch.nn.functional as F
+    rng = np.random.default_rng(dim + ways)
+    t = rb.generate_trace(rb.TraceGenConfig([3000] * 4, 40_000, 1.05, 0.4, 32, dim))
+    V = t.total_ids
+    host = torch.from_numpy(rng.standard_normal((V, dim)).astype(np.float32)).pin_memory()
+    C = int(0.2 * t.unique_count)
+    C -= C % ways
+    K = rb.num_chunks(len(t))
+    bits = torch.from_numpy(rng.integers(0, 2, (K, 15)).astype(np.uint8)).cuda()
+    pf = torch.from_numpy(rng.integers(0, V, (K, 5)).astype(np.int32)).cuda()
+    rep = BufferReplay(C, V, 4, ways, len(t), pf_stride=5)
+    rows = RowStore(rep, host)
+    g = to_device_gids(torch, t.gid_array)
+    half = (K // 2)
+    pieces = [(0, half, False), (half, K, True)]
+    n_bags = len(t) // bag
+    offsets = torch.arange(0, (n_bags + 1) * bag, bag, dtype=torch.int64).cuda()
+    want = F.embedding_bag(torch.from_numpy(t.gid_array[:n_bags * bag]).long(), host,
+                           offsets[:-1].cpu(), mode="sum")
+    for k0, k1, tail in pieces:
+        rep.run_chunks(g, k0, k1, tail, bits, pf)
+        rows.refresh()
+        torch.cuda.synchronize()
+        # every resident slot holds exactly its id's host row
+        st = rep.state
+        S, W = C // ways, ways
+        tags = st[64:64 + 4 * S * W].view(torch.int32).cpu().numpy()
+        buf = rows.buf.cpu().numpy()
+        res = tags >= 0
+        assert np.array_equal(buf[res], host.numpy()[tags[res]])
+        out = rows.pool(g[:n_bags * bag], offsets)
+        got = out.cpu()
+        assert torch.equal(got, want), (got - want).abs().max()
+    hb, hh = (int(x) for x in rows.src.cpu().numpy())
+    assert hb + hh == 2 * n_bags * bag and hb > 0
