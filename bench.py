@@ -63,6 +63,8 @@ def parse():
                     help="skip the K5/K6 host-row gather + EmbeddingBag measurement")
     ap.add_argument("--row-dim", type=int, default=128)
     ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
+    ap.add_argument("--pieces", type=int, default=8, help="replay pipeline pieces")
+    ap.add_argument("--model-sms", type=int, default=146, help="SMs the forwards may use")
     return ap.parse_args()
 
 
@@ -234,6 +236,7 @@ def measure_rows(args, hp, n, torch):
             "refresh_pcie_gbs": copied * D * 4 / (t_ref / 1e3) / 1e9,
             "pcie_h2d_peak_gbs": best, "pcie_peak_source": "pinned cudaMemcpy H2D 1 GiB, best of 5",
             "pool_ms": t_pool, "bags": n_bags, "rows_from_hbm": hb, "rows_from_host": hh,
+            "pool_host_pcie_gbs": hh * D * 4 / (t_pool / 1e3) / 1e9,
             "pool_gbs": pool_bytes / (t_pool / 1e3) / 1e9,
             "note": "K5/K6 run after the timed replay; not part of `value`"}
 
@@ -279,7 +282,8 @@ def main():
     t, U, C, C32, cp, emb_c, pp, emb_p, setup_s = build_state(args, rank, torch)
     n = len(t)
     hp = HotPath(DeviceModel(cp, emb_c), DeviceModel(pp, emb_p), t.table_sizes, C32, n,
-                 ways=32, eviction_speed=4, lru_capacity=C32, lru_ways=32)
+                 ways=32, eviction_speed=4, lru_capacity=C32, lru_ways=32,
+                 pieces=args.pieces, model_sms=args.model_sms)
     host = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
     hp.gids[:n].copy_(host)
     torch.cuda.synchronize()
@@ -394,7 +398,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
-        "config": workload(args, 0),
+        "config": dict(workload(args, 0), pipeline_pieces=args.pieces, model_sms=args.model_sms),
         "quality": {"on_demand": c[2], "lru32_misses": c[7],
                     "on_demand_vs_lru32": (c[2] / c[7]) if c[7] else None,
                     "cache_hits": c[0], "prefetch_hits": c[1], "prefetch_issued": c[3],

@@ -32,7 +32,7 @@ class HotPath:
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
                  n_max: int, ways: int | None = 32, eviction_speed: int = 4,
                  lru_capacity: int | None = None, lru_ways: int | None = 32, l_in: int = 15,
-                 l_out: int = 5, window_ratio: int = 3, pieces: int = 4, model_sms: int = 146):
+                 l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 146):
         """pieces > 1 pipelines the replay: chunks are scored in `pieces`
         ranges on the main stream while earlier ranges replay on a side stream
         (recmg_replay_chunks continues the buffer state, so the result is the
