@@ -79,3 +79,41 @@ def test_gloo_world2_counters_sum():
     assert out[0][0] == want and out[1][0] == want
     assert out[0][1] == out[1][1] == assign.tolist()
     assert out[0][2] + out[1][2] == len(t)
+
+
+def _dlrm_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+    from paper_2511_08568_b200 import dlrm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = _trace()
+    assign = shard.assign_tables(shard.table_access_counts(t), world)
+    rows = torch.from_numpy(np.random.default_rng(3).standard_normal((t.total_ids, 8))
+                            .astype(np.float32))
+    pool = lambda ids, offs: F.embedding_bag(ids.long(), rows, offs[:-1], mode="sum")
+    stage = dlrm.DlrmEmbeddingStage(t.table_sizes, assign, rank, world, 8, pool)
+    bags = torch.from_numpy(dlrm.build_bags(t, stage.local_tables, 6, 3, start=rank * 0))
+    out[rank] = stage.forward(bags).numpy()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_dlrm_all_to_all():
+    """Config-4 layout: table-sharded pooling + one all_to_all_single gives
+    every rank the pooled rows of all tables for its block of samples."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2511_08568_b200 import dlrm
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_dlrm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    t = _trace()
+    rows = torch.from_numpy(np.random.default_rng(3).standard_normal((t.total_ids, 8))
+                            .astype(np.float32))
+    all_bags = dlrm.build_bags(t, list(range(len(t.table_sizes))), 6, 3)   # [6, T, 3]
+    want = F.embedding_bag(torch.from_numpy(all_bags.reshape(-1, 3)), rows, mode="sum")
+    want = want.reshape(6, len(t.table_sizes), 8).numpy()
+    assert np.array_equal(out[0], want[:3]) and np.array_equal(out[1], want[3:])

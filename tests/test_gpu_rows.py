@@ -48,3 +48,38 @@ def test_gather_and_pool_vs_torch(dim, ways, bag):
         assert torch.equal(got, want), (got - want).abs().max()
     hb, hh = (int(x) for x in rows.src.cpu().numpy())
     assert hb + hh == 2 * n_bags * bag and hb > 0
+
+
+def test_dlrm_stage_single_rank_nccl():
+    """Config-4 stage on one GPU: replay the batch's accesses (K3), gather
+    changed rows (K5), pool the bags (K6), all-to-all over NCCL (world 1)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+    from paper_2511_08568_b200 import dlrm, shard
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        t = rb.generate_trace(rb.TraceGenConfig([2000] * 6, 30_000, 1.05, 0.4, 32, 8))
+        V, D = t.total_ids, 128
+        host = torch.from_numpy(np.random.default_rng(1).standard_normal((V, D))
+                                .astype(np.float32)).pin_memory()
+        assign = shard.assign_tables(shard.table_access_counts(t), 1)
+        B, P = 64, 2
+        bags = dlrm.build_bags(t, list(range(6)), B, P)
+        flat = bags.reshape(-1)
+        C = 32 * 20
+        rep = BufferReplay(C, V, 4, 32, len(flat))
+        rows = RowStore(rep, host)
+        g = to_device_gids(torch, flat)
+        rep.run(g)
+        rows.refresh()
+        stage = dlrm.DlrmEmbeddingStage(t.table_sizes, assign, 0, 1, D, rows.pool)
+        got = stage.forward(torch.from_numpy(bags).cuda()).cpu()
+        want = F.embedding_bag(torch.from_numpy(flat.reshape(-1, P)), host, mode="sum")
+        assert torch.equal(got, want.reshape(B, 6, D))
+    finally:
+        dist.destroy_process_group()
