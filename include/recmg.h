@@ -48,7 +48,10 @@ const char *recmg_status_category(int status);
 
 /* ---- buffer configuration --------------------------------------------- */
 enum { RECMG_POLICY_PRIORITY = 0, /* Alg. 1/2 priority-decay buffer (runtime.py:41-141) */
-       RECMG_POLICY_LRU = 1 };    /* LRU comparator (cache_sim.py:92-106)              */
+       RECMG_POLICY_LRU = 1,      /* LRU comparator (cache_sim.py:92-106)              */
+       RECMG_POLICY_LRU_PF = 2 }; /* LRU + prefetch tags: replay_policy_only with a
+                                     prefetcher (runtime.py:304-349); recmg_replay
+                                     ignores the bits; capacity <= 4096 ways      */
 
 typedef struct {
     int64_t capacity;       /* BufferConfig.capacity (runtime.py:29-38) /

@@ -27,6 +27,7 @@ RECMG_E_WORKSPACE = -7
 
 POLICY_PRIORITY = 0
 POLICY_LRU = 1
+POLICY_LRU_PF = 2
 OP_ADD, OP_POPULATE, OP_REFERENCE, OP_SET_PRIORITY, OP_QUERY = range(5)
 MODEL_CACHING, MODEL_PREFETCH = 0, 1
 PREC_FP32 = 0

@@ -33,7 +33,9 @@ bool plan_replay(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in, int32_t l
                  int32_t window_ratio, int32_t pf_stride, bool with_class, int64_t k_begin,
                  int64_t k_end, bool with_tail, Arena &a, ReplayPlan &p) {
     if (!geometry_of(cfg, &p.g)) return false;
-    if (cfg->policy != RECMG_POLICY_PRIORITY || cfg->eviction_speed < 1) return false;
+    if (cfg->policy != RECMG_POLICY_PRIORITY && cfg->policy != RECMG_POLICY_LRU_PF) return false;
+    if (cfg->policy == RECMG_POLICY_PRIORITY && cfg->eviction_speed < 1) return false;
+    if (cfg->policy == RECMG_POLICY_LRU_PF && p.g.W > kSmemMaxWays) return false;
     if (n < 0 || l_in < 1 || l_out < 1 || window_ratio < 1 || pf_stride < 0) return false;
     if ((int64_t)window_ratio * l_out > 255) return false;  // uint8 coverage counts
     p.K = recmg_num_chunks(n, l_in, l_out, window_ratio);
@@ -101,7 +103,14 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     ra.st = st;
     ra.ctr = counters;
     ra.access_class = access_class;
-    return launch_replay(RECMG_POLICY_PRIORITY, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
+    int rc = launch_replay(cfg->policy, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
+    if (rc) return rc;
+    if (cfg->policy == RECMG_POLICY_LRU_PF) {
+        // clocks are event positions of this call: keep them monotonic across calls
+        clock_bump_kernel<<<1, 1, 0, s>>>(st.header, p.E);
+        RECMG_LAUNCH_CHECK();
+    }
+    return RECMG_OK;
 }
 
 }  // namespace

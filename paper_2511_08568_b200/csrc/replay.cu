@@ -311,6 +311,11 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
     unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
     const unsigned lt = (1u << lane) - 1u;
     int64_t free_hint = 0;
+    // LRU_PF (replay_policy_only with a prefetcher, runtime.py:318-339):
+    // meta = clock | prefetch tag << 62; keep-bit updates do not exist there
+    constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
+    constexpr bool LRUPF = (POLICY == RECMG_POLICY_LRU_PF);
+    constexpr int64_t kClockMask = (int64_t(1) << 62) - 1;
 
     // Apply the hit-run part held by one 32-event half (events base+lane,
     // lane < n_run): group by way, the group leader updates its way.
@@ -319,7 +324,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
         const bool inrun = way >= 0 && lane < n_run;
         const unsigned peers = __match_any_sync(FULL, inrun ? (unsigned)way : (0x80000000u | lane));
         const int leader = 31 - __clz(peers);
-        if (POLICY == RECMG_POLICY_PRIORITY) {
+        if (PRIO) {
             const unsigned Smask = __ballot_sync(FULL, inrun && ty == EV_SERVE);
             const unsigned UPmask = __ballot_sync(FULL, inrun && ty != EV_SERVE);
             const unsigned U1mask = __ballot_sync(FULL, inrun && ty == EV_UPD1);
@@ -348,6 +353,29 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                     write_class(a, base + lane, (f0 && first) ? 1 : 0);
                 }
             }
+        } else if (LRUPF) {
+            // S hits: first S on a tagged way is the prefetch hit, the way moves
+            // to MRU at its last S; P hits change nothing (runtime.py:318-325,336)
+            const unsigned Smask = __ballot_sync(FULL, inrun && ty == EV_SERVE);
+            bool flag0 = false;
+            if (inrun && lane == leader) {
+                const unsigned sp = peers & Smask;
+                if (sp) {
+                    const int64_t m0 = v.meta[way];
+                    flag0 = (m0 >> 62) & 1;
+                    const unsigned c = __popc(sp);
+                    if (flag0) { ph += 1; ch += c - 1; }
+                    else ch += c;
+                    v.meta[way] = clock_base + base + (31 - __clz(sp));
+                }
+            }
+            if (CLASS) {
+                const bool f0 = __shfl_sync(FULL, flag0, leader);
+                if (inrun && ty == EV_SERVE) {
+                    const bool first = ((peers & Smask) & lt) == 0;
+                    write_class(a, base + lane, (f0 && first) ? 1 : 0);
+                }
+            }
         } else {
             if (inrun && lane == leader) {
                 v.meta[way] = clock_base + base + leader;
@@ -368,11 +396,15 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
         const uint32_t e0 = v0 ? ring.at(pos - lo + lane) : 0u;
         const uint32_t e1 = v1 ? ring.at(pos - lo + 32 + lane) : 0u;
         const uint32_t g0 = ev_gid(e0), g1 = ev_gid(e1);
-        const bool real0 = v0 && g0 != kGidMask, real1 = v1 && g1 != kGidMask;
+        bool real0 = v0 && g0 != kGidMask, real1 = v1 && g1 != kGidMask;
+        if (LRUPF) {
+            real0 = real0 && (ev_type(e0) == EV_SERVE || ev_type(e0) == EV_PREFETCH);
+            real1 = real1 && (ev_type(e1) == EV_SERVE || ev_type(e1) == EV_PREFETCH);
+        }
         const int way0 = real0 ? ht_find(v, g0) : -1;
         const int way1 = real1 ? ht_find(v, g1) : -1;
         unsigned miss0, miss1;
-        if (POLICY == RECMG_POLICY_PRIORITY) {
+        if (PRIO || LRUPF) {
             const uint32_t t0 = ev_type(e0), t1 = ev_type(e1);
             miss0 = __ballot_sync(FULL, real0 && way0 < 0 && (t0 == EV_SERVE || t0 == EV_PREFETCH));
             miss1 = __ballot_sync(FULL, real1 && way1 < 0 && (t1 == EV_SERVE || t1 == EV_PREFETCH));
@@ -389,7 +421,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             const uint32_t ec = __shfl_sync(FULL, e, cut & 31);
             const uint32_t gc = ev_gid(ec);
             const uint32_t tc = ev_type(ec);
-            if (POLICY == RECMG_POLICY_PRIORITY) {
+            if (PRIO || LRUPF) {
                 if (tc == EV_SERVE) {
                     od++;
                     if (CLASS && lane == 0) write_class(a, pos + cut, 2);
@@ -410,9 +442,9 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                     const int32_t t = v.tags[w];
                     if (t < 0) continue;
                     const int64_t m = v.meta[w];
-                    const unsigned long long key = (POLICY == RECMG_POLICY_PRIORITY)
+                    const unsigned long long key = PRIO
                         ? (((unsigned long long)(uint32_t)m << 32) | (uint32_t)t)
-                        : (unsigned long long)m;
+                        : (unsigned long long)(m & kClockMask);
                     if (key < best) { best = key; bslot = w; }
                 }
 #pragma unroll
@@ -421,7 +453,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                     const int os = __shfl_xor_sync(FULL, bslot, o);
                     if (ob < best) { best = ob; bslot = os; }
                 }
-                if (POLICY == RECMG_POLICY_PRIORITY) {
+                if (PRIO) {
                     for (int w = lane; w < W; w += 32) {
                         if (v.tags[w] < 0) continue;
                         const int64_t m = v.meta[w];
@@ -451,9 +483,9 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             __syncwarp();
             if (lane == 0) {
                 v.tags[target] = (int32_t)gc;
-                v.meta[target] = (POLICY == RECMG_POLICY_PRIORITY)
+                v.meta[target] = PRIO
                     ? ((int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32))
-                    : (clock_base + pos + cut);
+                    : ((clock_base + pos + cut) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0));
                 ht_insert(v, gc, (uint32_t)target);
             }
             count++;
@@ -470,7 +502,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
         a.st.meta[sbase + w] = v.meta[w];
     }
     if (lane == 0) a.st.count[set] = count;
-    if (POLICY == RECMG_POLICY_PRIORITY) {
+    if (PRIO || LRUPF) {
         ch = __reduce_add_sync(FULL, (unsigned)ch);
         ph = __reduce_add_sync(FULL, (unsigned)ph);
         if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
@@ -785,11 +817,15 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, true);
             else RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, false);
+        } else if (policy == RECMG_POLICY_LRU_PF) {
+            if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU_PF, true);
+            else RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU_PF, false);
         } else {
             RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU, false);
         }
 #undef RECMG_SMEM_LAUNCH
     } else {
+        if (policy == RECMG_POLICY_LRU_PF) return RECMG_E_INVALID_CONFIG;  // <= 4096 ways only
         if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) replay_wide_kernel<RECMG_POLICY_PRIORITY, true><<<(unsigned)nsets, 32, 0, s>>>(a);
             else replay_wide_kernel<RECMG_POLICY_PRIORITY, false><<<(unsigned)nsets, 32, 0, s>>>(a);

@@ -18,11 +18,12 @@ class BufferReplay:
     """recmg_replay: chunked replay through the priority buffer."""
 
     def __init__(self, capacity, total_ids, eviction_speed=4, ways=None, n=0, l_in=15,
-                 l_out=5, window_ratio=3, pf_stride=0):
+                 l_out=5, window_ratio=3, pf_stride=0, policy=None):
         torch = _native.torch_cuda()
         L = _native.lib()
         self.torch = torch
-        self.cfg = _native.buffer_cfg(capacity, ways, eviction_speed, _native.POLICY_PRIORITY,
+        self.cfg = _native.buffer_cfg(capacity, ways, eviction_speed,
+                                      _native.POLICY_PRIORITY if policy is None else policy,
                                       total_ids)
         sb = L.recmg_buffer_state_bytes(ctypes.byref(self.cfg))
         if sb == 0:

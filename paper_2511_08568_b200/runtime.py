@@ -311,7 +311,32 @@ def replay_policy_only(trace, cache_cfg: CacheConfig, prefetch_params=None, pref
     if cache_cfg.policy != Policy.LRU or cache_cfg.ways is not None:
         raise InvalidConfigError("prefetch-augmented baseline supports fully associative LRU only")
     _check_vocab(prefetch_params, trace)
-    raise NotImplementedError("LRU + prefetch baseline is not on the GPU path yet")
+    # fully associative LRU with prefetch tags (runtime.py:309-349) on the
+    # replay engine's LRU_PF policy: S = serve (hit -> MRU, first hit on a
+    # prefetched row counts as a prefetch hit), P = insert at MRU if absent
+    gids = np.asarray(trace.gid_array)
+    n = len(gids)
+    K = num_chunks(n, l_in, l_out, window_ratio)
+    samples = chunk(trace, l_in, l_out, window_ratio) if prefetch_fn is not None else None
+    hpf = _host_prefetches(prefetch_fn, samples, trace.total_ids) \
+        if prefetch_fn is not None and K else None
+    torch = _native.torch_cuda()
+    gdev = to_device_gids(torch, gids)
+    if prefetch_fn is not None:
+        pf = torch.from_numpy(hpf).cuda() if hpf is not None else None
+    else:
+        p = prefetch_params
+        if p.l_in != l_in or p.l_out != l_out:
+            p = ModelParameters(p.kind, p.table_sizes, p.dim, p.stacks, l_in, l_out, p.arrays)
+        pf = _gpu_prefetches(torch, p, gdev, K, l_in)
+    eng = BufferReplay(cache_cfg.capacity, trace.total_ids, 1, None, n, l_in, l_out,
+                       window_ratio, pf.shape[1] if pf is not None else 0,
+                       policy=_native.POLICY_LRU_PF)
+    eng.run(gdev, None, pf)
+    r = eng.result()
+    return BreakdownReport(r["cache_hits"], r["prefetch_hits"], r["on_demand"],
+                           r["prefetch_issued"], r["prefetch_useful"], r["coverage"],
+                           r["evictions"], r["prefetch_inserts"])
 
 
 def correctness_vs_window(trace, prefetch_params: ModelParameters, ratios, l_in=None,

@@ -182,3 +182,33 @@ def test_config1_golden_counts_on_gpu():
                 rep.prefetch_inserts] == list(z[f"w32_es{es_name}"][:5])
     res = rb.simulate(t, rb.CacheConfig(C32, rb.Policy.LRU, 32), per_access=False)
     assert res.misses == int(z["lru32_misses"])
+
+
+def test_lru_plus_prefetch_vs_reference(small):
+    """replay_policy_only with a prefetcher (runtime.py:304-349) == reference."""
+    t = rb.trace_from_gids(small["gids"], [int(x) for x in small["table_sizes"]])
+    pf = small["opt_pf"]
+    rep = rb.replay_policy_only(t, rb.CacheConfig(24, rb.Policy.LRU),
+                                prefetch_fn=lambda s: [int(g) for g in pf[s.origin // 15] if g >= 0])
+    assert [rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
+            rep.prefetch_useful] == list(small["lrupf_counts"])
+    assert rep.coverage == float(small["lrupf_coverage"])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_lru_plus_prefetch_random_vs_oracle(seed):
+    rng = np.random.default_rng(50 + seed)
+    V = int(rng.integers(50, 2000))
+    n = int(rng.integers(500, 30000))
+    gids = (rng.zipf(1.2, n) - 1) % V
+    K = rb.num_chunks(n)
+    pf = rng.integers(0, V, (K, 5))
+    pf[np.arange(5)[None, :] >= rng.integers(0, 6, K)[:, None]] = -1
+    t = rb.trace_from_gids(gids, [V])
+    for cap in (1, 7, int(rng.integers(8, 300))):
+        rep = rb.replay_policy_only(t, rb.CacheConfig(cap, rb.Policy.LRU),
+                                    prefetch_fn=lambda s: [int(g) for g in pf[s.origin // 15] if g >= 0])
+        ref, cov = oracle.lru_prefetch(gids, V, cap, pf)
+        assert [rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
+                rep.prefetch_useful] == [ref[k] for k in NAMES[:5]], cap
+        assert rep.coverage == cov
