@@ -49,9 +49,13 @@ const char *recmg_status_category(int status);
 /* ---- buffer configuration --------------------------------------------- */
 enum { RECMG_POLICY_PRIORITY = 0, /* Alg. 1/2 priority-decay buffer (runtime.py:41-141) */
        RECMG_POLICY_LRU = 1,      /* LRU comparator (cache_sim.py:92-106)              */
-       RECMG_POLICY_LRU_PF = 2 }; /* LRU + prefetch tags: replay_policy_only with a
+       RECMG_POLICY_LRU_PF = 2,   /* LRU + prefetch tags: replay_policy_only with a
                                      prefetcher (runtime.py:304-349); recmg_replay
                                      ignores the bits; capacity <= 4096 ways      */
+       RECMG_POLICY_LFU = 3,      /* cache_sim.py:109-137 (ties -> least recent)   */
+       RECMG_POLICY_SRRIP = 4,    /* cache_sim.py:140-170; max rrpv in
+                                     eviction_speed                                */
+       RECMG_POLICY_OPTGEN = 5 }; /* Belady / optgen, cache_sim.py:173-249          */
 
 typedef struct {
     int64_t capacity;       /* BufferConfig.capacity (runtime.py:29-38) /
@@ -133,12 +137,19 @@ double recmg_coverage_mean(const uint8_t *host_num, const uint8_t *host_den, int
 
 /* ---- policy-only simulation  (cache_sim.py:223-260, LRU) --------------- */
 int recmg_simulate_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, size_t *bytes);
-/* simulate(trace, CacheConfig(capacity, Policy.LRU, ways)): hits/misses
+/* simulate(trace, CacheConfig(capacity, policy, ways)) for LRU, and for
+ * LFU / SRRIP / OPTGEN with at most 4096 ways per set: hits/misses
  * accumulated into device int64[2]; per_access_hit[n] (nullable) as
- * SimResult.per_access_hit.                                                 */
+ * SimResult.per_access_hit.  Use recmg_simulate_ex for OPTGEN keep bits.    */
 int recmg_simulate(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                    uint8_t *per_access_hit, int64_t *hits_misses, void *ws, size_t ws_bytes,
                    void *stream);
+
+/* As recmg_simulate, plus keep_decisions[n] (OPTGEN only, nullable):
+ * SimResult.keep_decisions of simulate_optgen (cache_sim.py:199-220).       */
+int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                      uint8_t *per_access_hit, uint8_t *keep_decisions, int64_t *hits_misses,
+                      void *ws, size_t ws_bytes, void *stream);
 
 /* ---- single buffer operations (PriorityBuffer object API) -------------- */
 enum {

@@ -5,7 +5,7 @@ The compute runs in hand-written sm_100a kernels (csrc/) behind the C ABI
 in include/recmg.h, loaded from the in-tree librecmg.so; there is no CPU
 fallback on this path.
 """
-from .cache_sim import CacheConfig, Policy, SimResult, simulate
+from .cache_sim import CacheConfig, Policy, SimResult, simulate, simulate_optgen, sweep
 from .errors import (CheckpointError, EmbcacheError, InvalidConfigError,
                      MissingArtifactError, NumericalError, OutOfVocabularyError,
                      TraceParseError, TraceValidationError, VocabularyMismatchError)

@@ -28,6 +28,9 @@ RECMG_E_WORKSPACE = -7
 POLICY_PRIORITY = 0
 POLICY_LRU = 1
 POLICY_LRU_PF = 2
+POLICY_LFU = 3
+POLICY_SRRIP = 4
+POLICY_OPTGEN = 5
 OP_ADD, OP_POPULATE, OP_REFERENCE, OP_SET_PRIORITY, OP_QUERY = range(5)
 MODEL_CACHING, MODEL_PREFETCH = 0, 1
 PREC_FP32 = 0
@@ -43,6 +46,7 @@ EXPORTS = (
     "recmg_launch_count", "recmg_selftest_umma", "recmg_model_pack_tc",
     "recmg_model_workspace_bytes", "recmg_replay_chunks", "recmg_set_model_sm_budget",
     "recmg_model_forward_profile", "recmg_rows_refresh", "recmg_embedding_bag",
+    "recmg_simulate_ex",
 )
 
 
@@ -95,6 +99,7 @@ def lib():
         "recmg_model_forward_profile": (ctypes.c_int, [shp, vp, vp, vp, i64, vp, vp, sz, vp, vp]),
         "recmg_simulate_workspace_bytes": (ctypes.c_int, [cfgp, i64, ctypes.POINTER(sz)]),
         "recmg_simulate": (ctypes.c_int, [cfgp, vp, vp, i64, vp, vp, vp, sz, vp]),
+        "recmg_simulate_ex": (ctypes.c_int, [cfgp, vp, vp, i64, vp, vp, vp, vp, sz, vp]),
         "recmg_buffer_op": (ctypes.c_int, [cfgp, vp, i32, i64, i64, i32, vp, vp]),
         "recmg_model_dense_floats": (i64, [shp]),
         "recmg_model_packed_bytes": (sz, [shp, i32]),

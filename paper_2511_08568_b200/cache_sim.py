@@ -1,8 +1,8 @@
-"""Cache simulators (cache_sim.py of the reference): the LRU comparator on
-the GPU (K4: recmg_simulate, set = gid % set_count, cache_sim.py:92-106).
-
-LFU / SRRIP / optgen (cache_sim.py:109-220) are SURVEY.md §8(f) "next"
-items and are not on the GPU path yet: asking for them raises.
+"""Cache simulators (cache_sim.py of the reference) on the GPU: LRU (the
+32-way comparator, K4), LFU, SRRIP and the offline optimum (optgen / Belady
+with keep decisions) as policies of the replay engine's shared-memory set
+kernel (set = gid % set_count, cache_sim.py:33-35).  LFU / SRRIP / OPTGEN
+support up to 4096 ways per set (fully associative: capacity <= 4096).
 """
 from __future__ import annotations
 
@@ -68,22 +68,51 @@ def _gids_of(trace) -> np.ndarray:
     return np.asarray(trace, dtype=np.int64)
 
 
-def simulate(trace, cfg: CacheConfig, per_access: bool = True) -> SimResult:
-    """cache_sim.py:223-260 for Policy.LRU, on the GPU."""
-    cfg.validate()
-    if cfg.policy != Policy.LRU:
-        raise NotImplementedError(f"{cfg.policy.value} is not on the GPU path yet "
-                                  "(SURVEY.md §8(f) next #3/#4)")
-    from .engine import LruSim, to_device_gids
+def _run(trace, capacity, ways, policy, srrip_max_rrpv=3, per_access=True, keep=False):
+    from .engine import SetSim, to_device_gids
     torch = _native.torch_cuda()
     gids = _gids_of(trace)
     if len(gids) == 0:
-        return SimResult(0, 0, [])
+        return SimResult(0, 0, [], [] if keep else None)
     total_ids = int(gids.max()) + 1
     if hasattr(trace, "total_ids"):
         total_ids = max(total_ids, int(trace.total_ids))
-    sim = LruSim(cfg.capacity, total_ids, cfg.ways, len(gids))
-    pa = torch.empty(len(gids), dtype=torch.uint8, device="cuda") if per_access else None
-    sim.run(to_device_gids(torch, gids), pa)
+    sim = SetSim(capacity, total_ids, ways, len(gids), policy, srrip_max_rrpv)
+    pa = torch.empty(len(gids), dtype=torch.uint8, device="cuda") \
+        if (per_access or keep) else None
+    kd = torch.empty(len(gids), dtype=torch.uint8, device="cuda") if keep else None
+    sim.run(to_device_gids(torch, gids), pa, kd)
     hits, misses = sim.result()
-    return SimResult(hits, misses, pa.cpu().numpy().tolist() if per_access else [])
+    return SimResult(hits, misses, pa.cpu().numpy().tolist() if per_access else [],
+                     kd.cpu().numpy().tolist() if keep else None)
+
+
+def simulate(trace, cfg: CacheConfig, per_access: bool = True) -> SimResult:
+    """cache_sim.py:223-260 on the GPU."""
+    cfg.validate()
+    if cfg.policy == Policy.OPTGEN:
+        return _run(trace, cfg.capacity if cfg.set_count > 1 else cfg.ways_per_set,
+                    cfg.ways if cfg.set_count > 1 else None, "optgen", per_access=per_access,
+                    keep=True)
+    return _run(trace, cfg.capacity, cfg.ways, cfg.policy.value, cfg.srrip_max_rrpv,
+                per_access=per_access)
+
+
+def simulate_optgen(trace, capacity: int) -> SimResult:
+    """cache_sim.py:199-220: fully associative Belady with keep decisions."""
+    if capacity < 1:
+        raise InvalidConfigError("capacity must be >= 1")
+    return _run(trace, capacity, None, "optgen", keep=True)
+
+
+def sweep(trace, policies, capacities, ways=None) -> list:
+    """cache_sim.py:304-320."""
+    rows = []
+    for policy in policies:
+        for cap in capacities:
+            w = ways if ways is not None and policy != Policy.OPTGEN else None
+            res = simulate(trace, CacheConfig(capacity=cap, policy=policy, ways=w),
+                           per_access=False)
+            rows.append({"policy": policy.value, "capacity": cap, "hits": res.hits,
+                         "misses": res.misses, "hit_rate": res.hit_rate})
+    return rows

@@ -213,17 +213,44 @@ double recmg_coverage_mean(const uint8_t *num, const uint8_t *den, int64_t K) {
     return K ? acc / (double)K : 0.0;
 }
 
+static bool sim_policy_ok(const recmg_buffer_cfg *cfg, const Geometry &g) {
+    switch (cfg->policy) {
+        case RECMG_POLICY_LRU: return true;
+        case RECMG_POLICY_LFU:
+        case RECMG_POLICY_OPTGEN: return g.W <= kSmemMaxWays;
+        case RECMG_POLICY_SRRIP: return g.W <= kSmemMaxWays && cfg->eviction_speed >= 0;
+        default: return false;
+    }
+}
+
+struct SimPlan {
+    uint32_t *keys = nullptr, *vals = nullptr;
+    PartitionBuffers pb, pb_id;        // by set; by id (OPTGEN next use)
+    int32_t *next_use = nullptr;
+    uint8_t *hit = nullptr;            // OPTGEN keep bits need the hits
+    uint32_t *ids = nullptr, *pos = nullptr;
+};
+
+static void plan_sim(const recmg_buffer_cfg *cfg, const Geometry &g, int64_t n, bool keep,
+                     bool have_hits, Arena &a, SimPlan &p) {
+    p.keys = a.take<uint32_t>((size_t)n);
+    p.vals = a.take<uint32_t>((size_t)n);
+    if (g.S > 1) partition_plan(a, p.pb, n, g.S, true);
+    if (cfg->policy == RECMG_POLICY_OPTGEN) {
+        p.next_use = a.take<int32_t>((size_t)n);
+        p.ids = a.take<uint32_t>((size_t)n);
+        p.pos = a.take<uint32_t>((size_t)n);
+        partition_plan(a, p.pb_id, n, cfg->total_ids, true);
+        if (keep && !have_hits) p.hit = a.take<uint8_t>((size_t)n);
+    }
+}
+
 int recmg_simulate_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, size_t *bytes) {
     Geometry g;
-    if (!geometry_of(cfg, &g) || cfg->policy != RECMG_POLICY_LRU || n < 0)
-        return RECMG_E_INVALID_CONFIG;
+    if (!geometry_of(cfg, &g) || !sim_policy_ok(cfg, g) || n < 0) return RECMG_E_INVALID_CONFIG;
     Arena a{nullptr, 0, 0};
-    a.take<uint32_t>((size_t)n);  // keys copy
-    a.take<uint32_t>((size_t)n);  // positions
-    if (g.S > 1) {
-        PartitionBuffers pb;
-        partition_plan(a, pb, n, g.S, true);
-    }
+    SimPlan p;
+    plan_sim(cfg, g, n, true, false, a, p);
     *bytes = a.used + 256;
     return RECMG_OK;
 }
@@ -236,45 +263,68 @@ __global__ void iota_copy_kernel(const int32_t *in, uint32_t *keys, uint32_t *va
     }
 }
 
-int recmg_simulate(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
-                   uint8_t *per_access_hit, int64_t *hits_misses, void *ws, size_t ws_bytes,
-                   void *stream) {
+int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                      uint8_t *per_access_hit, uint8_t *keep_decisions, int64_t *hits_misses,
+                      void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t s = as_stream(stream);
     Geometry g;
-    if (!geometry_of(cfg, &g) || cfg->policy != RECMG_POLICY_LRU || !state || n < 0)
+    if (!geometry_of(cfg, &g) || !sim_policy_ok(cfg, g) || !state || n < 0)
         return RECMG_E_INVALID_CONFIG;
+    if (keep_decisions && cfg->policy != RECMG_POLICY_OPTGEN) return RECMG_E_INVALID_CONFIG;
     if (n == 0) return RECMG_OK;
     Arena a{(char *)ws, ws_bytes, 0};
-    uint32_t *keys = a.take<uint32_t>((size_t)n);
-    uint32_t *vals = a.take<uint32_t>((size_t)n);
-    PartitionBuffers pb;
-    if (g.S > 1) partition_plan(a, pb, n, g.S, true);
+    SimPlan p;
+    plan_sim(cfg, g, n, keep_decisions != nullptr, per_access_hit != nullptr, a, p);
     if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
-    iota_copy_kernel<<<(unsigned)imin64((n + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
-        gids, keys, vals, n);
+    const unsigned grid = (unsigned)imin64((n + 255) / 256, 16 * kSmCount);
+    uint8_t *hit = per_access_hit ? per_access_hit : p.hit;
+    if (cfg->policy == RECMG_POLICY_OPTGEN) {
+        // next use of every access: stable sort by id, neighbours (cache_sim.py:80-89)
+        iota_copy_kernel<<<grid, 256, 0, s>>>(gids, p.ids, p.pos, n);
+        RECMG_LAUNCH_CHECK();
+        uint32_t *ki = p.ids, *vi = p.pos;
+        int rc = partition_run(p.pb_id, ki, vi, s);
+        if (rc) return rc;
+        next_use_kernel<<<grid, 256, 0, s>>>(ki, vi, n, p.next_use);
+        RECMG_LAUNCH_CHECK();
+    }
+    iota_copy_kernel<<<grid, 256, 0, s>>>(gids, p.keys, p.vals, n);
     RECMG_LAUNCH_CHECK();
     ReplayArgs ra;
     memset(&ra, 0, sizeof(ra));
-    uint32_t *k = keys, *v = vals;
+    uint32_t *k = p.keys, *v = p.vals;
     if (g.S > 1) {
-        int rc = partition_run(pb, k, v, s);
+        int rc = partition_run(p.pb, k, v, s);
         if (rc) return rc;
-        ra.seg_start = pb.seg_start;
-        ra.seg_end = pb.seg_end;
+        ra.seg_start = p.pb.seg_start;
+        ra.seg_end = p.pb.seg_end;
     }
     ra.ev = k;
     ra.vals = v;
     ra.E = n;
     ra.S = g.S;
     ra.W = g.W;
+    ra.es = cfg->eviction_speed;            // SRRIP: max rrpv
     ra.st = state_view(state, cfg, g);
     ra.hits_misses = hits_misses;
-    ra.per_access_hit = per_access_hit;
-    int rc = launch_replay(RECMG_POLICY_LRU, !g.wide, false, ra, g.S, s);
+    ra.per_access_hit = hit;
+    ra.next_use = p.next_use;
+    int rc = launch_replay(cfg->policy, !g.wide, false, ra, g.S, s);
     if (rc) return rc;
     clock_bump_kernel<<<1, 1, 0, s>>>(ra.st.header, n);
     RECMG_LAUNCH_CHECK();
+    if (keep_decisions) {
+        keep_kernel<<<grid, 256, 0, s>>>(p.next_use, hit, n, keep_decisions);
+        RECMG_LAUNCH_CHECK();
+    }
     return RECMG_OK;
+}
+
+int recmg_simulate(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
+                   uint8_t *per_access_hit, int64_t *hits_misses, void *ws, size_t ws_bytes,
+                   void *stream) {
+    return recmg_simulate_ex(cfg, state, gids, n, per_access_hit, nullptr, hits_misses, ws,
+                             ws_bytes, stream);
 }
 
 int recmg_buffer_op(const recmg_buffer_cfg *cfg, void *state, int32_t op, int64_t gid,

@@ -316,6 +316,16 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
     constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
     constexpr bool LRUPF = (POLICY == RECMG_POLICY_LRU_PF);
     constexpr int64_t kClockMask = (int64_t(1) << 62) - 1;
+    // simulate() policies (cache_sim.py:92-249), serve events only:
+    //   LRU    meta = clock of the last use                victim min clock
+    //   LFU    meta = freq << 40 | clock of the last use   victim min (freq, clock)
+    //   SRRIP  meta = rrpv                                 victim first way with
+    //          rrpv >= max after aging (max_rrpv in a.es)
+    //   OPTGEN meta = next use of the last access          victim max next use,
+    //          ties (never used again) -> smallest gid
+    constexpr bool LFU = (POLICY == RECMG_POLICY_LFU);
+    constexpr bool SRRIP = (POLICY == RECMG_POLICY_SRRIP);
+    constexpr bool OPT = (POLICY == RECMG_POLICY_OPTGEN);
 
     // Apply the hit-run part held by one 32-event half (events base+lane,
     // lane < n_run): group by way, the group leader updates its way.
@@ -377,8 +387,15 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 }
             }
         } else {
+            int64_t nu = 0;
+            if (OPT && inrun && lane == leader)
+                nu = a.next_use[a.vals ? a.vals[base + lane] : base + lane];
             if (inrun && lane == leader) {
-                v.meta[way] = clock_base + base + leader;
+                const int64_t clk = clock_base + base + leader;
+                if (LFU) v.meta[way] = (((v.meta[way] >> 40) + __popc(peers)) << 40) | clk;
+                else if (SRRIP) v.meta[way] = 0;
+                else if (OPT) v.meta[way] = nu;
+                else v.meta[way] = clk;
                 lhits += __popc(peers);
             }
             if (a.per_access_hit && lane < n_run)
@@ -442,10 +459,34 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                     const int32_t t = v.tags[w];
                     if (t < 0) continue;
                     const int64_t m = v.meta[w];
-                    const unsigned long long key = PRIO
-                        ? (((unsigned long long)(uint32_t)m << 32) | (uint32_t)t)
-                        : (unsigned long long)(m & kClockMask);
+                    unsigned long long key;
+                    if (PRIO) key = ((unsigned long long)(uint32_t)m << 32) | (uint32_t)t;
+                    else if (OPT) key = ((unsigned long long)((int64_t(1) << 31) - m) << 32) | (uint32_t)t;
+                    else if (SRRIP) key = (unsigned long long)w;   // chosen below
+                    else if (LFU) key = (unsigned long long)m;
+                    else key = (unsigned long long)(m & kClockMask);
                     if (key < best) { best = key; bslot = w; }
+                }
+                if (SRRIP) {
+                    // age until some way reaches max (cache_sim.py:158-165), then
+                    // take the first such way in slot order
+                    int64_t mx = 0;
+                    for (int w = lane; w < W; w += 32)
+                        if (v.tags[w] >= 0) mx = v.meta[w] > mx ? v.meta[w] : mx;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const int64_t om = __shfl_xor_sync(FULL, mx, o);
+                        mx = om > mx ? om : mx;
+                    }
+                    const int64_t dlt = (int64_t)a.es - mx;
+                    best = ~0ull;
+                    bslot = -1;
+                    for (int w = lane; w < W; w += 32) {
+                        if (v.tags[w] < 0) continue;
+                        const int64_t r = v.meta[w] + (dlt > 0 ? dlt : 0);
+                        if (dlt > 0) v.meta[w] = r;
+                        if (r >= a.es && (unsigned long long)w < best) { best = (unsigned long long)w; bslot = w; }
+                    }
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -483,9 +524,13 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             __syncwarp();
             if (lane == 0) {
                 v.tags[target] = (int32_t)gc;
-                v.meta[target] = PRIO
-                    ? ((int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32))
-                    : ((clock_base + pos + cut) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0));
+                int64_t m;
+                if (PRIO) m = (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
+                else if (LFU) m = (int64_t(1) << 40) | (clock_base + pos + cut);
+                else if (SRRIP) m = a.es > 1 ? a.es - 1 : 0;
+                else if (OPT) m = a.next_use[a.vals ? a.vals[pos + cut] : pos + cut];
+                else m = (clock_base + pos + cut) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0);
+                v.meta[target] = m;
                 ht_insert(v, gc, (uint32_t)target);
             }
             count++;
@@ -710,6 +755,29 @@ __global__ void state_reset_kernel(StateView st, int64_t SW, int64_t S, int64_t 
 
 __global__ void clock_bump_kernel(int64_t *header, int64_t by) { header[0] += by; }
 
+// next_use[i] = index of the next access to gids[i] (n if none), from the
+// accesses stably sorted by id (cache_sim.py:80-89)
+__global__ void next_use_kernel(const uint32_t *__restrict__ sorted_ids,
+                                const uint32_t *__restrict__ sorted_pos, int64_t n,
+                                int32_t *__restrict__ next_use) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool more = i + 1 < n && sorted_ids[i + 1] == sorted_ids[i];
+        next_use[sorted_pos[i]] = more ? (int32_t)sorted_pos[i + 1] : (int32_t)n;
+    }
+}
+
+// keep[i] = 1 exactly when the next reference to the block hits
+// (simulate_optgen keep_decisions, cache_sim.py:214-218)
+__global__ void keep_kernel(const int32_t *__restrict__ next_use, const uint8_t *__restrict__ hit,
+                            int64_t n, uint8_t *__restrict__ keep) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = next_use[i];
+        keep[i] = (j < n && hit[j]) ? 1 : 0;
+    }
+}
+
 // Single PriorityBuffer operation on set (gid % S); one warp.
 __global__ void buffer_op_kernel(StateView st, int64_t S, int64_t W, int32_t op, int64_t gid,
                                  int64_t arg, int32_t flag, int64_t *result) {
@@ -820,12 +888,19 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         } else if (policy == RECMG_POLICY_LRU_PF) {
             if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU_PF, true);
             else RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU_PF, false);
+        } else if (policy == RECMG_POLICY_LFU) {
+            RECMG_SMEM_LAUNCH(RECMG_POLICY_LFU, false);
+        } else if (policy == RECMG_POLICY_SRRIP) {
+            RECMG_SMEM_LAUNCH(RECMG_POLICY_SRRIP, false);
+        } else if (policy == RECMG_POLICY_OPTGEN) {
+            RECMG_SMEM_LAUNCH(RECMG_POLICY_OPTGEN, false);
         } else {
             RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU, false);
         }
 #undef RECMG_SMEM_LAUNCH
     } else {
-        if (policy == RECMG_POLICY_LRU_PF) return RECMG_E_INVALID_CONFIG;  // <= 4096 ways only
+        if (policy != RECMG_POLICY_PRIORITY && policy != RECMG_POLICY_LRU)
+            return RECMG_E_INVALID_CONFIG;   // the other policies: <= 4096 ways per set
         if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) replay_wide_kernel<RECMG_POLICY_PRIORITY, true><<<(unsigned)nsets, 32, 0, s>>>(a);
             else replay_wide_kernel<RECMG_POLICY_PRIORITY, false><<<(unsigned)nsets, 32, 0, s>>>(a);

@@ -19,6 +19,11 @@ __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t 
                                       recmg_counters *__restrict__ ctr);
 __global__ void state_reset_kernel(StateView st, int64_t SW, int64_t S, int64_t V);
 __global__ void clock_bump_kernel(int64_t *header, int64_t by);
+__global__ void next_use_kernel(const uint32_t *__restrict__ sorted_ids,
+                                const uint32_t *__restrict__ sorted_pos, int64_t n,
+                                int32_t *__restrict__ next_use);
+__global__ void keep_kernel(const int32_t *__restrict__ next_use, const uint8_t *__restrict__ hit,
+                            int64_t n, uint8_t *__restrict__ keep);
 __global__ void buffer_op_kernel(StateView st, int64_t S, int64_t W, int32_t op, int64_t gid,
                                  int64_t arg, int32_t flag, int64_t *result);
 
@@ -37,6 +42,7 @@ struct ReplayArgs {
     uint8_t *access_class;
     int64_t *hits_misses;
     uint8_t *per_access_hit;
+    const int32_t *next_use;   // OPTGEN: next reference of each access (n if none)
 };
 
 int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_t nsets,

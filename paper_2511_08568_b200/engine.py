@@ -101,14 +101,20 @@ class BufferReplay:
         return out
 
 
-class LruSim:
-    """recmg_simulate: set-associative (or fully associative) LRU."""
+class SetSim:
+    """recmg_simulate_ex: LRU / LFU / SRRIP / OPTGEN over set = gid % S
+    (cache_sim.py:92-249); LRU for any ways, the others up to 4096 ways."""
 
-    def __init__(self, capacity, total_ids, ways=None, n=0):
+    POLICIES = {"lru": _native.POLICY_LRU, "lfu": _native.POLICY_LFU,
+                "srrip": _native.POLICY_SRRIP, "optgen": _native.POLICY_OPTGEN}
+
+    def __init__(self, capacity, total_ids, ways=None, n=0, policy="lru", srrip_max_rrpv=3):
         torch = _native.torch_cuda()
         L = _native.lib()
         self.torch = torch
-        self.cfg = _native.buffer_cfg(capacity, ways, 1, _native.POLICY_LRU, total_ids)
+        self.policy = policy
+        self.cfg = _native.buffer_cfg(capacity, ways, srrip_max_rrpv if policy == "srrip" else 1,
+                                      self.POLICIES[policy], total_ids)
         sb = L.recmg_buffer_state_bytes(ctypes.byref(self.cfg))
         if sb == 0:
             _native.check(_native.RECMG_E_INVALID_CONFIG, "cache config")
@@ -134,17 +140,25 @@ class LruSim:
             _native.stream_handle(self.torch)), "buffer_reset")
         self.hm.zero_()
 
-    def run(self, gids, per_access_hit=None):
+    def run(self, gids, per_access_hit=None, keep=None):
         n = gids.numel()
         self.reserve(n)
-        _native.check(_native.lib().recmg_simulate(
+        _native.check(_native.lib().recmg_simulate_ex(
             ctypes.byref(self.cfg), _native.ptr(self.state), _native.ptr(gids), n,
-            _native.ptr(per_access_hit), _native.ptr(self.hm), _native.ptr(self._ws),
-            self._ws.numel(), _native.stream_handle(self.torch)), "simulate")
+            _native.ptr(per_access_hit), _native.ptr(keep), _native.ptr(self.hm),
+            _native.ptr(self._ws), self._ws.numel(), _native.stream_handle(self.torch)),
+            "simulate")
 
     def result(self):
         h, m = (int(x) for x in self.hm.cpu().numpy())
         return h, m
+
+
+class LruSim(SetSim):
+    """The 32-way LRU comparator (K4)."""
+
+    def __init__(self, capacity, total_ids, ways=None, n=0):
+        super().__init__(capacity, total_ids, ways, n, "lru")
 
 
 class RowStore:

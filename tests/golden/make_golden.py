@@ -197,6 +197,20 @@ def make_small():
     out["lru_cases"] = np.array(lru_cases)
     out["lru_hits"] = np.array(lru_hits)
     out["lru_per_access"] = np.stack(lru_pa)
+    # LFU / SRRIP / optgen comparators (cache_sim.py:109-249), set-assoc and FA
+    pol_cases, pol_hits, pol_pa, pol_keep = [], [], [], []
+    for pi, pol in enumerate((cache_sim.Policy.LFU, cache_sim.Policy.SRRIP, cache_sim.Policy.OPTGEN)):
+        for cap, ways in ((24, None), (24, 4), (32, 32), (64, 8), (96, 32), (7, None), (30, 1)):
+            r = cache_sim.simulate(t, cache_sim.CacheConfig(cap, pol, ways))
+            pol_cases.append([pi, cap, 0 if ways is None else ways])
+            pol_hits.append(r.hits)
+            pol_pa.append(np.array(r.per_access_hit, dtype=np.uint8))
+            pol_keep.append(np.array(r.keep_decisions if r.keep_decisions is not None
+                                     else [0] * len(t), dtype=np.uint8))
+    out["pol_cases"] = np.array(pol_cases)
+    out["pol_hits"] = np.array(pol_hits)
+    out["pol_per_access"] = np.stack(pol_pa)
+    out["pol_keep"] = np.stack(pol_keep)
     # variable-length prefetch lists from the optgen miss oracle
     # (test_runtime.py:157-171) with optgen keep bits
     cap = max(1, int(0.2 * t.unique_count))

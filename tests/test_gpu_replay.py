@@ -212,3 +212,29 @@ def test_lru_plus_prefetch_random_vs_oracle(seed):
         assert [rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
                 rep.prefetch_useful] == [ref[k] for k in NAMES[:5]], cap
         assert rep.coverage == cov
+
+
+def test_lfu_srrip_optgen_vs_reference(small):
+    """simulate() for LFU / SRRIP / OPTGEN (cache_sim.py:109-249) == reference,
+    incl. per-access hits and optgen keep decisions."""
+    t = rb.trace_from_gids(small["gids"], [int(x) for x in small["table_sizes"]])
+    pols = (rb.Policy.LFU, rb.Policy.SRRIP, rb.Policy.OPTGEN)
+    for case, hits, pa, keep in zip(small["pol_cases"], small["pol_hits"],
+                                    small["pol_per_access"], small["pol_keep"]):
+        pol, cap, ways = pols[int(case[0])], int(case[1]), int(case[2]) or None
+        res = rb.simulate(t, rb.CacheConfig(cap, pol, ways))
+        assert res.hits == hits and res.per_access_hit == pa.tolist(), (pol, cap, ways)
+        if pol == rb.Policy.OPTGEN:
+            assert res.keep_decisions == keep.tolist(), (cap, ways)
+
+
+def test_optgen_known_answers():
+    # test_cache_sim.py:33-42
+    res = rb.simulate_optgen(rb.trace_from_gids(letters("ABCABC"), [3]), 2)
+    assert res.hits == 2 and res.per_access_hit == [0, 0, 0, 1, 0, 1]
+    assert rb.simulate_optgen(rb.trace_from_gids([0, 0, 0], [2]), 1).hits == 2
+    res = rb.simulate_optgen(rb.trace_from_gids(letters("ABACB"), [3]), 2)
+    assert res.per_access_hit == [0, 0, 1, 0, 1] and res.keep_decisions == [1, 1, 0, 0, 0]
+    # test_cache_sim.py:19-24 (LFU keeps the hot block)
+    res = rb.simulate(rb.trace_from_gids(letters("AABCA"), [3]), rb.CacheConfig(2, rb.Policy.LFU))
+    assert res.per_access_hit == [0, 1, 0, 0, 1]
