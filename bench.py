@@ -338,6 +338,16 @@ def main():
         e2e_ms = (time.perf_counter() - t0) * 1000.0
         assert rep_e == rep and lru_e == lru, "e2e replay disagrees with device replay"
 
+    # ---- the paper's other comparators on the same trace (not timed) --------
+    comp = {}
+    try:
+        from paper_2511_08568_b200.cache_sim import CacheConfig, Policy, simulate
+        comp["lfu32_misses"] = simulate(t, CacheConfig(C32, Policy.LFU, 32), per_access=False).misses
+        comp["optgen32_misses"] = simulate(t, CacheConfig(C32, Policy.OPTGEN, 32),
+                                           per_access=False).misses
+    except Exception as exc:  # comparators are informational
+        comp["error"] = str(exc)
+
     # ---- K5/K6: host-row gathers + EmbeddingBag (config 2 rows) -------------
     rows_line = None
     if not args.no_rows:
@@ -403,7 +413,8 @@ def main():
                     "on_demand_vs_lru32": (c[2] / c[7]) if c[7] else None,
                     "cache_hits": c[0], "prefetch_hits": c[1], "prefetch_issued": c[3],
                     "prefetch_useful": c[4], "evictions": c[5], "prefetch_inserts": c[6],
-                    "coverage_rank0": rep.coverage, "capacity_rank0": C32, "unique_rank0": U},
+                    "coverage_rank0": rep.coverage, "capacity_rank0": C32, "unique_rank0": U,
+                    "comparators_rank0": comp},
         "stages_ms": mean,
         "gpu_launches": int(launches // args.steps),
         "roofline": roof,
