@@ -393,7 +393,8 @@ def main():
     roof = {"kernel": dominant, "bound": "tensor", "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)",
-            "algorithmic_flop_per_launch": fl,
+            "algorithmic_flop_per_launch": fl / max(1, args.pieces),
+            "launches_per_step": max(1, args.pieces),
             "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch"),
             "kernels": {
                 "caching_fwd": {"ms": mean["caching_fwd"], "tflops": fl_c / (mean["caching_fwd"] / 1e3) / 1e12},
