@@ -43,10 +43,38 @@ constexpr uint32_t P_H0_HI = COL_A + 0, P_H0_LO = COL_A + 32, P_CTX_HI = COL_A +
 template <int KIND> struct PartsOf { static constexpr int value = 2; };
 template <> struct PartsOf<RECMG_MODEL_PREFETCH> { static constexpr int value = 4; };
 
-__device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float ftanh(float x) {
     return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
 }
+
+// The epilogues are bound by the SFU (MUFU: ex2 + rcp per sigmoid/tanh at
+// 16 lanes/clk/SM).  rcp4 replaces four reciprocals of denominators d >= 1 by
+// one MUFU.RCP and nine FMULs; clamping each d at 2^31 keeps the product of
+// four finite and changes 1/d by < 5e-10 absolute.
+__device__ __forceinline__ float frcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+constexpr float kDenMax = 2147483648.0f;
+__device__ __forceinline__ void rcp4(float &a, float &b, float &c, float &d) {
+    a = fminf(a, kDenMax); b = fminf(b, kDenMax); c = fminf(c, kDenMax); d = fminf(d, kDenMax);
+    const float ab = a * b, cd = c * d;
+    const float r = frcp(ab * cd);
+    const float rab = r * cd, rcd = r * ab;
+    const float ia = rab * b, ib = rab * a, ic = rcd * d, id = rcd * c;
+    a = ia; b = ib; c = ic; d = id;
+}
+// 1 / (1 + e^(-x)) and tanh = 1 - 2 / (1 + e^(2x)) denominators
+__device__ __forceinline__ float sig_den(float x) { return 1.0f + __expf(-x); }
+__device__ __forceinline__ float tanh_den(float x) { return 1.0f + __expf(2.0f * x); }
+
+// Attention scores tanh(e + q) (model.py:118) use e^(2(e+q)) = e^(2e) e^(2q):
+// the encoder stores X = e^(2e) once per position, each decoder step
+// computes e^(2q) once, and every (position, unit) pair costs one FFMA and a
+// quarter MUFU.RCP instead of ex2 + rcp.  Exponents beyond +-kExpLim fall
+// back to the direct form (raw e kept for that position / q out of range).
+constexpr float kExpLim = 80.0f;
 
 struct TcArgs {
     recmg_model_shape m;
@@ -209,6 +237,38 @@ __device__ __forceinline__ void init_z_from_table(const Ctx<PARTS> &c, const flo
     }
 }
 
+// Folded-table row of the NEXT step, gathered while the current step's MMA
+// and epilogue run: the first NPRE float4 are loaded early into registers,
+// the rest when the row is committed into Z (after the cell has read Z).
+template <int PARTS>
+struct RowStage {
+    static constexpr int NF4 = Ctx<PARTS>::U;            // 4U floats = U float4
+    static constexpr int NPRE = NF4 < 16 ? NF4 : 16;
+    float4 x[NPRE];
+    const float4 *src;
+    __device__ __forceinline__ void prefetch(const Ctx<PARTS> &c, const float *pid, int32_t g) {
+        src = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + 4 * Ctx<PARTS>::U * c.part);
+#pragma unroll
+        for (int q = 0; q < NPRE; q++) x[q] = __ldg(src + q);
+    }
+    __device__ __forceinline__ void commit(const Ctx<PARTS> &c) {
+#pragma unroll
+        for (int blk = 0; blk < NF4 / 4; blk++) {
+            uint32_t r[16];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int i = blk * 4 + q;
+                const float4 u = i < NPRE ? x[i < NPRE ? i : 0] : __ldg(src + i);
+                r[4 * q + 0] = __float_as_uint(u.x);
+                r[4 * q + 1] = __float_as_uint(u.y);
+                r[4 * q + 2] = __float_as_uint(u.z);
+                r[4 * q + 3] = __float_as_uint(u.w);
+            }
+            umma::tmem_st16(c.lane_addr + COL_Z + 4 * Ctx<PARTS>::U * c.part + 16 * blk, r);
+        }
+    }
+};
+
 // Z[my 4U columns] = row (same for every chunk: prefetch slot projection)
 template <int PARTS>
 __device__ __forceinline__ void init_z_from_row(const Ctx<PARTS> &c, const float *rowp) {
@@ -242,17 +302,27 @@ __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
         umma::tmem_ld16(c.lane_addr + COL_Z + 4 * U * c.part + 16 * (blk + 1), z1);
         umma::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const int j = 4 * blk + u;
-            const float *z = (u < 4) ? &z0[4 * u] : &z1[4 * (u - 4)];
-            float zi = z[0], zf = z[1], zg = z[2], zo = z[3];
-            if (BIAS) {
-                const float4 bb = __ldg(b4 + j);
-                zi += bb.x; zf += bb.y; zg += bb.z; zo += bb.w;
+        for (int g4 = 0; g4 < 2; g4++) {
+            float og[4], dc[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = 4 * blk + 4 * g4 + u;
+                const float *z = g4 == 0 ? &z0[4 * u] : &z1[4 * u];
+                float zi = z[0], zf = z[1], zg = z[2], zo = z[3];
+                if (BIAS) {
+                    const float4 bb = __ldg(b4 + j);
+                    zi += bb.x; zf += bb.y; zg += bb.z; zo += bb.w;
+                }
+                float ig = sig_den(zi), fg = sig_den(zf), gd = tanh_den(zg), o = sig_den(zo);
+                rcp4(ig, fg, gd, o);
+                const float gg = fmaf(-2.0f, gd, 1.0f);
+                cs[j] = fg * cs[j] + ig * gg;
+                og[u] = o;
+                dc[u] = tanh_den(cs[j]);
             }
-            const float ig = fsig(zi), fg = fsig(zf), gg = ftanh(zg), og = fsig(zo);
-            cs[j] = fg * cs[j] + ig * gg;
-            h[j] = og * ftanh(cs[j]);
+            rcp4(dc[0], dc[1], dc[2], dc[3]);
+#pragma unroll
+            for (int u = 0; u < 4; u++) h[4 * blk + 4 * g4 + u] = og[u] * fmaf(-2.0f, dc[u], 1.0f);
         }
     }
 }
@@ -288,20 +358,59 @@ __device__ __forceinline__ void storeU(float *base, const Ctx<PARTS> &c, int j,
         *scratch_at(base, c, j, u) = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
 }
 
+// encoder: position j of the attention keys, stored as X = e^(2e) (bit j of
+// rawmask clear) or as raw e when any of this thread's units is out of range
+template <int PARTS>
+__device__ __forceinline__ void store_keys(float *Es, const Ctx<PARTS> &c, int j,
+                                           float (&e)[Ctx<PARTS>::U], uint32_t &rawmask) {
+    constexpr int U = Ctx<PARTS>::U;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < U; k++) ok = ok && fabsf(2.0f * e[k]) <= kExpLim;
+    if (ok) {
+#pragma unroll
+        for (int k = 0; k < U; k++) e[k] = __expf(2.0f * e[k]);
+    } else {
+        rawmask |= 1u << j;
+    }
+    storeU(Es, c, j, e);
+}
+
+// sum_u v_u tanh(e_u + q_u) over this thread's units for one position
 template <int NQ>
-__device__ __forceinline__ float score_part(const float4 (&e)[NQ], const float (&q)[4 * NQ],
+__device__ __forceinline__ float score_fast(const float4 (&x)[NQ], const float (&qx)[4 * NQ],
                                             const float4 *v4) {
-    // four independent accumulators: the dot is a latency chain otherwise
     float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
 #pragma unroll
     for (int u = 0; u < NQ; u++) {
         const float4 v = __ldg(v4 + u);
-        s0 += v.x * ftanh(e[u].x + q[4 * u + 0]);
-        s1 += v.y * ftanh(e[u].y + q[4 * u + 1]);
-        s2 += v.z * ftanh(e[u].z + q[4 * u + 2]);
-        s3 += v.w * ftanh(e[u].w + q[4 * u + 3]);
+        float a = fmaf(x[u].x, qx[4 * u + 0], 1.0f), b = fmaf(x[u].y, qx[4 * u + 1], 1.0f);
+        float cc = fmaf(x[u].z, qx[4 * u + 2], 1.0f), d = fmaf(x[u].w, qx[4 * u + 3], 1.0f);
+        rcp4(a, b, cc, d);
+        s0 = fmaf(v.x, a, s0);
+        s1 = fmaf(v.y, b, s1);
+        s2 = fmaf(v.z, cc, s2);
+        s3 = fmaf(v.w, d, s3);
     }
-    return (s0 + s1) + (s2 + s3);
+    return -2.0f * ((s0 + s1) + (s2 + s3));   // + sum_u v_u by the caller
+}
+
+// direct form: raw keys (raw) or keys stored as X = e^(2e) recovered by log
+template <int NQ>
+__device__ __forceinline__ float score_slow(const float4 (&x)[NQ], const float (&q)[4 * NQ],
+                                            const float4 *v4, bool raw) {
+    float s = 0.0f;
+#pragma unroll
+    for (int u = 0; u < NQ; u++) {
+        const float4 v = __ldg(v4 + u);
+        const float4 e = raw ? x[u] : make_float4(0.5f * __logf(x[u].x), 0.5f * __logf(x[u].y),
+                                                  0.5f * __logf(x[u].z), 0.5f * __logf(x[u].w));
+        s += v.x * ftanh(e.x + q[4 * u + 0]);
+        s += v.y * ftanh(e.y + q[4 * u + 1]);
+        s += v.z * ftanh(e.z + q[4 * u + 2]);
+        s += v.w * ftanh(e.w + q[4 * u + 3]);
+    }
+    return s;
 }
 
 // partial attention scores over this thread's units (model.py:118-119),
@@ -309,22 +418,35 @@ __device__ __forceinline__ float score_part(const float4 (&e)[NQ], const float (
 template <int PARTS>
 __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int npos,
                                             const float (&q)[Ctx<PARTS>::U], const float *vp,
-                                            float *s_part, int L) {
+                                            float vsum, uint32_t rawmask, float *s_part, int L) {
     constexpr int NQ = Ctx<PARTS>::NQ;
+    constexpr int U = Ctx<PARTS>::U;
     const float4 *v4 = reinterpret_cast<const float4 *>(vp) + NQ * c.part;
+    float qx[U];
+    bool qok = true;
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+        qok = qok && fabsf(2.0f * q[k]) <= kExpLim;
+        qx[k] = __expf(2.0f * q[k]);
+    }
+    const uint32_t slow = qok ? rawmask : 0xFFFFFFFFu;
+    auto score = [&](const float4 (&x)[NQ], int j) {
+        return ((slow >> j) & 1u) ? score_slow<NQ>(x, q, v4, (rawmask >> j) & 1u)
+                                  : vsum + score_fast<NQ>(x, qx, v4);
+    };
     int j = 0;
     for (; j + 2 <= npos; j += 2) {
         float4 e0[NQ], e1[NQ];
 #pragma unroll
         for (int u = 0; u < NQ; u++) { e0[u] = *scratch_at(Es, c, j, u); e1[u] = *scratch_at(Es, c, j + 1, u); }
-        s_part[(c.part * L + j) * 128 + c.row] = score_part<NQ>(e0, q, v4);
-        s_part[(c.part * L + j + 1) * 128 + c.row] = score_part<NQ>(e1, q, v4);
+        s_part[(c.part * L + j) * 128 + c.row] = score(e0, j);
+        s_part[(c.part * L + j + 1) * 128 + c.row] = score(e1, j + 1);
     }
     if (j < npos) {
         float4 e0[NQ];
 #pragma unroll
         for (int u = 0; u < NQ; u++) e0[u] = *scratch_at(Es, c, j, u);
-        s_part[(c.part * L + j) * 128 + c.row] = score_part<NQ>(e0, q, v4);
+        s_part[(c.part * L + j) * 128 + c.row] = score(e0, j);
     }
 }
 
@@ -391,8 +513,15 @@ __device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
     readU(c, col, v);
     float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int k = 0; k < U; k++)
-        s[k & 3] += ftanh(v[k] + __ldg(comb_b + U * c.part + k)) * __ldg(head_w + U * c.part + k);
+    for (int k = 0; k < U; k += 4) {
+        float d[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) d[i] = tanh_den(v[k + i] + __ldg(comb_b + U * c.part + k + i));
+        rcp4(d[0], d[1], d[2], d[3]);
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            s[i] += fmaf(-2.0f, d[i], 1.0f) * __ldg(head_w + U * c.part + k + i);
+    }
     return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
@@ -461,6 +590,8 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     const float *comb_b = a.dense + pl.comb_b;
     const float *head_w = a.dense + pl.head_w;
     const float head_b = __ldg(a.dense + pl.head_b);
+    float vsum = 0.0f;   // sum of this thread's att_v units (score_fast)
+    for (int k = 0; k < U; k++) vsum += __ldg(att_v + U * c.part + k);
     const int64_t n_tiles = (a.batch + 127) / 128;
 
     // dynamic tile scheduler: a CTA that starts late (its SM busy with a
@@ -484,10 +615,13 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             zero_operand(c, P_H0_HI, P_H0_LO);
             zero_operand(c, P_H1_HI, P_H1_LO);
         }
+        uint32_t rawmask = 0;   // attention key positions stored raw (store_keys)
+        RowStage<PARTS> stage;
+        stage.prefetch(c, pid_enc, __ldg(gid));
+        stage.commit(c);
         for (int t = 0; t <= L; t++) {
             const bool last = (t == L);   // t == L: only enc_pre of the last state
             pc.mark(0);
-            if (!last) init_z_from_table(c, pid_enc, __ldg(gid + t));
             tmem_writes_done();
             pc.mark(1);
             if (caching) {
@@ -499,17 +633,21 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                          sbase + tl.b_off[1], 64, false);                  // Q = h att_enc
                     umma::commit(&mbar);
                 }
+                pc.mark(12);
+                if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
+                pc.mark(13);
                 wait_mma(&mbar, phase);
                 pc.mark(2);
                 if (t >= 1) {
                     float ep[U];
                     readU(c, COL_Q, ep);
-                    storeU(Es, c, t - 1, ep);
+                    store_keys(Es, c, t - 1, ep, rawmask);
                 }
                 if (!last) {
                     cell<false>(c, nullptr, cs0, h);
                     store_operand(c, A_H_HI, A_H_LO, h);
                     storeU(Hs, c, t, h);
+                    if (t + 1 < L) stage.commit(c);
                 }
             } else {
                 if (!last) {
@@ -538,16 +676,18 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                          sbase + tl.b_off[3], 64, false);
                     umma::commit(&mbar);
                 }
+                if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
                 wait_mma(&mbar, phase);
                 if (t >= 1) {
                     float ep[U];
                     readU(c, COL_Q, ep);
-                    storeU(Es, c, t - 1, ep);
+                    store_keys(Es, c, t - 1, ep, rawmask);
                 }
                 if (!last) {
                     cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
                     store_operand(c, P_H1_HI, P_H1_LO, h);
                     storeU(Hs, c, t, h);
+                    if (t + 1 < L) stage.commit(c);
                 }
             }
         }
@@ -562,10 +702,12 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         if (caching) {
             zero_operand(c, A_H_HI, A_H_LO);
             zero_operand(c, A_X_HI, A_X_LO);
+            RowStage<PARTS> dstage;
+            dstage.prefetch(c, pid_dec, __ldg(gid));
+            dstage.commit(c);
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);   // t == T: only finish comb_{T-1}
                 pc.mark(3);
-                if (!last) init_z_from_table(c, pid_dec, __ldg(gid + t));
                 tmem_writes_done();
                 pc.mark(4);
                 // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
@@ -588,7 +730,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     float q[U];
                     readU(c, COL_Q, q);
-                    attn_scores(c, Es, t + 1, q, att_v, s_part, L);   // causal: j <= t
+                    attn_scores(c, Es, t + 1, q, att_v, vsum, rawmask, s_part, L);   // causal: j <= t
                 }
                 __syncthreads();
                 if (t >= 1 && c.part == 0) {
@@ -613,10 +755,12 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                          sbase + tl.b_off[6], 64, false);
                     umma::commit(&mbar);
                 }
+                if (t + 1 < T) dstage.prefetch(c, pid_dec, __ldg(gid + t + 1));
                 wait_mma(&mbar, phase);
                 pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
                 store_operand(c, A_H_HI, A_H_LO, h);
+                if (t + 1 < T) dstage.commit(c);
             }
         } else {
             zero_operand(c, P_H0_HI, P_H0_LO);
@@ -647,7 +791,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     float q[U];
                     readU(c, COL_Q, q);
-                    attn_scores(c, Es, L, q, att_v, s_part, L);       // non-causal
+                    attn_scores(c, Es, L, q, att_v, vsum, rawmask, s_part, L);      // non-causal
                 }
                 __syncthreads();
                 if (t >= 1 && c.part == 0) {

@@ -14,7 +14,7 @@ from paper_2511_08568_b200.model import DeviceModel, init_params_device
 
 NAMES = ["enc table init+sync", "enc MMA wait", "enc epilogue", "dec init+sync",
          "dec MMA1 wait", "dec head+scores+sync", "dec softmax/ctx+sync", "dec MMA2 wait",
-         "dec cell", "weight loads", "pf L1 MMA wait", "pf L1 cell", "", "", "", "other"]
+         "dec cell", "weight loads", "pf L1 MMA wait", "pf L1 cell", "enc MMA issue", "enc row prefetch", "", "other"]
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 t = rb.generate_trace(rb.TraceGenConfig([50000] * 256, n, 1.05, 0.4, 32, 2))

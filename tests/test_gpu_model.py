@@ -56,6 +56,29 @@ def test_config1_shapes_vs_oracle(scale, precision):
     assert np.all(np.abs(rc[flips]) < 1e-4)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tc32"])
+@pytest.mark.parametrize("which", ["att_enc", "att_dec", "both"])
+def test_attention_exponent_range(which, precision):
+    """Attention keys / queries beyond the e^(2x) fast path's range (|x| > 40)
+    take the direct tanh form (lstm_tc.cu store_keys / attn_scores)."""
+    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 300 * 15 + 30, 1.05, 0.4, 32, 0))
+    K = rb.num_chunks(len(t))
+    gid = t.gid_array[:K * 15].reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    for kind, seed in (("caching", 0), ("prefetch", 1)):
+        p = rb.init_params(kind, t.table_sizes, dim=64, seed=seed, init_scale=0.4)
+        for name in ("att_enc", "att_dec"):
+            if which in (name, "both"):
+                p.arrays[name] = (p.arrays[name] * 60.0).astype(p.arrays[name].dtype)
+        if kind == "caching":
+            got = rb.forward_caching_batch(p, gid, tid, precision).logits
+            ref = mo.caching_logits(p.arrays, 64, 1, gid, tid)
+        else:
+            got = rb.forward_prefetch_batch(p, gid, tid, precision).logits
+            ref = mo.prefetch_logits(p.arrays, 64, 2, 5, gid, tid)
+        _check(got, ref)
+
+
 def test_gpu_decisions_in_replay_path():
     """bits / decoded prefetch ids emitted by the kernel (runtime.py:192,
     model.py:250-258) vs the oracle's, through the replay entry point."""
