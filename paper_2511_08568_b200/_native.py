@@ -14,7 +14,8 @@ from .errors import (CheckpointError, EmbcacheError, InvalidConfigError, Numeric
                      OutOfVocabularyError, VocabularyMismatchError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librecmg.so")
+# RECMG_LIB: an alternative in-tree build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.path.join(_HERE, os.environ.get("RECMG_LIB", "librecmg.so"))
 
 RECMG_OK = 0
 RECMG_E_INVALID_CONFIG = -1

@@ -243,7 +243,7 @@ __device__ __forceinline__ void init_z_from_table(const Ctx<PARTS> &c, const flo
 template <int PARTS>
 struct RowStage {
     static constexpr int NF4 = Ctx<PARTS>::U;            // 4U floats = U float4
-    static constexpr int NPRE = NF4 < 16 ? NF4 : 16;
+    static constexpr int NPRE = PARTS == 4 ? 4 : 16;   // measured: more early loads clog the LSU
     float4 x[NPRE];
     const float4 *src;
     __device__ __forceinline__ void prefetch(const Ctx<PARTS> &c, const float *pid, int32_t g) {

@@ -12,12 +12,15 @@ import paper_2511_08568_b200 as rb
 from paper_2511_08568_b200 import _native
 from paper_2511_08568_b200.model import DeviceModel, init_params_device
 
+PF_NAMES = {1: "enc L0 MMA issue+wait", 2: "enc cell0+sync", 12: "enc L1 MMA issue", 14: "enc row prefetch",
+            13: "enc L1 MMA wait", 11: "enc keys+cell1 / dec L1 cell"}
 NAMES = ["enc table init+sync", "enc MMA wait", "enc epilogue", "dec init+sync",
          "dec MMA1 wait", "dec head+scores+sync", "dec softmax/ctx+sync", "dec MMA2 wait",
          "dec cell", "weight loads", "pf L1 MMA wait", "pf L1 cell", "enc MMA issue", "enc row prefetch", "", "other"]
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
-t = rb.generate_trace(rb.TraceGenConfig([50000] * 256, n, 1.05, 0.4, 32, 2))
+rows = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
+t = rb.generate_trace(rb.TraceGenConfig([rows] * 256, n, 1.05, 0.4, 32, 2))
 K = rb.num_chunks(len(t))
 g = torch.from_numpy(t.gid_array[:K * 15].astype(np.int32).reshape(K, 15)).cuda()
 for kind, seed in (("caching", 0), ("prefetch", 1)):
@@ -44,5 +47,6 @@ for kind, seed in (("caching", 0), ("prefetch", 1)):
     for i in range(16):
         v = pr[:, i].mean()
         if v > 0:
-            print(f"   {NAMES[i]:24s} {v / tot * 100:5.1f}%")
+            name = PF_NAMES.get(i, NAMES[i]) if kind == "prefetch" else NAMES[i]
+            print(f"   {name:26s} {v / tot * 100:5.1f}%")
     del dm, emb
