@@ -19,6 +19,13 @@ N > 1 (torchrun): weak scaling, table-sharded: every rank owns its own
 256-table shard and its own 25 M-access slice (seed 2 + rank), no collective
 on the data path; counters are summed at the end.
 
+--config 3: the 856-table x 100k-row, 500 M-access trace (seed 3), drawn by
+the streamed bit-exact generator (TraceStream) and table-sharded over
+--shards ranks (default: the world size) greedily by access count; every
+rank runs its shard's sub-trace with shard-local models (strong scaling).
+On one GPU, --shards 8 --shard-index r measures rank r's share of the
+8-GPU job alone.
+
 --impl reference: the reference's CPU algorithm (the oracle port: numpy
 float64 forwards + the C replay restatement, oracle/) on a bounded sample of
 the same workload, rank 0 only.
@@ -65,10 +72,37 @@ def parse():
     ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
     ap.add_argument("--pieces", type=int, default=8, help="replay pipeline pieces")
     ap.add_argument("--model-sms", type=int, default=146, help="SMs the forwards may use")
-    return ap.parse_args()
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--shards", type=int, default=0, help="config 3: table shards (0 = world)")
+    ap.add_argument("--shard-index", type=int, default=0,
+                    help="config 3 on one process: which shard to run")
+    args = ap.parse_args()
+    if args.config == 3:
+        d = {"accesses": 25_000_000, "tables": 256, "rows": 50_000}
+        c3 = {"accesses": 500_000_000, "tables": 856, "rows": 100_000}
+        for k, v in c3.items():
+            if getattr(args, k) == d[k]:
+                setattr(args, k, v)
+        args.no_rows = True   # 44 GB of pinned host rows: config 2 measures K5/K6
+    return args
 
 
 def workload(args, rank):
+    if args.config == 3:
+        return {
+            "workload": f"config3: synthetic Zipf trace, {args.tables} tables x {args.rows} rows, "
+                        f"{args.accesses} accesses (streamed generator), table-sharded greedily "
+                        f"by access count over {args.shards_eff} GPUs; this line: "
+                        + ("all shards" if args.world > 1 else f"shard {args.shard_index} of "
+                           f"{args.shards_eff} alone") + "; caching LSTM (1 stack) + prefetch "
+                        "LSTM (2 stacks), d=64, shard-local models; 32-way priority buffer at 20% "
+                        "of the shard's unique ids (es=4) + 32-way LRU comparator",
+            "accesses_total": args.accesses, "tables": args.tables, "rows_per_table": args.rows,
+            "shards": args.shards_eff, "zipf": 1.05, "stickiness": 0.4, "pool": 32,
+            "trace_seed": 3, "dim": args.dim, "init_scale": args.init_scale, "ways": 32,
+            "eviction_speed": 4, "window_ratio": 3,
+            "l2": "inputs larger than L2 (ids + shard-local folded tables, GBs per step)",
+        }
     return {
         "workload": "config2: synthetic Zipf trace, 256 tables x 50k rows, 25M accesses; "
                     "caching LSTM (1 stack) + prefetch LSTM (2 stacks), d=64, l_in 15 / l_out 5; "
@@ -147,7 +181,7 @@ def load_profile_traffic():
 
 
 # --------------------------------------------------------------------------
-def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways):
+def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways, shard=None):
     """The reference algorithm on the host cores (oracle port), on the first
     n_sample accesses: float64 numpy forwards in batches of 256 (runtime.py:
     181-210), fp64 decode, the C replay restatement in the reference's dense
@@ -158,12 +192,16 @@ def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways):
     gids = t.gid_array[:n_sample]
     K = num_chunks(len(gids))
     uniq, inv = np.unique(gids[:K * 15], return_inverse=True)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    rows = uniq
+    if shard is not None:   # shard-local embed_id rows / embed_table rows
+        rows = shard.to_local(uniq)[0]
+        tid = shard.table_local[tid]
     ac = dict(cparams.arrays)
     ap = dict(pparams.arrays)
-    ac["embed_id"] = emb_c[uniq].double().cpu().numpy() if hasattr(emb_c, "cpu") else emb_c[uniq]
-    ap["embed_id"] = emb_p[uniq].double().cpu().numpy() if hasattr(emb_p, "cpu") else emb_p[uniq]
+    ac["embed_id"] = emb_c[rows].double().cpu().numpy() if hasattr(emb_c, "cpu") else emb_c[rows]
+    ap["embed_id"] = emb_p[rows].double().cpu().numpy() if hasattr(emb_p, "cpu") else emb_p[rows]
     lg = inv.reshape(K, 15)
-    tid = t.table_ids[:K * 15].reshape(K, 15)
     V = t.total_ids
     oracle.lib()
     # untimed warm-up batch (BLAS thread pool, page faults)
@@ -183,7 +221,7 @@ def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways):
     t2 = time.perf_counter()
     return {"value": len(gids) / (t2 - t0), "unit": UNIT,
             "cores": len(os.sched_getaffinity(0)), "kind": "port",
-            "sample": f"first {len(gids)} accesses of the rank-0 config-2 trace ({K} chunks): "
+            "sample": f"first {len(gids)} accesses of the {'shard' if shard is not None else 'rank-0 config-2'} trace ({K} chunks): "
                       f"numpy float64 forwards (OpenBLAS threads) {t1 - t0:.2f}s + C replay "
                       f"(dense per-id layout) + 32-way LRU {t2 - t1:.2f}s",
             "model_s": t1 - t0, "replay_s": t2 - t1}
@@ -241,9 +279,48 @@ def measure_rows(args, hp, n, torch):
             "note": "K5/K6 run after the timed replay; not part of `value`"}
 
 
+def build_state_config3(args, idx, torch):
+    """Config 3: stream the whole trace, assign tables by access count,
+    keep shard `idx`'s order-preserving sub-trace, draw its local models."""
+    import paper_2511_08568_b200 as rb
+    from paper_2511_08568_b200 import shard as shd
+    from paper_2511_08568_b200.trace import Trace, TraceStream, table_offsets
+    t0 = time.time()
+    sizes = [args.rows] * args.tables
+    ts = TraceStream(rb.TraceGenConfig(sizes, args.accesses, 1.05, 0.4, 32, 3))
+    g = np.empty(args.accesses, dtype=np.int32)
+    counts = np.zeros(args.tables, dtype=np.int64)
+    for b in ts.blocks(1 << 24):
+        g[ts.pos - len(b):ts.pos] = b
+        counts += np.bincount(b // args.rows, minlength=args.tables)
+    del ts
+    assign = shd.assign_tables(counts, args.shards_eff)
+    mine = assign == idx
+    parts = []
+    for i in range(0, len(g), 1 << 24):
+        b = g[i:i + (1 << 24)]
+        parts.append(b[mine[b // args.rows]])
+    del g
+    sub = np.concatenate(parts)
+    del parts
+    t = Trace(sub, sizes)
+    t._unique = int(np.count_nonzero(np.bincount(sub, minlength=sum(sizes))))
+    U = t.unique_count
+    C = int(math.floor(0.2 * U))
+    C32 = C - C % 32
+    sh = shd.TableShard(sizes, np.nonzero(mine)[0])
+    cp, emb_c = shd.init_params_shard("caching", sizes, sh, dim=args.dim, seed=0,
+                                      init_scale=args.init_scale)
+    pp, emb_p = shd.init_params_shard("prefetch", sizes, sh, dim=args.dim, seed=1,
+                                      init_scale=args.init_scale)
+    return t, U, C, C32, cp, emb_c, pp, emb_p, time.time() - t0, sh
+
+
 def build_state(args, rank, torch):
     import paper_2511_08568_b200 as rb
     from paper_2511_08568_b200.model import DeviceModel, init_params_device
+    if args.config == 3:
+        return build_state_config3(args, rank if args.world > 1 else args.shard_index, torch)
     t0 = time.time()
     t = rb.generate_trace(rb.TraceGenConfig([args.rows] * args.tables, args.accesses, 1.05, 0.4,
                                             32, 2 + rank))
@@ -254,7 +331,7 @@ def build_state(args, rank, torch):
                                    init_scale=args.init_scale)
     pp, emb_p = init_params_device("prefetch", t.table_sizes, dim=args.dim, seed=1,
                                    init_scale=args.init_scale)
-    return t, U, C, C32, cp, emb_c, pp, emb_p, time.time() - t0
+    return t, U, C, C32, cp, emb_c, pp, emb_p, time.time() - t0, None
 
 
 def main():
@@ -271,6 +348,10 @@ def main():
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
 
+    args.world = world
+    args.shards_eff = args.shards or world
+    if args.config == 3 and world > 1 and args.shards_eff != world:
+        raise SystemExit("--config 3 under torchrun runs one shard per rank (--shards = world)")
     if args.impl == "reference":
         return run_reference(args, rank, world, torch, dist)
 
@@ -279,11 +360,12 @@ def main():
     from paper_2511_08568_b200.model import DeviceModel
     from paper_2511_08568_b200.pipeline import HotPath
 
-    t, U, C, C32, cp, emb_c, pp, emb_p, setup_s = build_state(args, rank, torch)
+    t, U, C, C32, cp, emb_c, pp, emb_p, setup_s, sh = build_state(args, rank, torch)
     n = len(t)
-    hp = HotPath(DeviceModel(cp, emb_c), DeviceModel(pp, emb_p), t.table_sizes, C32, n,
-                 ways=32, eviction_speed=4, lru_capacity=C32, lru_ways=32,
-                 pieces=args.pieces, model_sms=args.model_sms)
+    dec = sh.total_ids if sh is not None else 0
+    hp = HotPath(DeviceModel(cp, emb_c, decode_ids=dec), DeviceModel(pp, emb_p, decode_ids=dec),
+                 t.table_sizes, C32, n, ways=32, eviction_speed=4, lru_capacity=C32, lru_ways=32,
+                 pieces=args.pieces, model_sms=args.model_sms, shard=sh)
     host = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
     hp.gids[:n].copy_(host)
     torch.cuda.synchronize()
@@ -407,7 +489,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "higher_is_better": True, "scaling": "strong" if args.config == 3 else "weak",
+        "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
         "config": dict(workload(args, 0), pipeline_pieces=args.pieces, model_sms=args.model_sms),
         "quality": {"on_demand": c[2], "lru32_misses": c[7],
@@ -431,7 +514,8 @@ def main():
     if rows_line is not None:
         line["rows"] = rows_line
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32)
+        line["cpu_baseline"] = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32,
+                                            shard=sh)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -237,6 +237,17 @@ int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
                         const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
                         int32_t *pf_gid, void *ws, size_t ws_bytes, void *stream);
 
+/* recmg_model_forward for a table shard: the model's
+ * vocabulary (shape->total_ids, n_tables, the packed folded tables and
+ * gid/tid) is the shard's local one, while the prefetch decode keeps the
+ * global id scale of model.py:255, floor(po*(decode_ids-1)+0.5) over the
+ * whole layout (decode_ids = 0: shape->total_ids, i.e. recmg_model_forward). */
+int recmg_model_forward_ex(const recmg_model_shape *shape, int32_t precision,
+                           const float *embed_id, const void *packed, const int32_t *gid,
+                           const int32_t *tid, int64_t batch, int64_t decode_ids, float *logits,
+                           uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes,
+                           void *stream);
+
 /* Upper bound on the CTAs (= SMs) the TC32 forwards occupy (default 148);
  * returns the previous value.  Leaving a few SMs to the replay lets a
  * pipelined replay of earlier chunks run beside the forwards.              */
@@ -247,11 +258,42 @@ int recmg_set_model_sm_budget(int n);
  * searchsorted of trace.py:86 / index_of_global trace.py:44-51.             */
 int recmg_table_ids(const int32_t *gids, int64_t n, const int64_t *offsets, int32_t n_tables,
                     int32_t *tid, void *stream);
+/* Table shard: for every global gid, its row in the
+ * shard's local vocabulary and its local table.  table_local[n_tables] maps
+ * a global table to its local index (-1: another shard's, then both outputs
+ * are -1); local_offsets[n_local+1] are the local table offsets.  The
+ * models of a shard are packed over the local vocabulary and run with
+ * recmg_model_forward_ex(decode_ids = global total_ids).                    */
+int recmg_shard_local_ids(const int32_t *gids, int64_t n, const int64_t *offsets,
+                          int32_t n_tables, const int32_t *table_local,
+                          const int64_t *local_offsets, int32_t *local_gids,
+                          int32_t *local_tids, void *stream);
 /* Host: the sticky-pool pass of generate_trace (trace.py:144-160), given
  * the already-drawn zipf gids and coins.  Returns 0.                        */
 int recmg_trace_pool_pass(const int64_t *host_zipf_gids, const double *host_sticky_coin,
                           const double *host_pool_coin, int64_t n, double stickiness,
                           int32_t pool_size, int64_t *host_out_gids);
+
+/* ---- streamed generator (trace.py:124-161 without materialising it) ---- */
+/* pcg[4] = numpy PCG64 {state_hi, state_lo, inc_hi, inc_lo} as
+ * default_rng(seed) holds it right after permutation(V).                    */
+/* Host: count doubles of Generator.random() starting `skip` outputs ahead
+ * of pcg (PCG64.advance + next_double), on `threads` host threads.          */
+int recmg_pcg64_uniforms(const uint64_t pcg[4], int64_t skip, int64_t count, double *host_out,
+                         int32_t threads);
+/* Host: guide[b] = #{j : cdf[j] <= b / 2^guide_log2}, b = 0..2^guide_log2
+ * (host_guide has 2^guide_log2 + 1 entries).                                */
+int recmg_trace_guide(const double *host_cdf, int64_t V, int32_t guide_log2, int64_t *host_guide);
+/* Host: accesses [i0, i0+count) of generate_trace(n_total accesses): the
+ * zipf draw choice(V, p) == cdf.searchsorted(random(), 'right') mapped
+ * through rank_to_gid, the two coin streams, and the sticky-pool pass with
+ * its state (host_pool[pool_size], *host_pool_len; start empty, len 0)
+ * carried from the previous block.  Blocks must be generated in order.     */
+int recmg_trace_generate_block(const uint64_t pcg[4], int64_t n_total, int64_t i0, int64_t count,
+                               const double *host_cdf, int64_t V, const int64_t *host_guide,
+                               int32_t guide_log2, const int64_t *host_rank_to_gid,
+                               double stickiness, int32_t pool_size, int64_t *host_pool,
+                               int32_t *host_pool_len, int32_t *host_out_gids, int32_t threads);
 
 /* ---- diagnostics -------------------------------------------------------- */
 /* tcgen05 self-test GEMM: D[128 x N] (fp32, row-major) = A[128 x K] * B[N x K]^T

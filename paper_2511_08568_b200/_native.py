@@ -47,7 +47,8 @@ EXPORTS = (
     "recmg_launch_count", "recmg_selftest_umma", "recmg_model_pack_tc",
     "recmg_model_workspace_bytes", "recmg_replay_chunks", "recmg_set_model_sm_budget",
     "recmg_model_forward_profile", "recmg_rows_refresh", "recmg_embedding_bag",
-    "recmg_simulate_ex",
+    "recmg_simulate_ex", "recmg_model_forward_ex", "recmg_pcg64_uniforms", "recmg_trace_guide",
+    "recmg_trace_generate_block", "recmg_shard_local_ids",
 )
 
 
@@ -107,6 +108,13 @@ def lib():
         "recmg_model_pack": (ctypes.c_int, [shp, vp, vp, i32, vp]),
         "recmg_model_forward": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp,
                                                sz, vp]),
+        "recmg_model_forward_ex": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, i64, vp, vp,
+                                                  vp, vp, sz, vp]),
+        "recmg_shard_local_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, vp, vp, vp]),
+        "recmg_pcg64_uniforms": (ctypes.c_int, [vp, i64, i64, vp, i32]),
+        "recmg_trace_guide": (ctypes.c_int, [vp, i64, i32, vp]),
+        "recmg_trace_generate_block": (ctypes.c_int, [vp, i64, i64, i64, vp, i64, vp, i32, vp,
+                                                      ctypes.c_double, i32, vp, vp, vp, i32]),
         "recmg_model_pack_tc": (ctypes.c_int, [shp, vp, vp, vp, vp, vp]),
         "recmg_model_workspace_bytes": (sz, [shp, i32, i64]),
         "recmg_table_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp]),

@@ -380,22 +380,33 @@ size_t recmg_model_workspace_bytes(const recmg_model_shape *shape, int32_t preci
     return 0;
 }
 
-int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
-                        const float *embed_id, const void *packed, const int32_t *gid,
-                        const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
-                        int32_t *pf_gid, void *ws, size_t ws_bytes, void *stream) {
-    if (!shape_ok(shape) || batch < 0 || !logits) return RECMG_E_INVALID_CONFIG;
+int recmg_model_forward_ex(const recmg_model_shape *shape, int32_t precision,
+                           const float *embed_id, const void *packed, const int32_t *gid,
+                           const int32_t *tid, int64_t batch, int64_t decode_ids, float *logits,
+                           uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes,
+                           void *stream) {
+    if (!shape_ok(shape) || batch < 0 || !logits || decode_ids < 0 ||
+        decode_ids >= (int64_t)kGidMask)
+        return RECMG_E_INVALID_CONFIG;
     if (batch > 0 && (!packed || !gid || !tid)) return RECMG_E_INVALID_CONFIG;
     if (precision == RECMG_PREC_TC32) {
         if (!tc_supported(shape)) return RECMG_E_INVALID_CONFIG;
         return model_forward_tc(shape, packed, (const char *)packed + dense_bytes_aligned(shape),
                                 gid, tid, batch, logits, bits, pf_gid, ws, ws_bytes,
-                                as_stream(stream));
+                                as_stream(stream), nullptr, decode_ids);
     }
     if (precision != RECMG_PREC_FP32) return RECMG_E_INVALID_CONFIG;
     if (batch > 0 && !embed_id) return RECMG_E_INVALID_CONFIG;
     return model_forward_fp32(shape, embed_id, packed, gid, tid, batch, logits, bits, pf_gid,
-                              as_stream(stream));
+                              as_stream(stream), decode_ids);
+}
+
+int recmg_model_forward(const recmg_model_shape *shape, int32_t precision,
+                        const float *embed_id, const void *packed, const int32_t *gid,
+                        const int32_t *tid, int64_t batch, float *logits, uint8_t *bits,
+                        int32_t *pf_gid, void *ws, size_t ws_bytes, void *stream) {
+    return recmg_model_forward_ex(shape, precision, embed_id, packed, gid, tid, batch, 0, logits,
+                                  bits, pf_gid, ws, ws_bytes, stream);
 }
 
 int recmg_set_model_sm_budget(int n) { return set_model_sm_budget(n); }
@@ -432,6 +443,38 @@ int recmg_table_ids(const int32_t *gids, int64_t n, const int64_t *offsets, int3
     if (n == 0) return RECMG_OK;
     table_ids_kernel<<<(unsigned)imin64((n + 255) / 256, 16 * kSmCount), 256, 0,
                        as_stream(stream)>>>(gids, n, offsets, n_tables, tid);
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+// global gid -> (shard-local row, shard-local table) for a table shard
+__global__ void shard_local_ids_kernel(const int32_t *gids, int64_t n, const int64_t *offsets,
+                                       int32_t n_tables, const int32_t *table_local,
+                                       const int64_t *local_offsets, int32_t *lgid,
+                                       int32_t *ltid) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = gids[i];
+        int lo = 0, hi = n_tables;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(offsets + mid) <= g) lo = mid; else hi = mid;
+        }
+        const int32_t lt = __ldg(table_local + lo);
+        ltid[i] = lt;
+        lgid[i] = lt < 0 ? -1 : (int32_t)(g - __ldg(offsets + lo) + __ldg(local_offsets + lt));
+    }
+}
+
+int recmg_shard_local_ids(const int32_t *gids, int64_t n, const int64_t *offsets,
+                          int32_t n_tables, const int32_t *table_local,
+                          const int64_t *local_offsets, int32_t *local_gids,
+                          int32_t *local_tids, void *stream) {
+    if (n < 0 || n_tables < 1) return RECMG_E_INVALID_CONFIG;
+    if (n == 0) return RECMG_OK;
+    shard_local_ids_kernel<<<(unsigned)imin64((n + 255) / 256, 16 * kSmCount), 256, 0,
+                             as_stream(stream)>>>(gids, n, offsets, n_tables, table_local,
+                                                  local_offsets, local_gids, local_tids);
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
 }

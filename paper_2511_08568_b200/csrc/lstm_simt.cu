@@ -339,11 +339,12 @@ int model_pack(const recmg_model_shape *m, const float *raw, void *packed, cudaS
 
 int model_forward_fp32(const recmg_model_shape *m, const float *embed_id, const void *packed,
                        const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
-                       uint8_t *bits, int32_t *pf_gid, cudaStream_t s) {
+                       uint8_t *bits, int32_t *pf_gid, cudaStream_t s, int64_t decode_ids) {
     if (batch <= 0) return RECMG_OK;
     FwdArgs a;
     a.m = *m;
     a.pl = packed_layout(m);
+    if (decode_ids > 0) a.m.total_ids = decode_ids;   // decode scale only (table shards)
     a.embed_id = embed_id;
     a.w = (const float *)packed;
     a.gid = gid;

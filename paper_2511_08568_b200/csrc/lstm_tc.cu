@@ -1061,7 +1061,7 @@ int set_model_sm_budget(int n) {
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,
-                     long long *prof) {
+                     long long *prof, int64_t decode_ids) {
     if (batch <= 0) return RECMG_OK;
     const int64_t n_tiles = (batch + 127) / 128;
     const int grid = (int)imin64(n_tiles, g_model_sm_budget);
@@ -1070,6 +1070,7 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
     a.m = *m;
     a.tl = tc_layout(m);
     a.pl = packed_layout(m);
+    if (decode_ids > 0) a.m.total_ids = decode_ids;   // decode scale only (table shards)
     a.blob = (const uint8_t *)tc_blob;
     a.dense = (const float *)packed_dense;
     a.gid = gid;

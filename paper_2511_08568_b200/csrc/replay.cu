@@ -163,47 +163,70 @@ __device__ __forceinline__ void flush_counters(recmg_counters *ctr, unsigned lon
 // round trip per 32-event batch (the replay of the hottest set is a single
 // dependency chain).
 constexpr int kRingBlk = 256;
-constexpr int kRingSlots = 4;
+constexpr int kRingSlots = 8;                      // power of two
+constexpr int kRingMask = kRingBlk * kRingSlots - 1;
+constexpr int kL2Ahead = 32;   // blocks prefetched into L2 beyond the ring (long segments)
 
 struct EventRing {
-    uint32_t *buf;       // [kRingSlots * kRingBlk] shared
-    const uint32_t *ev;  // global segment base (= ev + lo)
-    int64_t n;           // segment length
+    uint32_t *buf;       // [kRingSlots * kRingBlk] shared, 16 B aligned
+    const uint32_t *src; // segment base rounded down to 16 B
+    int64_t n;           // words from src to the segment end
     int64_t nblk, issued;
+    int shift;           // words between src and the segment start
     int lane;
 
+    // block k = words [k*256, k*256+256) from src into slot k % kRingSlots:
+    // full blocks as 16 B cp.async (2 per lane), the last one word by word
     __device__ __forceinline__ void issue_next() {
         const int64_t k = issued;
-        const uint32_t *src = ev + k * kRingBlk;
-        uint32_t *dst = buf + (k % kRingSlots) * kRingBlk;
-        const int cnt = (int)imin64(kRingBlk, n - k * kRingBlk);
-        for (int i = lane; i < cnt; i += 32) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(dst + i)),
-                         "l"(src + i) : "memory");
+        const uint32_t *s = src + k * kRingBlk;
+        uint32_t *d = buf + (k & (kRingSlots - 1)) * kRingBlk;
+        const int64_t cnt = n - k * kRingBlk;
+        // the hottest set's segment is one long serial stream: keep L2 ahead of
+        // the ring so every ring block is an L2 hit (one 128 B line per lane)
+        if (k + kL2Ahead < nblk && lane < kRingBlk * 4 / 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(s + kL2Ahead * kRingBlk + lane * 32));
+        if (cnt >= kRingBlk) {
+#pragma unroll
+            for (int t = 0; t < 2; t++) {
+                const int c = (lane + 32 * t) * 4;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(d + c)),
+                             "l"(s + c) : "memory");
+            }
+        } else {
+            for (int i = lane; i < cnt; i += 32) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(d + i)),
+                             "l"(s + i) : "memory");
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         issued++;
     }
     __device__ __forceinline__ void init(uint32_t *b, const uint32_t *e, int64_t len, int l) {
-        buf = b; ev = e; n = len; lane = l; issued = 0;
-        nblk = (len + kRingBlk - 1) / kRingBlk;
+        shift = (int)((reinterpret_cast<uintptr_t>(e) >> 2) & 3);
+        buf = b; src = e - shift; n = len + shift; lane = l; issued = 0;
+        nblk = len > 0 ? (n + kRingBlk - 1) / kRingBlk : 0;
         while (issued < nblk && issued < kRingSlots) issue_next();
     }
-    // make events [r, r + cnt) (relative) readable; refill freed slots
+    // make segment events [r, r + cnt) readable; refill freed slots
     __device__ __forceinline__ void ensure(int64_t r, int cnt) {
-        const int64_t k0 = r / kRingBlk;
+        const int64_t k0 = (r + shift) / kRingBlk;
         while (issued < nblk && issued < k0 + kRingSlots) issue_next();
-        const int64_t k1 = (r + cnt - 1) / kRingBlk;
+        const int64_t k1 = (r + shift + cnt - 1) / kRingBlk;
         const int64_t pending = issued - 1 - k1;   // groups allowed to stay in flight
         if (pending <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
         else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
         else if (pending == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-        else asm volatile("cp.async.wait_group 3;" ::: "memory");
+        else if (pending == 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+        else if (pending == 4) asm volatile("cp.async.wait_group 4;" ::: "memory");
+        else if (pending == 5) asm volatile("cp.async.wait_group 5;" ::: "memory");
+        else asm volatile("cp.async.wait_group 6;" ::: "memory");
         __syncwarp();
     }
     __device__ __forceinline__ uint32_t at(int64_t r) const {
-        return buf[((r / kRingBlk) % kRingSlots) * kRingBlk + (r % kRingBlk)];
+        return buf[(uint32_t)(r + shift) & kRingMask];
     }
 };
 
@@ -404,7 +427,118 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
         __syncwarp();
     };
 
+    // Uniform-run fast path.  Under Zipf skew the hottest set's segment is
+    // mostly long runs of events on ONE resident gid (at
+    // config 3 one id is half of a shard's accesses).  Hits never change
+    // residency, so a window whose real events all name one resident gid is
+    // applied in O(1): S count (the first S takes the prefetch tag), last
+    // U/P write, last-use clock.  Tried only after a 64-event step that was
+    // itself one such run, so other sets pay nothing.
+    constexpr int kFast = 512;          // events per fast step (16 per lane)
+    bool try_fast = false;
     for (int64_t pos = lo; pos < hi;) {
+        if (try_fast && hi - pos >= 64) {
+            const int nf = (int)imin64(kFast, hi - pos);
+            const int64_t r0 = pos - lo;
+            ring.ensure(r0, nf);
+            const uint32_t ef = ring.at(r0);
+            const uint32_t G = ev_gid(ef);
+            // the window's events all name G (in any event type): its effect
+            // is the first/last S, the last U/P and the counts.  Per event: one
+            // LDS, an xor-and into the uniformity word and (replays only) two
+            // ballots; positions i = j*32 + lane are in event order.
+            uint32_t diff = 0, lastUe = 0;
+            unsigned sm[kFast / 32], um[kFast / 32];
+            constexpr bool TRACK = PRIO || LRUPF;
+#pragma unroll
+            for (int j = 0; j < kFast / 32; j++) {
+                const int i = j * 32 + lane;
+                const uint32_t e = i < nf ? ring.at(r0 + i) : ef;
+                diff |= (e ^ G) & kGidMask;
+                if (TRACK) {
+                    const bool isS = i < nf && e == G;            // EV_SERVE == 0
+                    const bool isU = i < nf && e != G && (!LRUPF || ev_type(e) == EV_PREFETCH);
+                    sm[j] = __ballot_sync(FULL, isS);
+                    um[j] = __ballot_sync(FULL, isU);
+                    lastUe = isU ? e : lastUe;
+                }
+            }
+            const int way = (G != kGidMask) ? ht_find(v, G) : -1;
+            if (__all_sync(FULL, diff == 0) && way >= 0) {
+                unsigned nS = 0;
+                int fS = -1, lS = -1, lU = -1;
+                if (TRACK) {
+#pragma unroll
+                    for (int j = 0; j < kFast / 32; j++) {
+                        nS += __popc(sm[j]);
+                        if (fS < 0 && sm[j]) fS = j * 32 + __ffs(sm[j]) - 1;
+                        if (sm[j]) lS = j * 32 + 31 - __clz(sm[j]);
+                        if (um[j]) lU = j * 32 + 31 - __clz(um[j]);
+                    }
+                }
+                const uint32_t lUty = ev_type(__shfl_sync(FULL, lastUe, lU >= 0 ? (lU & 31) : 0));
+                if (PRIO) {
+                    const int64_t m0 = v.meta[way];
+                    const bool f0 = (m0 >> 32) & 1;
+                    if (lane == 0) {
+                        int32_t pr = (int32_t)(m0 & 0xFFFFFFFF);
+                        bool f = f0;
+                        if (nS) {
+                            if (f) { ph += 1; ch += nS - 1; f = false; }
+                            else ch += nS;
+                        }
+                        if (lU >= 0) pr = a.es + (lUty == EV_UPD1 ? 1 : 0);
+                        if (nS || lU >= 0) v.meta[way] = (int64_t)(uint32_t)pr | ((int64_t)f << 32);
+                    }
+                    if (CLASS) {
+#pragma unroll
+                        for (int j = 0; j < kFast / 32; j++) {
+                            const int i = j * 32 + lane;
+                            if (i < nf && ev_type(ring.at(r0 + i)) == EV_SERVE)
+                                write_class(a, pos + i, (f0 && i == fS) ? 1 : 0);
+                        }
+                    }
+                } else if (LRUPF) {
+                    const int64_t m0 = v.meta[way];
+                    const bool f0 = (m0 >> 62) & 1;
+                    if (lane == 0 && nS) {
+                        if (f0) { ph += 1; ch += nS - 1; }
+                        else ch += nS;
+                        v.meta[way] = clock_base + pos + lS;
+                    }
+                    if (CLASS) {
+#pragma unroll
+                        for (int j = 0; j < kFast / 32; j++) {
+                            const int i = j * 32 + lane;
+                            if (i < nf && ev_type(ring.at(r0 + i)) == EV_SERVE)
+                                write_class(a, pos + i, (f0 && i == fS) ? 1 : 0);
+                        }
+                    }
+                } else {
+                    // simulate(): every event is a serve hit
+                    if (lane == 0) {
+                        const int last = nf - 1;
+                        const int64_t clk = clock_base + pos + last;
+                        if (LFU) v.meta[way] = (((v.meta[way] >> 40) + nf) << 40) | clk;
+                        else if (SRRIP) v.meta[way] = 0;
+                        else if (OPT) v.meta[way] = a.next_use[a.vals ? a.vals[pos + last] : pos + last];
+                        else v.meta[way] = clk;
+                        lhits += nf;
+                    }
+                    if (a.per_access_hit) {
+#pragma unroll
+                        for (int j = 0; j < kFast / 32; j++) {
+                            const int i = j * 32 + lane;
+                            if (i < nf) a.per_access_hit[a.vals ? a.vals[pos + i] : pos + i] = 1;
+                        }
+                    }
+                }
+                __syncwarp();
+                pos += nf;
+                continue;
+            }
+            try_fast = false;
+        }
         // 64 events per step (two per lane): membership of both halves against
         // the same tag set, one cut, the run applied half by half
         const int nb = (int)imin64(64, hi - pos);
@@ -430,6 +564,15 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             miss1 = __ballot_sync(FULL, real1 && way1 < 0);
         }
         const int cut = miss0 ? (__ffs(miss0) - 1) : (miss1 ? 32 + __ffs(miss1) - 1 : nb);
+        {
+            // a whole 64-window of hits on one gid: the next window may be a long run
+            const uint32_t gref = __shfl_sync(FULL, g0, 0);
+            const bool same = (!real0 || g0 == gref) && (!real1 || g1 == gref);
+            try_fast = cut == nb && nb == 64 && __all_sync(FULL, same);
+#ifdef RECMG_NO_FASTRUN
+            try_fast = false;
+#endif
+        }
         apply_run(pos, e0, way0, cut < 32 ? cut : 32);
         if (cut > 32) apply_run(pos + 32, e1, way1, cut - 32);
         const uint32_t e = cut < 32 ? e0 : e1;
@@ -580,7 +723,7 @@ replay_wide_kernel(ReplayArgs a) {
     const unsigned lt = (1u << lane) - 1u;
     int64_t free_hint = 0;
 
-    __shared__ uint32_t ring_buf[kRingSlots * kRingBlk];
+    __shared__ __align__(16) uint32_t ring_buf[kRingSlots * kRingBlk];
     EventRing ring;
     ring.init(ring_buf, a.ev + lo, hi - lo, lane);
     for (int64_t pos = lo; pos < hi;) {

@@ -126,11 +126,15 @@ class DeviceModel:
     precision "fp32": the SIMT kernel (csrc/lstm_simt.cu), any dim <= 64.
     """
 
-    def __init__(self, params: ModelParameters, embed_id=None, precision: str = "auto"):
+    def __init__(self, params: ModelParameters, embed_id=None, precision: str = "auto",
+                 decode_ids: int = 0):
+        """decode_ids: the global id count a table shard's prefetch decode
+        scales by (model.py:255); 0 = params.total_ids (an unsharded model)."""
         torch = _native.torch_cuda()
         L = _native.lib()
         self.params = params
         self.kind = params.kind
+        self.decode_ids = int(decode_ids)
         self.shape = _native.ModelShape(
             _native.MODEL_CACHING if params.kind == CACHING else _native.MODEL_PREFETCH,
             int(params.dim), int(params.stacks), int(params.l_in), int(params.l_out),
@@ -193,9 +197,9 @@ class DeviceModel:
         if logits is None:
             logits = torch.empty((B, self.out_len), dtype=torch.float32, device="cuda")
         ws = self.workspace(B)
-        _native.check(_native.lib().recmg_model_forward(
+        _native.check(_native.lib().recmg_model_forward_ex(
             ctypes.byref(self.shape), self.prec, _native.ptr(self.embed_id),
-            _native.ptr(self.packed), _native.ptr(gid), _native.ptr(tid), B,
+            _native.ptr(self.packed), _native.ptr(gid), _native.ptr(tid), B, self.decode_ids,
             _native.ptr(logits), _native.ptr(bits), _native.ptr(pf_gid), _native.ptr(ws),
             ws.numel() if ws is not None else 0, _native.stream_handle(torch)), "model_forward")
         return logits

@@ -32,13 +32,19 @@ class HotPath:
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
                  n_max: int, ways: int | None = 32, eviction_speed: int = 4,
                  lru_capacity: int | None = None, lru_ways: int | None = 32, l_in: int = 15,
-                 l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 146):
+                 l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 146,
+                 shard=None):
         """pieces > 1 pipelines the replay: chunks are scored in `pieces`
         ranges on the main stream while earlier ranges replay on a side stream
         (recmg_replay_chunks continues the buffer state, so the result is the
         same as one replay); the LRU comparator runs on a third stream from
         the start.  The TC forwards then use `model_sms` SMs, leaving the rest
-        to the replay CTAs."""
+        to the replay CTAs.
+
+        shard (shard.TableShard): the models are a table shard's, packed over
+        its local vocabulary (shard.init_params_shard, DeviceModel with
+        decode_ids = the global id count); the forwards then read local ids
+        made on the device by recmg_shard_local_ids, the replay global ones."""
         torch = _native.torch_cuda()
         self.torch = torch
         self.table_sizes = [int(s) for s in table_sizes]
@@ -47,9 +53,15 @@ class HotPath:
             else DeviceModel(caching)
         self.prefetch = prefetch if (prefetch is None or isinstance(prefetch, DeviceModel)) \
             else DeviceModel(prefetch)
+        self.shard = shard
+        model_sizes = self.table_sizes if shard is None else list(shard.local_sizes)
+        if shard is not None and list(shard.table_sizes) != self.table_sizes:
+            raise ValueError("shard does not match the table layout")
         for m, kind in ((self.caching, CACHING), (self.prefetch, PREFETCH)):
-            if m is not None and (m.kind != kind or m.params.table_sizes != self.table_sizes):
+            if m is not None and (m.kind != kind or m.params.table_sizes != model_sizes):
                 raise ValueError(f"{kind} model does not match the table layout")
+            if m is not None and shard is not None and m.decode_ids != shard.total_ids:
+                raise ValueError(f"{kind} shard model must decode over the global ids")
         self.l_in, self.l_out, self.window_ratio = l_in, l_out, window_ratio
         self.n_max = int(n_max)
         self.K_max = num_chunks(self.n_max, l_in, l_out, window_ratio)
@@ -57,6 +69,11 @@ class HotPath:
         self.offsets = torch.from_numpy(table_offsets(self.table_sizes)).cuda()
         self.gids = torch.empty(max(self.n_max, 1), dtype=torch.int32, device="cuda")
         self.tid = torch.empty(max(self.K_max * l_in, 1), dtype=torch.int32, device="cuda")
+        self.lgid = None
+        if shard is not None:
+            self.lgid = torch.empty(max(self.K_max * l_in, 1), dtype=torch.int32, device="cuda")
+            self.table_local = torch.from_numpy(shard.table_local).cuda()
+            self.local_offsets = torch.from_numpy(shard.local_offsets).cuda()
         self.bits = torch.empty((max(self.K_max, 1), l_in), dtype=torch.uint8, device="cuda")
         self.pf = torch.empty((max(self.K_max, 1), l_out), dtype=torch.int32, device="cuda")
         self.clog = torch.empty((max(self.K_max, 1), l_in), dtype=torch.float32, device="cuda")
@@ -122,9 +139,18 @@ class HotPath:
             if K and (self.caching is not None or self.prefetch is not None):
                 gk = g[:K * self.l_in].view(K, self.l_in)
                 tk = self.tid[:K * self.l_in].view(K, self.l_in)
-                _native.check(L.recmg_table_ids(_native.ptr(gk), K * self.l_in,
-                                                _native.ptr(self.offsets), len(self.table_sizes),
-                                                _native.ptr(tk), _native.stream_handle(torch)))
+                if self.shard is None:
+                    _native.check(L.recmg_table_ids(
+                        _native.ptr(gk), K * self.l_in, _native.ptr(self.offsets),
+                        len(self.table_sizes), _native.ptr(tk), _native.stream_handle(torch)))
+                else:
+                    lk = self.lgid[:K * self.l_in].view(K, self.l_in)
+                    _native.check(L.recmg_shard_local_ids(
+                        _native.ptr(gk), K * self.l_in, _native.ptr(self.offsets),
+                        len(self.table_sizes), _native.ptr(self.table_local),
+                        _native.ptr(self.local_offsets), _native.ptr(lk), _native.ptr(tk),
+                        _native.stream_handle(torch)))
+                    gk = lk   # the forwards read shard-local ids
             self._ev("table_ids", main)
             self.s_replay.wait_event(ready)
             with torch.cuda.stream(self.s_replay):

@@ -150,6 +150,87 @@ def generate_trace(cfg: TraceGenConfig) -> Trace:
     return Trace(gids, cfg.table_sizes)
 
 
+class TraceStream:
+    """generate_trace (trace.py:124-161) streamed block by block, bit-exact.
+
+    For traces the reference cannot materialise (config 3: 5e8 accesses over
+    8.56e7 ids).  The permutation is numpy's own (the same call on the same
+    default_rng); the PCG64 state right after it seeds the three random()
+    streams, which recmg_trace_generate_block reaches at outputs i0, n+i0
+    and 2n+i0 by jump-ahead.  Blocks must be drawn in order (the sticky pool
+    carries over); every block is int32 gids.
+    """
+
+    GUIDE_LOG2 = 24
+
+    def __init__(self, cfg: TraceGenConfig, threads: int | None = None):
+        import os
+        cfg.validate()
+        self.cfg = cfg
+        self.n = int(cfg.total_accesses)
+        self.V = int(sum(cfg.table_sizes))
+        if self.V > np.iinfo(np.int32).max:
+            raise InvalidConfigError("streamed traces need fewer than 2^31 ids")
+        rng = np.random.default_rng(cfg.rng_seed)
+        ranks = np.arange(1, self.V + 1, dtype=np.float64)
+        weights = ranks ** (-cfg.zipf_exponent)
+        del ranks
+        probs = weights / weights.sum()
+        del weights
+        self.rank_to_gid = rng.permutation(self.V)
+        cdf = probs.cumsum()
+        del probs
+        cdf /= cdf[-1]
+        self.cdf = cdf
+        st = rng.bit_generator.state["state"]
+        m64 = (1 << 64) - 1
+        self.pcg = np.array([st["state"] >> 64, st["state"] & m64, st["inc"] >> 64,
+                             st["inc"] & m64], dtype=np.uint64)
+        self.guide_log2 = self.GUIDE_LOG2 if self.V > 4096 else 12
+        self.guide = np.empty((1 << self.guide_log2) + 1, dtype=np.int64)
+        _native.check(_native.lib().recmg_trace_guide(self.cdf.ctypes.data, self.V,
+                                                      self.guide_log2, self.guide.ctypes.data),
+                      "trace_guide")
+        self.pool = np.zeros(cfg.correlation_pool_size, dtype=np.int64)
+        self.pool_len = np.zeros(1, dtype=np.int32)
+        self.pos = 0
+        self.threads = threads or max(1, min(16, len(os.sched_getaffinity(0))))
+
+    def next_block(self, count: int) -> np.ndarray:
+        count = min(int(count), self.n - self.pos)
+        out = np.empty(count, dtype=np.int32)
+        if count:
+            _native.check(_native.lib().recmg_trace_generate_block(
+                self.pcg.ctypes.data, self.n, self.pos, count, self.cdf.ctypes.data, self.V,
+                self.guide.ctypes.data, self.guide_log2, self.rank_to_gid.ctypes.data,
+                float(self.cfg.markov_stickiness), int(self.cfg.correlation_pool_size),
+                self.pool.ctypes.data, self.pool_len.ctypes.data, out.ctypes.data,
+                self.threads), "trace_generate_block")
+        self.pos += count
+        return out
+
+    def blocks(self, block: int = 1 << 24):
+        while self.pos < self.n:
+            yield self.next_block(block)
+
+    def uniforms(self, skip: int, count: int) -> np.ndarray:
+        """Generator.random() outputs [skip, skip+count) after the permutation."""
+        out = np.empty(int(count), dtype=np.float64)
+        _native.check(_native.lib().recmg_pcg64_uniforms(self.pcg.ctypes.data, int(skip),
+                                                         int(count), out.ctypes.data,
+                                                         self.threads), "pcg64_uniforms")
+        return out
+
+
+def generate_trace_streamed(cfg: TraceGenConfig, block: int = 1 << 24) -> np.ndarray:
+    """All gids of generate_trace(cfg) as int32, drawn block by block."""
+    s = TraceStream(cfg)
+    out = np.empty(s.n, dtype=np.int32)
+    for b in s.blocks(block):
+        out[s.pos - len(b):s.pos] = b
+    return out
+
+
 @dataclass
 class SequenceSample:
     """trace.py:207-223."""

@@ -240,6 +240,55 @@ def make_small():
     print("small_replay.npz written")
 
 
+def make_hot():
+    """A trace dominated by one id (85% of accesses, long runs): the replay
+    kernels' uniform-run fast path (csrc/replay.cu) against the reference
+    per-set buffer, simulate() policies and replay_policy_only."""
+    rng = np.random.default_rng(77)
+    V, n = 400, 12000
+    gids = np.where(rng.random(n) < 0.85, 7, rng.integers(0, V, n)).astype(np.int64)
+    gids[3000:3700] = 7                       # a run longer than any batch
+    gids[5000:5400] = 7 + 64                  # a second hot id sharing set 7 (mod 32/64)
+    t = embcache.trace_from_gids(gids, [V])
+    K = len(embcache.chunk(t))
+    bits = rng.integers(0, 2, (K, 15)).astype(np.uint8)
+    pf = rng.integers(0, V, (K, 5))
+    pf[rng.random((K, 5)) < 0.3] = 7          # full rows: per_set_replay takes them raw
+    lists = [[int(g) for g in row] for row in pf]
+    out = {"gids": gids, "bits": bits, "pf": pf}
+    sa_cases, sa_counts = [], []
+    for cap, ways in ((32, 32), (64, 32), (24, 4), (8, 8)):
+        for es in (4, cap):
+            sa_cases.append([cap, ways, es])
+            sa_counts.append(per_set_replay(t, cap, ways, es, bits, pf))
+    out["sa_cases"] = np.array(sa_cases)
+    out["sa_counts"] = np.array(sa_counts)
+    pol_cases, pol_hits, pol_pa, pol_keep = [], [], [], []
+    for pi, pol in enumerate((cache_sim.Policy.LRU, cache_sim.Policy.LFU, cache_sim.Policy.SRRIP,
+                              cache_sim.Policy.OPTGEN)):
+        for cap, ways in ((32, 32), (64, 32), (24, 4), (40, None)):
+            r = cache_sim.simulate(t, cache_sim.CacheConfig(cap, pol, ways))
+            pol_cases.append([pi, cap, 0 if ways is None else ways])
+            pol_hits.append(r.hits)
+            pol_pa.append(np.array(r.per_access_hit, dtype=np.uint8))
+            pol_keep.append(np.array(r.keep_decisions if r.keep_decisions is not None
+                                     else [0] * len(t), dtype=np.uint8))
+    out["pol_cases"] = np.array(pol_cases)
+    out["pol_hits"] = np.array(pol_hits)
+    out["pol_per_access"] = np.stack(pol_pa)
+    out["pol_keep"] = np.stack(pol_keep)
+    lp_counts = []
+    for cap in (16, 100):
+        lp = rt.replay_policy_only(t, cache_sim.CacheConfig(cap, cache_sim.Policy.LRU),
+                                   prefetch_fn=lambda s: lists[s.origin // 15])
+        lp_counts.append([cap, lp.cache_hits, lp.prefetch_hits, lp.on_demand,
+                          lp.prefetch_issued, lp.prefetch_useful])
+    out["lrupf_counts"] = np.array(lp_counts)
+    out["meta"] = np.array(json.dumps(META))
+    np.savez_compressed(os.path.join(HERE, "hot_runs.npz"), **out)
+    print("hot_runs.npz written")
+
+
 def make_models():
     """Reference forward outputs for several shapes / init scales."""
     out = {}
@@ -332,7 +381,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
     jobs = {"small": make_small, "models": make_models, "traces": make_traces,
-            "config1": make_config1}
+            "config1": make_config1, "hot": make_hot}
     for name, fn in jobs.items():
         if a.only and name != a.only:
             continue

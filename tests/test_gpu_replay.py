@@ -238,3 +238,36 @@ def test_optgen_known_answers():
     # test_cache_sim.py:19-24 (LFU keeps the hot block)
     res = rb.simulate(rb.trace_from_gids(letters("AABCA"), [3]), rb.CacheConfig(2, rb.Policy.LFU))
     assert res.per_access_hit == [0, 1, 0, 0, 1]
+
+
+def test_hot_runs_vs_reference():
+    """One id carries 85% of the trace (long single-gid runs): the replay
+    kernels' uniform-run fast path against the reference per-set buffer,
+    simulate() for LRU/LFU/SRRIP/OPTGEN (per-access hits, keep bits) and
+    replay_policy_only with prefetches; access classes against the oracle."""
+    z = golden("hot_runs.npz")
+    gids, bits, pf = z["gids"], z["bits"], z["pf"]
+    t = rb.trace_from_gids(gids, [400])
+    cfn, pfn = _fns(bits, pf)
+    for case, cnt in zip(z["sa_cases"], z["sa_counts"]):
+        cap, ways, es = (int(x) for x in case)
+        rep, cls = rb.replay(t, rb.BufferConfig(cap, es, ways), caching_fn=cfn, prefetch_fn=pfn,
+                             return_access_class=True)
+        got = [rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.evictions,
+               rep.prefetch_inserts]
+        assert got == list(cnt[:5]), case
+        _, _, rcls = oracle.replay(gids, 400, cap, ways, es, bits=bits, pf=pf, access_class=True)
+        assert np.array_equal(cls, rcls), case
+    pols = (rb.Policy.LRU, rb.Policy.LFU, rb.Policy.SRRIP, rb.Policy.OPTGEN)
+    for case, hits, pa, keep in zip(z["pol_cases"], z["pol_hits"], z["pol_per_access"],
+                                    z["pol_keep"]):
+        pol, cap, ways = pols[int(case[0])], int(case[1]), int(case[2]) or None
+        res = rb.simulate(t, rb.CacheConfig(cap, pol, ways))
+        assert res.hits == hits and res.per_access_hit == pa.tolist(), (pol, cap, ways)
+        if pol == rb.Policy.OPTGEN:
+            assert res.keep_decisions == keep.tolist(), (cap, ways)
+    for row in z["lrupf_counts"]:
+        cap = int(row[0])
+        rep = rb.replay_policy_only(t, rb.CacheConfig(cap, rb.Policy.LRU), prefetch_fn=pfn)
+        assert [rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
+                rep.prefetch_useful] == [int(x) for x in row[1:]], cap

@@ -108,6 +108,35 @@ def test_generate_trace_bit_exact():
         i += 1
 
 
+def test_streamed_generator_matches_reference_hashes():
+    """TraceStream (block-wise, PCG64 jump-ahead, guide-table searchsorted)
+    reproduces the reference generate_trace outputs (golden sha256 made by
+    running the reference, tests/golden/make_golden.py)."""
+    from paper_2511_08568_b200.trace import generate_trace_streamed
+    z = golden("traces.npz")
+    i = 0
+    while f"cfg{i}" in z:
+        ts, n, s, p, pool, seed = json.loads(str(z[f"cfg{i}"]))
+        for block in (997, 1 << 20):
+            g = generate_trace_streamed(rb.TraceGenConfig(ts, n, s, p, pool, seed), block)
+            assert hashlib.sha256(g.astype(np.int64).tobytes()).hexdigest() == str(z[f"sha{i}"])
+        i += 1
+    c1 = golden("config1.npz")
+    g = generate_trace_streamed(rb.TraceGenConfig([2000] * 8, 1_000_000, 1.05, 0.4, 32, 0),
+                                 300_001)
+    assert hashlib.sha256(g.astype(np.int64).tobytes()).hexdigest() == str(c1["sha"])
+
+
+def test_pcg64_jump_ahead_matches_numpy():
+    from paper_2511_08568_b200.trace import TraceStream
+    s = TraceStream(rb.TraceGenConfig([100] * 3, 1000, 1.05, 0.4, 32, 5))
+    rng = np.random.default_rng(5)
+    rng.permutation(300)
+    u = rng.random(5000)
+    assert np.array_equal(s.uniforms(0, 5000), u)
+    assert np.array_equal(s.uniforms(4321, 600), u[4321:4921])
+
+
 def test_coverage_mean_is_sequential_float64():
     rng = np.random.default_rng(0)
     num = rng.integers(0, 6, 5000).astype(np.uint8)

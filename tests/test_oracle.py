@@ -107,3 +107,22 @@ def test_config1_golden_counts_oracle():
     assert [r["cache_hits"], r["prefetch_hits"], r["on_demand"], r["evictions"],
             r["prefetch_inserts"]] == list(z["w32_es4"][:5])
     assert 1_000_000 - oracle.lru(t.gid_array, 16000, C32, 32) == int(z["lru32_misses"])
+
+
+def test_oracle_hot_runs_vs_reference():
+    """The C oracle on the hot-run fixture (one id = 85% of accesses) equals
+    the reference's per-set buffer and LRU."""
+    z = golden("hot_runs.npz")
+    gids, bits, pf = z["gids"], z["bits"], z["pf"]
+    for case, cnt in zip(z["sa_cases"], z["sa_counts"]):
+        cap, ways, es = (int(x) for x in case)
+        ref, _ = oracle.replay(gids, 400, cap, ways, es, bits=bits, pf=pf)
+        got = [ref[k] for k in ("cache_hits", "prefetch_hits", "on_demand", "evictions",
+                                "prefetch_inserts")]
+        assert got == list(cnt[:5]), case
+    for case, hits, pa in zip(z["pol_cases"], z["pol_hits"], z["pol_per_access"]):
+        if int(case[0]) != 0:
+            continue
+        cap, ways = int(case[1]), int(case[2])
+        h, p = oracle.lru(gids, 400, cap, ways, per_access=True)
+        assert h == hits and np.array_equal(p, pa), case
