@@ -258,6 +258,15 @@ int recmg_set_model_sm_budget(int n);
  * searchsorted of trace.py:86 / index_of_global trace.py:44-51.             */
 int recmg_table_ids(const int32_t *gids, int64_t n, const int64_t *offsets, int32_t n_tables,
                     int32_t *tid, void *stream);
+/* Host: body of the text trace format (read_trace, trace.py:172-204):
+ * parses "table_id,row_id" lines of host_buf from byte `pos` into global
+ * ids (host_out, up to cap, appended at *n_out) while every line has the
+ * plain form and is in range; stops at the first other line (*stop_pos =
+ * its first byte, for the caller's reference-rule reader) or at len.
+ * *lines_done = lines consumed, blank lines included.                        */
+int recmg_trace_parse_text(const char *host_buf, int64_t len, int64_t pos,
+                           const int64_t *host_offsets, int32_t n_tables, int32_t *host_out,
+                           int64_t cap, int64_t *n_out, int64_t *stop_pos, int64_t *lines_done);
 /* Table shard: for every global gid, its row in the
  * shard's local vocabulary and its local table.  table_local[n_tables] maps
  * a global table to its local index (-1: another shard's, then both outputs

@@ -5,6 +5,7 @@ The compute runs in hand-written sm_100a kernels (csrc/) behind the C ABI
 in include/recmg.h, loaded from the in-tree librecmg.so; there is no CPU
 fallback on this path.
 """
+from .checkpoint import load_checkpoint, load_checkpoint_shard, save_checkpoint, vocabulary_hash
 from .cache_sim import CacheConfig, Policy, SimResult, simulate, simulate_optgen, sweep
 from .errors import (CheckpointError, EmbcacheError, InvalidConfigError,
                      MissingArtifactError, NumericalError, OutOfVocabularyError,
@@ -16,7 +17,8 @@ from .runtime import (EVICTION_SPEED, BreakdownReport, BufferConfig, PriorityBuf
                       correctness_vs_window, coverage, gpu_buffer_populate, load_embeddings,
                       replay, replay_policy_only, write_breakdown_csv)
 from .trace import (EmbeddingIndex, SequenceSample, Trace, TraceGenConfig, chunk,
-                    generate_trace, index_of_global, make_index, num_chunks, table_offsets,
-                    trace_from_gids)
+                    TraceStream, generate_trace, generate_trace_streamed, index_of_global,
+                    make_index, num_chunks, read_trace, read_trace_binary, table_offsets,
+                    trace_from_gids, write_trace, write_trace_binary)
 
 __version__ = "0.1.0"

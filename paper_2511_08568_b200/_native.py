@@ -48,7 +48,7 @@ EXPORTS = (
     "recmg_model_workspace_bytes", "recmg_replay_chunks", "recmg_set_model_sm_budget",
     "recmg_model_forward_profile", "recmg_rows_refresh", "recmg_embedding_bag",
     "recmg_simulate_ex", "recmg_model_forward_ex", "recmg_pcg64_uniforms", "recmg_trace_guide",
-    "recmg_trace_generate_block", "recmg_shard_local_ids",
+    "recmg_trace_generate_block", "recmg_shard_local_ids", "recmg_trace_parse_text",
 )
 
 
@@ -110,6 +110,7 @@ def lib():
                                                sz, vp]),
         "recmg_model_forward_ex": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, i64, vp, vp,
                                                   vp, vp, sz, vp]),
+        "recmg_trace_parse_text": (ctypes.c_int, [vp, i64, i64, vp, i32, vp, i64, vp, vp, vp]),
         "recmg_shard_local_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, vp, vp, vp]),
         "recmg_pcg64_uniforms": (ctypes.c_int, [vp, i64, i64, vp, i32]),
         "recmg_trace_guide": (ctypes.c_int, [vp, i64, i32, vp]),

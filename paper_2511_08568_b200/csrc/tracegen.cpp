@@ -158,3 +158,58 @@ extern "C" int recmg_trace_generate_block(const uint64_t pcg[4], int64_t n_total
     *host_pool_len = len;
     return RECMG_OK;
 }
+
+// Text trace body (trace.py:172-204): lines "table_id,row_id".  Parses from
+// byte `pos` while lines have the plain form [ws][+-]digits[ws],[ws][+-]digits[ws]
+// and lie in range; stops at the first other line (the caller re-reads that
+// line with the reference's own rules, which raise or accept it) or at the
+// end.  Blank / whitespace-only lines are skipped, as the reference does.
+extern "C" int recmg_trace_parse_text(const char *host_buf, int64_t len, int64_t pos,
+                                      const int64_t *host_offsets, int32_t n_tables,
+                                      int32_t *host_out, int64_t cap, int64_t *n_out,
+                                      int64_t *stop_pos, int64_t *lines_done) {
+    int64_t n = *n_out, lines = 0;
+    auto ws = [](char ch) { return ch == ' ' || ch == '\t'; };
+    while (pos < len) {
+        const int64_t line_start = pos;
+        int64_t e = pos;
+        while (e < len && host_buf[e] != '\n') e++;
+        int64_t p = pos, q = e;
+        while (p < q && ws(host_buf[p])) p++;
+        while (q > p && ws(host_buf[q - 1])) q--;
+        if (p == q) {                       // blank line
+            pos = e + 1;
+            lines++;
+            continue;
+        }
+        int64_t v[2];
+        bool ok = true;
+        for (int f = 0; f < 2 && ok; f++) {
+            while (p < q && ws(host_buf[p])) p++;
+            bool neg = false;
+            if (p < q && (host_buf[p] == '+' || host_buf[p] == '-')) neg = host_buf[p++] == '-';
+            int64_t x = 0;
+            int digits = 0;
+            while (p < q && host_buf[p] >= '0' && host_buf[p] <= '9' && digits < 18) {
+                x = x * 10 + (host_buf[p++] - '0');
+                digits++;
+            }
+            while (p < q && ws(host_buf[p])) p++;
+            ok = digits > 0 && (f == 0 ? (p < q && host_buf[p] == ',') : p == q);
+            if (f == 0) p++;
+            v[f] = neg ? -x : x;
+        }
+        if (!ok || n >= cap || v[0] < 0 || v[0] >= n_tables || v[1] < 0 ||
+            v[1] >= host_offsets[v[0] + 1] - host_offsets[v[0]]) {
+            pos = line_start;
+            break;
+        }
+        host_out[n++] = (int32_t)(host_offsets[v[0]] + v[1]);
+        pos = e + 1;
+        lines++;
+    }
+    *n_out = n;
+    *stop_pos = pos < len ? pos : len;
+    *lines_done = lines;
+    return RECMG_OK;
+}

@@ -9,12 +9,13 @@ the replay API.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, replace
 
 import numpy as np
 
 from . import _native
-from .errors import InvalidConfigError, TraceValidationError
+from .errors import InvalidConfigError, TraceParseError, TraceValidationError
 
 
 @dataclass(frozen=True, slots=True)
@@ -266,3 +267,144 @@ def chunk(trace, l_in: int = 15, l_out: int = 5, window_ratio: int = 3) -> list:
         out.append(SequenceSample(input=acc[o:o + l_in], origin=o,
                                   window=acc[o + l_in:o + l_in + l_win]))
     return out
+
+
+# ---- trace files (trace.py:164-204) and a binary form for 1e8+ accesses ----
+_LINE_BREAKS = bytes([0x0B, 0x0C, 0x0D, 0x1C, 0x1D, 0x1E, 0x85, 0xA8, 0xA9])
+
+
+def write_trace(trace, path: str):
+    """trace.py:164-169: header 'tables: n1,n2,...' then 'table_id,row_id' lines."""
+    sizes = [int(s) for s in trace.table_sizes]
+    g = np.asarray(trace.gid_array, dtype=np.int64)
+    off = table_offsets(sizes)
+    t = np.searchsorted(off, g, side="right") - 1
+    with open(path, "w", encoding="utf-8") as f:
+        f.write("tables: " + ",".join(str(s) for s in sizes) + "\n")
+        blk = 1 << 20
+        for i in range(0, len(g), blk):
+            tt, rr = t[i:i + blk], g[i:i + blk] - off[t[i:i + blk]]
+            f.write("".join(f"{a},{b}\n" for a, b in zip(tt.tolist(), rr.tolist())))
+
+
+def _parse_line(raw, lineno, table_sizes, offsets):
+    """The reference's per-line rules (trace.py:186-203); None for blank lines."""
+    if not raw.strip():
+        return None
+    parts = raw.split(",")
+    if len(parts) != 2:
+        raise TraceParseError(f"expected 'table_id,row_id', got {raw!r}", line=lineno)
+    try:
+        table_id, row_id = int(parts[0]), int(parts[1])
+    except ValueError:
+        raise TraceParseError(f"non-integer field in {raw!r}", line=lineno)
+    if not 0 <= table_id < len(table_sizes):
+        raise TraceValidationError(f"table_id {table_id} out of range", line=lineno)
+    if not 0 <= row_id < table_sizes[table_id]:
+        raise TraceValidationError(
+            f"row_id {row_id} out of range for table {table_id}", line=lineno)
+    return int(offsets[table_id]) + row_id
+
+
+def _parse_header(first):
+    if not first.startswith("tables: "):
+        raise TraceParseError("expected header 'tables: n1,n2,...'", line=1)
+    try:
+        sizes = [int(tok) for tok in first[len("tables: "):].split(",")]
+    except ValueError as e:
+        raise TraceParseError(f"bad table size list: {e}", line=1)
+    if not sizes or any(s <= 0 for s in sizes):
+        raise TraceValidationError("table sizes must be positive", line=1)
+    return sizes
+
+
+def read_trace(path: str) -> Trace:
+    """trace.py:172-204, same errors and line numbers.  The body is parsed in
+    C (recmg_trace_parse_text) wherever lines have the plain 'int,int' form;
+    any other line is read with the reference's rules, which raise or accept
+    it exactly as the reference does."""
+    with open(path, "rb") as f:
+        data = f.read()
+    if any(b in data for b in _LINE_BREAKS):
+        # str.splitlines() separators beyond '\n' (or non-ASCII text): the
+        # reference's own line splitting, line by line
+        lines = data.decode("utf-8").splitlines()
+        if not lines:
+            raise TraceParseError("expected header 'tables: n1,n2,...'", line=1)
+        sizes = _parse_header(lines[0])
+        off = table_offsets(sizes)
+        out = [g for i, raw in enumerate(lines[1:], start=2)
+               if (g := _parse_line(raw, i, sizes, off)) is not None]
+        return Trace(np.asarray(out, dtype=np.int64), sizes)
+    data.decode("utf-8")    # the reference reads text: invalid UTF-8 raises here too
+    nl = data.find(b"\n")
+    first = (data if nl < 0 else data[:nl]).decode("utf-8")
+    if not data:
+        raise TraceParseError("expected header 'tables: n1,n2,...'", line=1)
+    sizes = _parse_header(first)
+    off = np.ascontiguousarray(table_offsets(sizes), dtype=np.int64)
+    cap = data.count(b"\n") + 1
+    out = np.empty(cap, dtype=np.int32)
+    buf = np.frombuffer(data, dtype=np.uint8)
+    pos, lineno, L = (len(data) if nl < 0 else nl + 1), 2, _native.lib()
+    n, stop, done = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    while pos < len(data):
+        _native.check(L.recmg_trace_parse_text(buf.ctypes.data, len(data), pos, off.ctypes.data,
+                                               len(sizes), out.ctypes.data, cap,
+                                               ctypes.byref(n), ctypes.byref(stop),
+                                               ctypes.byref(done)),
+                      "trace_parse_text")
+        lineno += done.value
+        pos = stop.value
+        if pos >= len(data):
+            break
+        e = data.find(b"\n", pos)
+        e = len(data) if e < 0 else e
+        g = _parse_line(data[pos:e].decode("utf-8"), lineno, sizes, off)
+        if g is not None:
+            out[n.value] = g
+            n.value += 1
+        lineno += 1
+        pos = e + 1
+    return Trace(out[:n.value].astype(np.int64), sizes)
+
+
+_BIN_MAGIC = b"RECMGTR1"
+
+
+def write_trace_binary(trace, path: str):
+    """Binary trace: magic, n_tables (int64), table sizes (int64), n (int64),
+    gids (int32, little endian) -- 4 bytes per access instead of ~10 of text."""
+    sizes = np.asarray([int(s) for s in trace.table_sizes], dtype="<i8")
+    g = np.asarray(trace.gid_array)
+    with open(path, "wb") as f:
+        f.write(_BIN_MAGIC)
+        f.write(np.asarray([len(sizes)], dtype="<i8").tobytes())
+        f.write(sizes.tobytes())
+        f.write(np.asarray([len(g)], dtype="<i8").tobytes())
+        blk = 1 << 24
+        for i in range(0, len(g), blk):
+            f.write(np.ascontiguousarray(g[i:i + blk], dtype="<i4").tobytes())
+
+
+def read_trace_binary(path: str, mmap: bool = False):
+    """Inverse of write_trace_binary; mmap=True maps the gids (int32) without
+    reading them, for traces larger than host memory."""
+    with open(path, "rb") as f:
+        if f.read(8) != _BIN_MAGIC:
+            raise TraceParseError("not a binary trace (bad magic)", line=None)
+        nt = int(np.frombuffer(f.read(8), dtype="<i8")[0])
+        sizes = np.frombuffer(f.read(8 * nt), dtype="<i8").tolist()
+        n = int(np.frombuffer(f.read(8), dtype="<i8")[0])
+        start = f.tell()
+    if not sizes or any(s <= 0 for s in sizes):
+        raise TraceValidationError("table sizes must be positive", line=None)
+    if mmap:
+        g = np.memmap(path, dtype="<i4", mode="r", offset=start, shape=(n,))
+        return g, sizes
+    g = np.fromfile(path, dtype="<i4", count=n, offset=start)
+    if len(g) != n:
+        raise TraceParseError("binary trace truncated", line=None)
+    if n and (g.min() < 0 or g.max() >= sum(sizes)):
+        raise TraceValidationError("global id out of range for table layout")
+    return Trace(g.astype(np.int64), sizes)

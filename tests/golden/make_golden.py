@@ -289,6 +289,38 @@ def make_hot():
     print("hot_runs.npz written")
 
 
+def make_artifacts():
+    """Reference-written artifacts: a checkpoint (save_checkpoint,
+    checkpoint.py:27-45), a text trace (write_trace, trace.py:164-169) and
+    the reference's outcome (gids or error class + message) of read_trace on
+    malformed traces."""
+    p = embcache.init_params("prefetch", [30, 5, 70, 12], dim=8, seed=9, init_scale=0.4)
+    embcache.save_checkpoint(p, os.path.join(HERE, "ref_ckpt_prefetch.npz"))
+    t = embcache.generate_trace(embcache.TraceGenConfig([300, 50, 7], 3000, 1.05, 0.4, 32, 1))
+    embcache.write_trace(t, os.path.join(HERE, "ref_trace.txt"))
+    cases = {"hdr": "tbl: 1,2\n0,0\n", "badsize": "tables: 3,x\n", "neg": "tables: 3,0\n",
+             "fields": "tables: 3,4\n0,1\n1,2,3\n", "nonint": "tables: 3,4\n0,1\n\n a , 2\n",
+             "range": "tables: 3,4\n0,1\n2,0\n", "row": "tables: 3,4\n1,4\n",
+             "ok_ws": "tables: 3,4\n 1 , 3 \n\n+0,2\n1_0,1\n",
+             "crlf": "tables: 3,4\r\n0,1\r\n1,3\r\n\r\n1,9\r\n", "empty": "",
+             "tail_blank": "tables: 3,4\n0,1\n   \n1,0\n\n"}
+    out = {}
+    import tempfile
+    for k, body in cases.items():
+        with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+            f.write(body)
+        try:
+            r = embcache.read_trace(f.name)
+            out[k] = {"body": body, "ok": [a.global_id for a in r.accesses],
+                      "sizes": r.table_sizes}
+        except Exception as e:  # noqa: BLE001 -- record the reference's outcome
+            out[k] = {"body": body, "error": type(e).__name__, "msg": str(e)}
+        os.unlink(f.name)
+    with open(os.path.join(HERE, "ref_trace_cases.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("artifacts written")
+
+
 def make_models():
     """Reference forward outputs for several shapes / init scales."""
     out = {}
@@ -381,7 +413,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
     jobs = {"small": make_small, "models": make_models, "traces": make_traces,
-            "config1": make_config1, "hot": make_hot}
+            "config1": make_config1, "hot": make_hot, "artifacts": make_artifacts}
     for name, fn in jobs.items():
         if a.only and name != a.only:
             continue
