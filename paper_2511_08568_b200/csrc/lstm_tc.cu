@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     constexpr int U = C::U;
     constexpr int NT = C::NT;
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t mbar, mbar2;   // caching: mbar2 tracks the MMAs split off
     __shared__ uint32_t tmem_base_s;
     __shared__ float lpart[PARTS][128];
     __shared__ int s_tile;
@@ -571,14 +571,17 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     c.quad = c.warp & 3;
     c.part = c.warp >> 2;
     c.row = 32 * c.quad + c.lane;
-    if (c.tid == 0) umma::mbar_init(&mbar, 1);
+    if (c.tid == 0) {
+        umma::mbar_init(&mbar, 1);
+        umma::mbar_init(&mbar2, 1);
+    }
     if (c.warp == 0) umma::tmem_alloc<512>(&tmem_base_s);
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
     c.tbase = tmem_base_s;
     c.lane_addr = c.tbase + ((uint32_t)(32 * c.quad) << 16);
-    uint32_t phase = 0;
+    uint32_t phase = 0, phase2 = 0;
     const uint32_t sbase = umma::smem_u32(smem);
     const TcLayout &tl = a.tl;
     const PackedLayout &pl = a.pl;
@@ -625,13 +628,18 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             tmem_writes_done();
             pc.mark(1);
             if (caching) {
+                // Q first (its own barrier), then Z: the keys of step t-1 are
+                // stored while the long N=256 Z product still runs
                 if (c.tid == 0) {
                     umma::fence_after();
-                    if (!last) mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                                    sbase + tl.b_off[0], 256, true);      // Z += h Wh
                     mma3(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
                          sbase + tl.b_off[1], 64, false);                  // Q = h att_enc
                     umma::commit(&mbar);
+                    if (!last) {
+                        mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                             sbase + tl.b_off[0], 256, true);             // Z += h Wh
+                        umma::commit(&mbar2);
+                    }
                 }
                 pc.mark(12);
                 if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
@@ -644,46 +652,54 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     store_keys(Es, c, t - 1, ep, rawmask);
                 }
                 if (!last) {
+                    wait_mma(&mbar2, phase2);
                     cell<false>(c, nullptr, cs0, h);
                     store_operand(c, A_H_HI, A_H_LO, h);
                     storeU(Hs, c, t, h);
                     if (t + 1 < L) stage.commit(c);
                 }
             } else {
-                if (!last) {
-                    // layer 0: Z = Pid + Ptab + h0 Wh0
-                    if (c.tid == 0) {
-                        umma::fence_after();
+                // Q = h1(t-1) att_enc (barrier 2) right behind layer 0: it only
+                // needs h1(t-1), so it runs under the layer-0 cell and the keys
+                // of step t-1 are ready before the layer-1 product finishes
+                if (c.tid == 0) {
+                    umma::fence_after();
+                    if (!last) {
+                        // layer 0: Z = Pid + Ptab + h0 Wh0
                         mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
                              sbase + tl.b_off[0], 256, true);
                         umma::commit(&mbar);
                     }
+                    if (t >= 1) {
+                        mma3(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                             sbase + tl.b_off[3], 64, false);
+                        umma::commit(&mbar2);
+                    }
+                }
+                if (!last) {
                     wait_mma(&mbar, phase);
                     cell<false>(c, nullptr, cs0, h);
                     store_operand(c, P_H0_HI, P_H0_LO, h);
                     tmem_writes_done();
-                }
-                // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell); Q = h1(t-1) att_enc
-                if (c.tid == 0) {
-                    umma::fence_after();
-                    if (!last) {
+                    // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell)
+                    if (c.tid == 0) {
+                        umma::fence_after();
                         mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
                              sbase + tl.b_off[1], 256, false);
                         mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
                              sbase + tl.b_off[2], 256, true);
+                        umma::commit(&mbar);
                     }
-                    mma3(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                         sbase + tl.b_off[3], 64, false);
-                    umma::commit(&mbar);
                 }
                 if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
-                wait_mma(&mbar, phase);
                 if (t >= 1) {
+                    wait_mma(&mbar2, phase2);
                     float ep[U];
                     readU(c, COL_Q, ep);
                     store_keys(Es, c, t - 1, ep, rawmask);
                 }
                 if (!last) {
+                    wait_mma(&mbar, phase);
                     cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
                     store_operand(c, P_H1_HI, P_H1_LO, h);
                     storeU(Hs, c, t, h);
@@ -708,21 +724,26 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);   // t == T: only finish comb_{T-1}
                 pc.mark(3);
+                if (t >= 1) wait_mma(&mbar2, phase2);   // C = ctx Wcomb_c of step t-1
                 tmem_writes_done();
                 pc.mark(4);
                 // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
+                // Q and C first (barrier 1), Z += h Wh_d after (barrier 2): the
+                // head and the attention run while the N=256 product finishes
                 if (c.tid == 0) {
                     umma::fence_after();
-                    if (!last) {
-                        mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase + tl.b_off[2], 256, true);
+                    if (!last)
                         mma3(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
                              sbase + tl.b_off[3], 64, false);
-                    }
                     if (t >= 1)
                         mma3(c.tbase + COL_C, c.tbase + A_H_HI, c.tbase + A_H_LO,
                              sbase + tl.b_off[4], 64, true);
                     umma::commit(&mbar);
+                    if (!last) {
+                        mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                             sbase + tl.b_off[2], 256, true);
+                        umma::commit(&mbar2);
+                    }
                 }
                 wait_mma(&mbar, phase);
                 pc.mark(5);
@@ -744,16 +765,19 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 float ctx[U];
                 attn_context(c, Hs, t + 1, s_part, L, ctx);
                 store_operand(c, A_X_HI, A_X_LO, ctx);
+                wait_mma(&mbar2, phase2);   // Z += h Wh_d (long done; keeps the phases paired)
                 tmem_writes_done();
                 pc.mark(7);
-                // GEMM2 on ctx_t: Z += ctx Wc ; C = ctx Wcomb_c
+                // GEMM2 on ctx_t: Z += ctx Wc (barrier 1, the cell needs it) ;
+                // C = ctx Wcomb_c (barrier 2, read by the next step's head)
                 if (c.tid == 0) {
                     umma::fence_after();
                     mma3(c.tbase + COL_Z, c.tbase + A_X_HI, c.tbase + A_X_LO,
                          sbase + tl.b_off[5], 256, true);
+                    umma::commit(&mbar);
                     mma3(c.tbase + COL_C, c.tbase + A_X_HI, c.tbase + A_X_LO,
                          sbase + tl.b_off[6], 64, false);
-                    umma::commit(&mbar);
+                    umma::commit(&mbar2);
                 }
                 if (t + 1 < T) dstage.prefetch(c, pid_dec, __ldg(gid + t + 1));
                 wait_mma(&mbar, phase);
