@@ -131,9 +131,12 @@ def generate_trace(cfg: TraceGenConfig) -> Trace:
     (recmg_trace_pool_pass).
     """
     cfg.validate()
-    rng = np.random.default_rng(cfg.rng_seed)
     total = int(sum(cfg.table_sizes))
     n = int(cfg.total_accesses)
+    if n >= (1 << 20) and total < np.iinfo(np.int32).max:
+        # same draws through the multi-threaded streamed path (TraceStream)
+        return Trace(generate_trace_streamed(cfg), cfg.table_sizes)
+    rng = np.random.default_rng(cfg.rng_seed)
     ranks = np.arange(1, total + 1, dtype=np.float64)
     weights = ranks ** (-cfg.zipf_exponent)
     probs = weights / weights.sum()
