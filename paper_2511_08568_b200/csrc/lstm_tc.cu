@@ -147,6 +147,22 @@ __device__ __forceinline__ void load_phase(uint8_t *smem, const uint8_t *blob, i
     __syncthreads();
 }
 
+// the same with one TMA bulk copy stream (thread 0 issues, everyone waits on
+// the byte-counting barrier): no register round trip per 16 B
+__device__ __forceinline__ void load_phase_tma(uint8_t *smem, const uint8_t *blob, int64_t off,
+                                               int64_t len, int tid, uint64_t *bar,
+                                               uint32_t &ph) {
+    umma::fence_proxy_async();   // order this thread's generic smem writes (s_part) before the TMA
+    __syncthreads();             // every reader of the old contents is done
+    if (tid == 0) {
+        umma::mbar_expect_tx(bar, (uint32_t)len);
+        for (int64_t o = 0; o < len; o += 32768)
+            umma::bulk_g2s(smem + o, blob + off + o, (uint32_t)imin64(32768, len - o), bar);
+    }
+    umma::mbar_wait(bar, ph);
+    ph ^= 1u;
+}
+
 // the three split products for one B matrix: d (+)= a * b, K = 64 (4 k-steps)
 __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_saddr,
                                      int N, bool acc) {
@@ -556,6 +572,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     constexpr int NT = C::NT;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar, mbar2;   // caching: mbar2 tracks the MMAs split off
+    __shared__ uint64_t tma_bar;       // prefetch decoder: async weight swaps
     __shared__ uint32_t tmem_base_s;
     __shared__ float lpart[PARTS][128];
     __shared__ int s_tile;
@@ -574,6 +591,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     if (c.tid == 0) {
         umma::mbar_init(&mbar, 1);
         umma::mbar_init(&mbar2, 1);
+        umma::mbar_init(&tma_bar, 1);
     }
     if (c.warp == 0) umma::tmem_alloc<512>(&tmem_base_s);
     umma::fence_before();
@@ -581,7 +599,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     umma::fence_after();
     c.tbase = tmem_base_s;
     c.lane_addr = c.tbase + ((uint32_t)(32 * c.quad) << 16);
-    uint32_t phase = 0, phase2 = 0;
+    uint32_t phase = 0, phase2 = 0, tphase = 0;
     const uint32_t sbase = umma::smem_u32(smem);
     const TcLayout &tl = a.tl;
     const PackedLayout &pl = a.pl;
@@ -609,7 +627,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
 
         // ====================== encoder (model.py:131-145) ======================
         pc.mark(9);
-        load_phase<NT>(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid);
+        load_phase_tma(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid, &tma_bar, tphase);
 #pragma unroll
         for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
         if (caching) {
@@ -713,7 +731,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
 #pragma unroll
         for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
         pc.mark(9);
-        load_phase<NT>(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
+        load_phase_tma(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid, &tma_bar, tphase);
         float lsum;
         if (caching) {
             zero_operand(c, A_H_HI, A_H_LO);
@@ -824,13 +842,17 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     for (int p = 0; p < PARTS; p++) lsum += lpart[p][c.row];
                     emit_logit(a, chunk, T, t - 1, lsum, false);
                 }
-                if (last) break;
+                if (last) {
+                    if (t >= 1) wait_mma(&tma_bar, tphase);   // the last DEC-A swap-back
+                    break;
+                }
                 pc.mark(6);
                 float ctx[U];
                 attn_context(c, Hs, L, s_part, L, ctx);
                 store_operand(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
                 init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
+                if (t >= 1) wait_mma(&tma_bar, tphase);       // Wctx0 | Wh0 back in the swap region
                 tmem_writes_done();
                 pc.mark(7);
                 if (c.tid == 0) {
@@ -842,31 +864,44 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                // Wctx0 | Wh0 are dead until the next step: swap DEC-B (Wx1 | Wh1)
+                // into their region with TMA while the layer-0 cell runs;
+                // att_dec / Wcomb stay resident below it
+                if (c.tid == 0) {
+                    umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.phase_len[2]);
+                    for (int64_t o = 0; o < tl.phase_len[2]; o += 32768)
+                        umma::bulk_g2s(smem + tl.swap_off + o, a.blob + tl.phase_off[2] + o,
+                                       (uint32_t)imin64(32768, tl.phase_len[2] - o), &tma_bar);
+                }
                 pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
                 store_operand(c, P_H0_HI, P_H0_LO, h);
-                umma::tmem_st_wait();
                 // layer 1 (DEC-B weights): Z = h0 Wx1 + h1 Wh1 (+ b1)
                 pc.mark(9);
-                load_phase<NT>(smem, a.blob, tl.phase_off[2], tl.phase_len[2], c.tid);
-                umma::fence_before();
-                __syncthreads();
+                wait_mma(&tma_bar, tphase);
+                tmem_writes_done();
                 if (c.tid == 0) {
                     umma::fence_after();
                     mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                         sbase + tl.b_off[9], 256, false);
+                         sbase + tl.swap_off + tl.b_off[9], 256, false);
                     mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                         sbase + tl.b_off[10], 256, true);
+                         sbase + tl.swap_off + tl.b_off[10], 256, true);
                     umma::commit(&mbar);
                 }
                 pc.mark(10);
                 wait_mma(&mbar, phase);
+                // swap Wctx0 | Wh0 back (needed at the next step's layer 0)
+                if (c.tid == 0) {
+                    const int64_t len = tl.phase_len[1] - tl.swap_off;
+                    umma::mbar_expect_tx(&tma_bar, (uint32_t)len);
+                    for (int64_t o = 0; o < len; o += 32768)
+                        umma::bulk_g2s(smem + tl.swap_off + o,
+                                       a.blob + tl.phase_off[1] + tl.swap_off + o,
+                                       (uint32_t)imin64(32768, len - o), &tma_bar);
+                }
                 pc.mark(11);
                 cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
                 store_operand(c, P_H1_HI, P_H1_LO, h);
-                umma::tmem_st_wait();
-                pc.mark(9);
-                load_phase<NT>(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid);
             }
         }
         __syncthreads();
@@ -1000,6 +1035,8 @@ TcLayout tc_layout(const recmg_model_shape *m) {
         t.b_off[10] = img(256) - t.phase_off[2];
         t.phase_len[2] = o - t.phase_off[2];
         t.nb = 11;
+        t.swap_off = t.b_off[7];   // DEC-B swaps in over Wctx0 | Wh0
+        if (t.phase_len[1] - t.swap_off != t.phase_len[2]) t.swap_off = -1;  // (never)
     }
     o = (o + 255) / 256 * 256;
     const int ntab = m->kind == RECMG_MODEL_CACHING ? 2 : 1;

@@ -90,6 +90,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
         "@!P bra WAIT_%=;\n\t}\n" ::"r"(a), "r"(phase) : "memory");
 }
 
+// TMA bulk copy global -> shared (SASS UBLKCP), completion counted in bytes
+// on an mbarrier: one thread arms the barrier with the total, then issues.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
+}
+
 // one full warp: allocate `cols` TMEM columns, base address written to *dst (smem)
 template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst) {
