@@ -65,6 +65,15 @@ __device__ __forceinline__ void rcp4(float &a, float &b, float &c, float &d) {
     const float ia = rab * b, ib = rab * a, ic = rcd * d, id = rcd * c;
     a = ia; b = ib; c = ic; d = id;
 }
+// rcp4 without the clamps, for denominators known to be in [1, 2^31]
+// (the attention scores: 1 + e^(2e) e^(2q) with |2e|, |2q| <= kExpLim = 11)
+__device__ __forceinline__ void rcp4_bounded(float &a, float &b, float &c, float &d) {
+    const float ab = a * b, cd = c * d;
+    const float r = frcp(ab * cd);
+    const float rab = r * cd, rcd = r * ab;
+    const float ia = rab * b, ib = rab * a, ic = rcd * d, id = rcd * c;
+    a = ia; b = ib; c = ic; d = id;
+}
 // 1 / (1 + e^(-x)) and tanh = 1 - 2 / (1 + e^(2x)) denominators
 __device__ __forceinline__ float sig_den(float x) { return 1.0f + __expf(-x); }
 __device__ __forceinline__ float tanh_den(float x) { return 1.0f + __expf(2.0f * x); }
@@ -74,7 +83,10 @@ __device__ __forceinline__ float tanh_den(float x) { return 1.0f + __expf(2.0f *
 // computes e^(2q) once, and every (position, unit) pair costs one FFMA and a
 // quarter MUFU.RCP instead of ex2 + rcp.  Exponents beyond +-kExpLim fall
 // back to the direct form (raw e kept for that position / q out of range).
-constexpr float kExpLim = 80.0f;
+// kExpLim = 11 bounds each denominator by 1 + e^22 < 2^32, so the product
+// of four stays finite and rcp4 needs no clamps (|e|, |q| < 4.5 at init
+// 0.4 / 0.6; at init 1.0 about 5% of positions take the direct form).
+constexpr float kExpLim = 11.0f;
 
 struct TcArgs {
     recmg_model_shape m;
@@ -402,7 +414,7 @@ __device__ __forceinline__ float score_fast(const float4 (&x)[NQ], const float (
         const float4 v = __ldg(v4 + u);
         float a = fmaf(x[u].x, qx[4 * u + 0], 1.0f), b = fmaf(x[u].y, qx[4 * u + 1], 1.0f);
         float cc = fmaf(x[u].z, qx[4 * u + 2], 1.0f), d = fmaf(x[u].w, qx[4 * u + 3], 1.0f);
-        rcp4(a, b, cc, d);
+        rcp4_bounded(a, b, cc, d);
         s0 = fmaf(v.x, a, s0);
         s1 = fmaf(v.y, b, s1);
         s2 = fmaf(v.z, cc, s2);
