@@ -185,10 +185,15 @@ int recmg_embedding_bag(const recmg_buffer_cfg *cfg, const void *state, const in
 enum { RECMG_MODEL_CACHING = 0, RECMG_MODEL_PREFETCH = 1 };
 enum {
     RECMG_PREC_FP32 = 0, /* SIMT: fp32 weights, fp32 FMA, any dim <= 64            */
-    RECMG_PREC_TC32 = 1  /* tcgen05: every GEMM as the fp16 hi/lo 3-product split
+    RECMG_PREC_TC32 = 1, /* tcgen05: every GEMM as the fp16 hi/lo 3-product split
                             with fp32 accumulation in TMEM (fp32-class logits);
                             dim 64, l_in/l_out <= 16, 1 (caching) / 2 (prefetch)
                             stacks; token projection folded into per-id tables   */
+    RECMG_PREC_TC16 = 2  /* reduced-precision variant of TC32 (the north star's
+                            "bf16 variant, reported separately"): ONE fp16 product
+                            per GEMM (x_hi * w_hi), same packed weights and
+                            kernels; logits ~1e-3..1e-1 off, decisions reported
+                            as agreement rates against TC32                    */
 };
 
 typedef struct {

@@ -36,6 +36,7 @@ OP_ADD, OP_POPULATE, OP_REFERENCE, OP_SET_PRIORITY, OP_QUERY = range(5)
 MODEL_CACHING, MODEL_PREFETCH = 0, 1
 PREC_FP32 = 0
 PREC_TC32 = 1
+PREC_TC16 = 2
 
 # every symbol include/recmg.h declares (tests check the export table)
 EXPORTS = (

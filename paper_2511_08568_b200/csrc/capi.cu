@@ -353,7 +353,7 @@ static size_t dense_bytes_aligned(const recmg_model_shape *shape) {
 size_t recmg_model_packed_bytes(const recmg_model_shape *shape, int32_t precision) {
     if (!shape_ok(shape)) return 0;
     if (precision == RECMG_PREC_FP32) return (size_t)packed_layout(shape).total * sizeof(float);
-    if (precision == RECMG_PREC_TC32 && tc_supported(shape))
+    if ((precision == RECMG_PREC_TC32 || precision == RECMG_PREC_TC16) && tc_supported(shape))
         return dense_bytes_aligned(shape) + (size_t)tc_layout(shape).total;
     return 0;
 }
@@ -376,7 +376,7 @@ int recmg_model_pack_tc(const recmg_model_shape *shape, const float *dense_raw,
 
 size_t recmg_model_workspace_bytes(const recmg_model_shape *shape, int32_t precision,
                                    int64_t batch) {
-    if (precision == RECMG_PREC_TC32 && tc_supported(shape)) return tc_workspace_bytes(shape, batch);
+    if ((precision == RECMG_PREC_TC32 || precision == RECMG_PREC_TC16) && tc_supported(shape)) return tc_workspace_bytes(shape, batch);
     return 0;
 }
 
@@ -389,11 +389,12 @@ int recmg_model_forward_ex(const recmg_model_shape *shape, int32_t precision,
         decode_ids >= (int64_t)kGidMask)
         return RECMG_E_INVALID_CONFIG;
     if (batch > 0 && (!packed || !gid || !tid)) return RECMG_E_INVALID_CONFIG;
-    if (precision == RECMG_PREC_TC32) {
+    if (precision == RECMG_PREC_TC32 || precision == RECMG_PREC_TC16) {
         if (!tc_supported(shape)) return RECMG_E_INVALID_CONFIG;
         return model_forward_tc(shape, packed, (const char *)packed + dense_bytes_aligned(shape),
                                 gid, tid, batch, logits, bits, pf_gid, ws, ws_bytes,
-                                as_stream(stream), nullptr, decode_ids);
+                                as_stream(stream), nullptr, decode_ids,
+                                precision == RECMG_PREC_TC16);
     }
     if (precision != RECMG_PREC_FP32) return RECMG_E_INVALID_CONFIG;
     if (batch > 0 && !embed_id) return RECMG_E_INVALID_CONFIG;

@@ -176,6 +176,8 @@ __device__ __forceinline__ void load_phase_tma(uint8_t *smem, const uint8_t *blo
 }
 
 // the three split products for one B matrix: d (+)= a * b, K = 64 (4 k-steps)
+// SINGLE: the reduced-precision variant (RECMG_PREC_TC16) keeps only xh * wh
+template <bool SINGLE>
 __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_saddr,
                                      int N, bool acc) {
     const uint32_t idesc = umma::idesc_f16(128, N);
@@ -184,6 +186,7 @@ __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, u
     for (int ks = 0; ks < 4; ks++)
         umma::mma_ts(d, a_hi + 8 * ks, umma::make_desc(b_saddr + 256 * ks, 128, 1024), idesc,
                      (acc || ks > 0) ? 1u : 0u);
+    if (SINGLE) return;
 #pragma unroll
     for (int ks = 0; ks < 4; ks++)
         umma::mma_ts(d, a_hi + 8 * ks, umma::make_desc(b_saddr + lo_off + 256 * ks, 128, 1024),
@@ -213,7 +216,7 @@ __device__ __forceinline__ void st_cols(uint32_t taddr, const uint32_t (&r)[N]) 
 }
 
 // this thread's U units as fp16 hi|lo into an A operand region (U/2 columns each)
-template <int PARTS>
+template <bool SINGLE, int PARTS>
 __device__ __forceinline__ void store_operand(const Ctx<PARTS> &c, uint32_t col_hi,
                                               uint32_t col_lo, const float (&v)[Ctx<PARTS>::U]) {
     constexpr int H = Ctx<PARTS>::U / 2;
@@ -226,7 +229,7 @@ __device__ __forceinline__ void store_operand(const Ctx<PARTS> &c, uint32_t col_
         lo[m] = umma::pack_half2(v[2 * m] - hf.x, v[2 * m + 1] - hf.y);
     }
     st_cols<H>(c.lane_addr + col_hi + H * c.part, hi);
-    st_cols<H>(c.lane_addr + col_lo + H * c.part, lo);
+    if (!SINGLE) st_cols<H>(c.lane_addr + col_lo + H * c.part, lo);
 }
 
 template <int PARTS>
@@ -574,8 +577,11 @@ __device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T
 // phases: 0 enc table init+sync, 1 enc MMA wait, 2 enc epilogue, 3 dec init+sync,
 // 4 dec MMA1 wait, 5 dec head+scores+sync, 6 dec softmax/ctx+sync, 7 dec MMA2 wait,
 // 8 dec cell, 9 weight loads, 10 prefetch layer-1 MMA wait, 11 prefetch layer-1 cell
-template <int KIND, bool PROF>
+// MODE bit 0: phase-cycle instrumentation; bit 1: single-product GEMMs (TC16)
+template <int KIND, int MODE>
 __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(TcArgs a) {
+    constexpr bool PROF = (MODE & 1) != 0;
+    constexpr bool SINGLE = (MODE & 2) != 0;
     PhaseClock<PROF> pc;
     pc.start();
     constexpr int PARTS = PartsOf<KIND>::value;
@@ -662,11 +668,11 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 // stored while the long N=256 Z product still runs
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                    mma3<SINGLE>(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
                          sbase + tl.b_off[1], 64, false);                  // Q = h att_enc
                     umma::commit(&mbar);
                     if (!last) {
-                        mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
                              sbase + tl.b_off[0], 256, true);             // Z += h Wh
                         umma::commit(&mbar2);
                     }
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     wait_mma(&mbar2, phase2);
                     cell<false>(c, nullptr, cs0, h);
-                    store_operand(c, A_H_HI, A_H_LO, h);
+                    store_operand<SINGLE>(c, A_H_HI, A_H_LO, h);
                     storeU(Hs, c, t, h);
                     if (t + 1 < L) stage.commit(c);
                 }
@@ -696,12 +702,12 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::fence_after();
                     if (!last) {
                         // layer 0: Z = Pid + Ptab + h0 Wh0
-                        mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
                              sbase + tl.b_off[0], 256, true);
                         umma::commit(&mbar);
                     }
                     if (t >= 1) {
-                        mma3(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                        mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
                              sbase + tl.b_off[3], 64, false);
                         umma::commit(&mbar2);
                     }
@@ -709,14 +715,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     wait_mma(&mbar, phase);
                     cell<false>(c, nullptr, cs0, h);
-                    store_operand(c, P_H0_HI, P_H0_LO, h);
+                    store_operand<SINGLE>(c, P_H0_HI, P_H0_LO, h);
                     tmem_writes_done();
                     // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell)
                     if (c.tid == 0) {
                         umma::fence_after();
-                        mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
                              sbase + tl.b_off[1], 256, false);
-                        mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
                              sbase + tl.b_off[2], 256, true);
                         umma::commit(&mbar);
                     }
@@ -731,7 +737,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     wait_mma(&mbar, phase);
                     cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
-                    store_operand(c, P_H1_HI, P_H1_LO, h);
+                    store_operand<SINGLE>(c, P_H1_HI, P_H1_LO, h);
                     storeU(Hs, c, t, h);
                     if (t + 1 < L) stage.commit(c);
                 }
@@ -763,14 +769,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last)
-                        mma3(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                        mma3<SINGLE>(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
                              sbase + tl.b_off[3], 64, false);
                     if (t >= 1)
-                        mma3(c.tbase + COL_C, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                        mma3<SINGLE>(c.tbase + COL_C, c.tbase + A_H_HI, c.tbase + A_H_LO,
                              sbase + tl.b_off[4], 64, true);
                     umma::commit(&mbar);
                     if (!last) {
-                        mma3(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
                              sbase + tl.b_off[2], 256, true);
                         umma::commit(&mbar2);
                     }
@@ -794,7 +800,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(6);
                 float ctx[U];
                 attn_context(c, Hs, t + 1, s_part, L, ctx);
-                store_operand(c, A_X_HI, A_X_LO, ctx);
+                store_operand<SINGLE>(c, A_X_HI, A_X_LO, ctx);
                 wait_mma(&mbar2, phase2);   // Z += h Wh_d (long done; keeps the phases paired)
                 tmem_writes_done();
                 pc.mark(7);
@@ -802,10 +808,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 // C = ctx Wcomb_c (barrier 2, read by the next step's head)
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3(c.tbase + COL_Z, c.tbase + A_X_HI, c.tbase + A_X_LO,
+                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_X_HI, c.tbase + A_X_LO,
                          sbase + tl.b_off[5], 256, true);
                     umma::commit(&mbar);
-                    mma3(c.tbase + COL_C, c.tbase + A_X_HI, c.tbase + A_X_LO,
+                    mma3<SINGLE>(c.tbase + COL_C, c.tbase + A_X_HI, c.tbase + A_X_LO,
                          sbase + tl.b_off[6], 64, false);
                     umma::commit(&mbar2);
                 }
@@ -813,7 +819,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 wait_mma(&mbar, phase);
                 pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
-                store_operand(c, A_H_HI, A_H_LO, h);
+                store_operand<SINGLE>(c, A_H_HI, A_H_LO, h);
                 if (t + 1 < T) dstage.commit(c);
             }
         } else {
@@ -829,12 +835,12 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last)
-                        mma3(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                        mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
                              sbase + tl.b_off[4], 64, false);
                     if (t >= 1) {
-                        mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
                              sbase + tl.b_off[5], 64, false);
-                        mma3(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
+                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
                              sbase + tl.b_off[6], 64, true);
                     }
                     umma::commit(&mbar);
@@ -861,7 +867,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(6);
                 float ctx[U];
                 attn_context(c, Hs, L, s_part, L, ctx);
-                store_operand(c, P_CTX_HI, P_CTX_LO, ctx);
+                store_operand<SINGLE>(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
                 init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
                 if (t >= 1) wait_mma(&tma_bar, tphase);       // Wctx0 | Wh0 back in the swap region
@@ -869,9 +875,9 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(7);
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
+                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
                          sbase + tl.b_off[7], 256, true);
-                    mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
                          sbase + tl.b_off[8], 256, true);
                     umma::commit(&mbar);
                 }
@@ -887,16 +893,16 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
-                store_operand(c, P_H0_HI, P_H0_LO, h);
+                store_operand<SINGLE>(c, P_H0_HI, P_H0_LO, h);
                 // layer 1 (DEC-B weights): Z = h0 Wx1 + h1 Wh1 (+ b1)
                 pc.mark(9);
                 wait_mma(&tma_bar, tphase);
                 tmem_writes_done();
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
                          sbase + tl.swap_off + tl.b_off[9], 256, false);
-                    mma3(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
                          sbase + tl.swap_off + tl.b_off[10], 256, true);
                     umma::commit(&mbar);
                 }
@@ -913,7 +919,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 pc.mark(11);
                 cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
-                store_operand(c, P_H1_HI, P_H1_LO, h);
+                store_operand<SINGLE>(c, P_H1_HI, P_H1_LO, h);
             }
         }
         __syncthreads();
@@ -1134,7 +1140,7 @@ int set_model_sm_budget(int n) {
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,
-                     long long *prof, int64_t decode_ids) {
+                     long long *prof, int64_t decode_ids, bool single) {
     if (batch <= 0) return RECMG_OK;
     const int64_t n_tiles = (batch + 127) / 128;
     const int grid = (int)imin64(n_tiles, g_model_sm_budget);
@@ -1164,11 +1170,13 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
         lstm_tc_kernel<K, P><<<grid, 128 * PartsOf<K>::value, smem, s>>>(a);                   \
     } while (0)
     if (m->kind == RECMG_MODEL_CACHING) {
-        if (prof) RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, true);
-        else RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, false);
+        if (prof) RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, 1);
+        else if (single) RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, 2);
+        else RECMG_TC_LAUNCH(RECMG_MODEL_CACHING, 0);
     } else {
-        if (prof) RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, true);
-        else RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, false);
+        if (prof) RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, 1);
+        else if (single) RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, 2);
+        else RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, 0);
     }
 #undef RECMG_TC_LAUNCH
     RECMG_LAUNCH_CHECK();

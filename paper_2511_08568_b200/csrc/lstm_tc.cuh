@@ -21,7 +21,8 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,
-                     long long *prof = nullptr, int64_t decode_ids = 0);
+                     long long *prof = nullptr, int64_t decode_ids = 0,
+                     bool single = false);
 size_t tc_workspace_bytes(const recmg_model_shape *m, int64_t batch);
 int set_model_sm_budget(int n);
 

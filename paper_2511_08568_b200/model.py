@@ -123,6 +123,8 @@ class DeviceModel:
     accumulation (recmg_model_pack_tc / RECMG_PREC_TC32; csrc/lstm_tc.cu);
     the layer-0 token projection is folded into per-id tables, so the
     packed weights hold total_ids x 4d fp32 per projection.
+    precision "tc16": the reduced-precision variant of tc32 (one fp16 product
+    per GEMM, RECMG_PREC_TC16), same packed weights; not parity-grade.
     precision "fp32": the SIMT kernel (csrc/lstm_simt.cu), any dim <= 64.
     """
 
@@ -146,12 +148,14 @@ class DeviceModel:
         tc_bytes = L.recmg_model_packed_bytes(ctypes.byref(self.shape), _native.PREC_TC32)
         if precision == "auto":
             precision = "tc32" if tc_bytes else "fp32"
-        if precision == "tc32" and not tc_bytes:
-            raise InvalidConfigError("tc32 needs dim 64, l_in/l_out <= 16 and the default stacks")
-        if precision not in ("tc32", "fp32"):
+        if precision in ("tc32", "tc16") and not tc_bytes:
+            raise InvalidConfigError(f"{precision} needs dim 64, l_in/l_out <= 16 and the "
+                                     "default stacks")
+        if precision not in ("tc32", "tc16", "fp32"):
             raise InvalidConfigError(f"unknown precision {precision!r}")
         self.precision = precision
-        self.prec = _native.PREC_TC32 if precision == "tc32" else _native.PREC_FP32
+        self.prec = {"tc32": _native.PREC_TC32, "tc16": _native.PREC_TC16,
+                     "fp32": _native.PREC_FP32}[precision]
         names = [n for n in _shapes(params.kind, params.total_ids, len(params.table_sizes),
                                     params.dim, params.stacks, params.l_out) if n != "embed_id"]
         raw = np.concatenate([np.asarray(params.arrays[n], dtype=np.float32).reshape(-1)
@@ -166,7 +170,7 @@ class DeviceModel:
         self.packed = _native.device_bytes(
             torch, L.recmg_model_packed_bytes(ctypes.byref(self.shape), self.prec))
         st = _native.stream_handle(torch)
-        if self.prec == _native.PREC_TC32:
+        if self.prec in (_native.PREC_TC32, _native.PREC_TC16):
             _native.check(L.recmg_model_pack_tc(ctypes.byref(self.shape), _native.ptr(raw_d),
                                                 _native.ptr(embed_id), _native.ptr(self.offsets),
                                                 _native.ptr(self.packed), st), "model_pack_tc")
@@ -178,6 +182,18 @@ class DeviceModel:
             self.embed_id = embed_id
         torch.cuda.current_stream().synchronize()
         self._ws = None
+
+    def variant(self, precision: str) -> "DeviceModel":
+        """The same resident weights run at another tensor-core precision
+        ("tc32" <-> "tc16": both use the TC32 packing); own workspace."""
+        import copy
+        if {precision, self.precision} - {"tc32", "tc16"}:
+            raise InvalidConfigError("variants exist between tc32 and tc16 only")
+        v = copy.copy(self)
+        v.precision = precision
+        v.prec = _native.PREC_TC32 if precision == "tc32" else _native.PREC_TC16
+        v._ws = None
+        return v
 
     @property
     def out_len(self):

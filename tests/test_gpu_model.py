@@ -174,3 +174,21 @@ def test_hotpath_pipelined_equals_single_replay():
     ref = rb.replay(t, rb.BufferConfig(C32, 4, 32), cp, pp)
     assert ref == rep and ref.evictions == rep.evictions
     assert m == rb.simulate(t, rb.CacheConfig(C32, rb.Policy.LRU, 32), per_access=False).misses
+
+
+def test_tc16_variant_bounded_and_reported():
+    """RECMG_PREC_TC16 (one fp16 product per GEMM, the reduced-precision
+    variant reported separately): bounded logit error, caching bits agree
+    with the float64 reference on >= 99.5% of accesses at init 0.4."""
+    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 1000 * 15 + 30, 1.05, 0.4, 32, 0))
+    K = rb.num_chunks(len(t))
+    gid = t.gid_array[:K * 15].reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    p = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
+    ref = mo.caching_logits(p.arrays, 64, 1, gid, tid)
+    got = rb.forward_caching_batch(p, gid, tid, precision="tc16").logits
+    tc32 = rb.forward_caching_batch(p, gid, tid, precision="tc32").logits
+    e16 = (np.abs(got - ref) / np.maximum(np.abs(ref), FLOOR)).max()
+    e32 = (np.abs(tc32 - ref) / np.maximum(np.abs(ref), FLOOR)).max()
+    assert e32 <= RTOL < e16 < 1.0, (e32, e16)
+    assert ((got >= 0) == (ref >= 0)).mean() >= 0.995
