@@ -26,7 +26,7 @@ from .trace import num_chunks
 
 
 class HotPath:
-    STAGES = ("table_ids", "caching_fwd", "prefetch_fwd", "replay", "lru")
+    STAGES = ("table_ids", "caching_fwd", "prefetch_fwd", "replay", "lru", "tail")
 
     def __init__(self, caching: ModelParameters | DeviceModel | None,
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
@@ -179,9 +179,11 @@ class HotPath:
                     self._ev("replay", self.s_replay)
         finally:
             L.recmg_set_model_sm_budget(prev)
+        self._ev("tail", main)          # forwards done ...
         main.wait_stream(self.s_replay)
         if self.lru is not None:
             main.wait_stream(self.s_lru)
+        self._ev("tail", main)          # ... -> last replay piece and LRU done
         self.K = K
         self.n = n
 
