@@ -73,7 +73,7 @@ def parse():
     ap.add_argument("--row-dim", type=int, default=128)
     ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
     ap.add_argument("--pieces", type=int, default=8, help="replay pipeline pieces")
-    ap.add_argument("--model-sms", type=int, default=146, help="SMs the forwards may use")
+    ap.add_argument("--model-sms", type=int, default=136, help="SMs the forwards may use")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3])
     ap.add_argument("--shards", type=int, default=0, help="config 3: table shards (0 = world)")
     ap.add_argument("--shard-index", type=int, default=0,
@@ -85,7 +85,7 @@ def parse():
         for k, v in c3.items():
             if getattr(args, k) == d[k]:
                 setattr(args, k, v)
-        if args.model_sms == 146:
+        if args.model_sms == 136:
             # the shard's hottest set makes the replay the long pole: leave it
             # more SMs beside the forwards (measured: 146 -> 124 SMs, +17%)
             args.model_sms = 124

@@ -79,7 +79,8 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
     StateView st = state_view(state, cfg, p.g);
     build_events_kernel<<<(unsigned)imin64((p.E + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
-        gids, n, l_in, bits, pf, pf_stride, p.K, p.k0, p.nk, p.tail ? 1 : 0, p.ev, p.vv);
+        gids, n, l_in, bits, pf, pf_stride, p.K, p.k0, p.nk, p.tail ? 1 : 0, (uint32_t)p.g.S,
+        p.ev, p.vv, counters, access_class);
     RECMG_LAUNCH_CHECK();
     uint32_t *ev = p.ev, *vv = p.vv;
     ReplayArgs ra;
@@ -263,6 +264,38 @@ __global__ void iota_copy_kernel(const int32_t *in, uint32_t *keys, uint32_t *va
     }
 }
 
+// LRU serve stream with collapsed repeats: an access whose previous same-set
+// access (within the last kLookback accesses) names the same id is an LRU hit
+// that leaves its way most recent -- no way of the set can pass it in
+// between -- so it is counted as a hit here and emitted as an empty event
+// (cache_sim.py:92-106; the same argument as build_events_kernel's).
+constexpr int kLookback = 8;
+__global__ void lru_events_kernel(const int32_t *in, uint32_t *keys, uint32_t *vals, int64_t n,
+                                  uint32_t S, uint8_t *per_access_hit, int64_t *hits_misses) {
+    unsigned collapsed = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = (uint32_t)in[i];
+        int64_t q = i - 1;
+        const int64_t lo = i - kLookback > 0 ? i - kLookback : 0;
+        while (q >= lo && (uint32_t)in[q] != g) q--;
+        bool dup = q >= lo;
+        if (dup) {
+            const uint32_t set = g % S;
+            for (int64_t p = q + 1; p < i && dup; p++) dup = (uint32_t)in[p] % S != set;
+        }
+        keys[i] = dup ? kGidMask : g;   // EV_SERVE == 0: the gid is the event word
+        if (vals) vals[i] = (uint32_t)i;
+        if (dup) {
+            collapsed++;
+            if (per_access_hit) per_access_hit[i] = 1;
+        }
+    }
+    collapsed = __reduce_add_sync(0xFFFFFFFFu, collapsed);
+    if ((threadIdx.x & 31) == 0 && collapsed)
+        atomicAdd((unsigned long long *)&hits_misses[0], (unsigned long long)collapsed);
+}
+
 int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                       uint8_t *per_access_hit, uint8_t *keep_decisions, int64_t *hits_misses,
                       void *ws, size_t ws_bytes, void *stream) {
@@ -288,7 +321,11 @@ int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *g
         next_use_kernel<<<grid, 256, 0, s>>>(ki, vi, n, p.next_use);
         RECMG_LAUNCH_CHECK();
     }
-    iota_copy_kernel<<<grid, 256, 0, s>>>(gids, p.keys, p.vals, n);
+    if (cfg->policy == RECMG_POLICY_LRU && hits_misses)
+        lru_events_kernel<<<grid, 256, 0, s>>>(gids, p.keys, p.vals, n, (uint32_t)g.S, hit,
+                                               hits_misses);
+    else
+        iota_copy_kernel<<<grid, 256, 0, s>>>(gids, p.keys, p.vals, n);
     RECMG_LAUNCH_CHECK();
     ReplayArgs ra;
     memset(&ra, 0, sizeof(ra));

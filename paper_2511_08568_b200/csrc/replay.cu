@@ -24,16 +24,42 @@ namespace recmg {
 
 // ---------------------------------------------------------------------------
 // event builder: one thread per event slot
+//
+// Collapsed serves: a serve S(g) whose previous same-set access in its chunk
+// (or in the tail) is also g is a guaranteed hit on an untagged entry -- no
+// event of its set lies between the two, so nothing can have evicted g, and
+// the first one cleared any prefetch tag (runtime.py:93-98, 254-258).  Its
+// only effect is cache_hits += 1 (and, for the LRU+prefetch policy, an LRU
+// position that no other way of the set can pass in between), so it is
+// counted here and emitted as an empty event.  Under Zipf skew with a sticky
+// pool this removes most of the hottest set's events.
 __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n, int32_t l_in,
                                     const uint8_t *__restrict__ bits,
                                     const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
-                                    int64_t k0, int64_t nk, int with_tail,
-                                    uint32_t *__restrict__ ev, uint32_t *__restrict__ vals) {
+                                    int64_t k0, int64_t nk, int with_tail, uint32_t S,
+                                    uint32_t *__restrict__ ev, uint32_t *__restrict__ vals,
+                                    recmg_counters *__restrict__ ctr,
+                                    uint8_t *__restrict__ access_class) {
     // events of chunks [k0, k0+nk) (+ the tail when with_tail, i.e. k0+nk == K);
     // local event i has global position k0*Ec + i
     const int64_t Ec = 2 * (int64_t)l_in + pf_stride;
     const int64_t chunk_ev = nk * Ec;
     const int64_t E = chunk_ev + (with_tail ? (n - K * l_in) : 0);
+    unsigned collapsed = 0;
+    // serve of access a: collapsed iff its previous same-set access in
+    // [block_start, a) exists and names the same id
+    // (the latest earlier access of the same id first; sets -- one modulo
+    // each -- only for the accesses between it and this one)
+    auto dup_serve = [&](int64_t block_start, int64_t acc) {
+        const uint32_t g = (uint32_t)gids[acc];
+        int64_t q = acc - 1;
+        while (q >= block_start && (uint32_t)gids[q] != g) q--;
+        if (q < block_start) return false;
+        const uint32_t set = g % S;
+        for (int64_t p = q + 1; p < acc; p++)
+            if ((uint32_t)gids[p] % S == set) return false;
+        return true;
+    };
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
          i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t e;
@@ -41,7 +67,14 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
             int64_t kk = i / Ec, r = i - kk * Ec;
             const int64_t k = k0 + kk;
             if (r < l_in) {
-                e = ev_make(EV_SERVE, (uint32_t)gids[k * l_in + r]);
+                const int64_t acc = k * l_in + r;
+                if (dup_serve(k * l_in, acc)) {
+                    e = ev_make(EV_SERVE, kGidMask);
+                    collapsed++;
+                    if (access_class) access_class[acc] = 0;
+                } else {
+                    e = ev_make(EV_SERVE, (uint32_t)gids[acc]);
+                }
             } else if (r < 2 * l_in) {
                 // keep-bit update; inside one chunk's update block nothing changes
                 // residency, so only the LAST update of an id can matter
@@ -62,11 +95,21 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
                 e = ev_make(EV_PREFETCH, pad ? kGidMask : (uint32_t)row[j]);
             }
         } else {
-            e = ev_make(EV_SERVE, (uint32_t)gids[K * l_in + (i - chunk_ev)]);
+            const int64_t acc = K * l_in + (i - chunk_ev);
+            if (dup_serve(K * l_in, acc)) {
+                e = ev_make(EV_SERVE, kGidMask);
+                collapsed++;
+                if (access_class) access_class[acc] = 0;
+            } else {
+                e = ev_make(EV_SERVE, (uint32_t)gids[acc]);
+            }
         }
         ev[i] = e;
         if (vals) vals[i] = (uint32_t)(k0 * Ec + i);
     }
+    collapsed = __reduce_add_sync(0xFFFFFFFFu, collapsed);
+    if ((threadIdx.x & 31) == 0 && collapsed)
+        atomicAdd((unsigned long long *)&ctr->cache_hits, (unsigned long long)collapsed);
 }
 
 // event position -> access index (only meaningful for serve events)

@@ -10,8 +10,10 @@ struct ReplayArgs;
 __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n, int32_t l_in,
                                     const uint8_t *__restrict__ bits,
                                     const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
-                                    int64_t k0, int64_t nk, int with_tail,
-                                    uint32_t *__restrict__ ev, uint32_t *__restrict__ vals);
+                                    int64_t k0, int64_t nk, int with_tail, uint32_t S,
+                                    uint32_t *__restrict__ ev, uint32_t *__restrict__ vals,
+                                    recmg_counters *__restrict__ ctr,
+                                    uint8_t *__restrict__ access_class);
 __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t k0, int64_t nk,
                                       int32_t l_in, int32_t l_win, const int32_t *__restrict__ pf,
                                       int32_t pf_stride, uint8_t *__restrict__ cov_num,

@@ -32,8 +32,8 @@ class HotPath:
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
                  n_max: int, ways: int | None = 32, eviction_speed: int = 4,
                  lru_capacity: int | None = None, lru_ways: int | None = 32, l_in: int = 15,
-                 l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 146,
-                 shard=None):
+                 l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 136,
+                 shard=None, replay_priority: bool = True):
         """pieces > 1 pipelines the replay: chunks are scored in `pieces`
         ranges on the main stream while earlier ranges replay on a side stream
         (recmg_replay_chunks continues the buffer state, so the result is the
@@ -86,8 +86,12 @@ class HotPath:
             self.lru = LruSim(lru_capacity, self.total_ids, lru_ways, self.n_max)
         self.pieces = max(1, int(pieces))
         self.model_sms = int(model_sms) if self.pieces > 1 else 148
-        self.s_replay = torch.cuda.Stream()
-        self.s_lru = torch.cuda.Stream()
+        # the replay and the LRU run under the forwards on the SMs they leave;
+        # high priority makes the block scheduler hand freed SMs to them first
+        # (at every forward launch boundary), so the replay does not lag
+        prio = torch.cuda.Stream.priority_range()[1] if replay_priority else 0
+        self.s_replay = torch.cuda.Stream(priority=prio)
+        self.s_lru = torch.cuda.Stream(priority=prio)
         self.events = None
         self.stage_ms = {}
 
