@@ -290,7 +290,7 @@ def build_state_config3(args, idx, torch, device=True):
     keep shard `idx`'s order-preserving sub-trace, draw its local models."""
     import paper_2511_08568_b200 as rb
     from paper_2511_08568_b200 import shard as shd
-    from paper_2511_08568_b200.trace import Trace, TraceStream, table_offsets
+    from paper_2511_08568_b200.trace import Trace, TraceStream
     t0 = time.time()
     sizes = [args.rows] * args.tables
     ts = TraceStream(rb.TraceGenConfig(sizes, args.accesses, 1.05, 0.4, 32, 3))

@@ -4,7 +4,6 @@ back identically, with the reference's errors; the shard readers return the
 same arrays as the whole-file readers restricted to the shard."""
 import json
 import os
-import shutil
 import zipfile
 
 import numpy as np

@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 import paper_2511_08568_b200 as rb
 from paper_2511_08568_b200 import shard
-from paper_2511_08568_b200.trace import TraceStream, generate_trace_streamed
+from paper_2511_08568_b200.trace import generate_trace_streamed
 
 SIZES = [900] * 10 + [300] * 6
 
