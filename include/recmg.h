@@ -134,6 +134,10 @@ int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t 
 
 /* Host: sequential float64 mean of num/den in chunk order (runtime.py:276,282). */
 double recmg_coverage_mean(const uint8_t *host_num, const uint8_t *host_den, int64_t K);
+/* Host: acc + the same left-to-right float64 sum over `count` chunks, for
+ * summing the coverage piece by piece in chunk order as pieces complete.    */
+double recmg_coverage_accumulate(const uint8_t *host_num, const uint8_t *host_den, int64_t count,
+                                 double acc);
 
 /* ---- policy-only simulation  (cache_sim.py:223-260, LRU) --------------- */
 int recmg_simulate_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, size_t *bytes);

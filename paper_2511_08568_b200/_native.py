@@ -50,6 +50,7 @@ EXPORTS = (
     "recmg_model_forward_profile", "recmg_rows_refresh", "recmg_embedding_bag",
     "recmg_simulate_ex", "recmg_model_forward_ex", "recmg_pcg64_uniforms", "recmg_trace_guide",
     "recmg_trace_generate_block", "recmg_shard_local_ids", "recmg_trace_parse_text",
+    "recmg_coverage_accumulate",
 )
 
 
@@ -94,6 +95,7 @@ def lib():
         "recmg_replay": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, vp, vp, i32, vp, vp,
                                         vp, vp, vp, sz, vp]),
         "recmg_coverage_mean": (ctypes.c_double, [vp, vp, i64]),
+        "recmg_coverage_accumulate": (ctypes.c_double, [vp, vp, i64, ctypes.c_double]),
         "recmg_replay_chunks": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64, i32,
                                                vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
         "recmg_set_model_sm_budget": (ctypes.c_int, [ctypes.c_int]),

@@ -214,6 +214,12 @@ double recmg_coverage_mean(const uint8_t *num, const uint8_t *den, int64_t K) {
     return K ? acc / (double)K : 0.0;
 }
 
+double recmg_coverage_accumulate(const uint8_t *num, const uint8_t *den, int64_t count,
+                                 double acc) {
+    for (int64_t k = 0; k < count; k++) acc += (double)num[k] / (double)den[k];
+    return acc;
+}
+
 static bool sim_policy_ok(const recmg_buffer_cfg *cfg, const Geometry &g) {
     switch (cfg->policy) {
         case RECMG_POLICY_LRU: return true;

@@ -89,10 +89,12 @@ class BufferReplay:
         c = self._cov[:, :self.K].cpu().numpy()
         return c[0], c[1]
 
-    def result(self):
+    def result(self, with_coverage=True):
         """Synchronise; counters dict plus the float64 coverage of the last run."""
         ctr = self.counters.cpu().numpy()
         out = dict(zip(_native.COUNTER_FIELDS, (int(x) for x in ctr)))
+        if not with_coverage:
+            return out
         if self.K:
             num, den = self.cov_host()
             out["coverage"] = _native.coverage_mean(num, den)

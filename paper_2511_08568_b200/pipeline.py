@@ -91,6 +91,9 @@ class HotPath:
         # (at every forward launch boundary), so the replay does not lag
         prio = torch.cuda.Stream.priority_range()[1] if replay_priority else 0
         self.s_replay = torch.cuda.Stream(priority=prio)
+        self.s_copy = torch.cuda.Stream()
+        self.cov_host = torch.empty((2, max(self.K_max, 1)), dtype=torch.uint8, pin_memory=True)
+        self._cov_events = []
         self.s_lru = torch.cuda.Stream(priority=prio)
         self.events = None
         self.stage_ms = {}
@@ -120,18 +123,58 @@ class HotPath:
         b = list(range(0, K, step)) + [K]
         return [(b[i], b[i + 1]) for i in range(len(b) - 1)]
 
-    def launch(self, n: int):
-        """Stream-ordered launches over self.gids[:n] (device-resident)."""
+    def _ids_of(self, g, k0, k1):
+        """(ids the forwards read, table ids) of chunks [k0, k1): recmg_table_ids,
+        or for a table shard recmg_shard_local_ids (global -> local rows)."""
+        torch = self.torch
+        L = _native.lib()
+        m = (k1 - k0) * self.l_in
+        gk = g[k0 * self.l_in:k1 * self.l_in].view(k1 - k0, self.l_in)
+        tk = self.tid[k0 * self.l_in:k1 * self.l_in].view(k1 - k0, self.l_in)
+        if self.shard is None:
+            _native.check(L.recmg_table_ids(
+                _native.ptr(gk), m, _native.ptr(self.offsets), len(self.table_sizes),
+                _native.ptr(tk), _native.stream_handle(torch)))
+            return gk, tk
+        lk = self.lgid[k0 * self.l_in:k1 * self.l_in].view(k1 - k0, self.l_in)
+        _native.check(L.recmg_shard_local_ids(
+            _native.ptr(gk), m, _native.ptr(self.offsets), len(self.table_sizes),
+            _native.ptr(self.table_local), _native.ptr(self.local_offsets), _native.ptr(lk),
+            _native.ptr(tk), _native.stream_handle(torch)))
+        return lk, tk
+
+    def launch(self, n: int, host_src=None):
+        """Stream-ordered launches over self.gids[:n].
+
+        host_src (pinned host int32 ids, the end-to-end path): the ids are
+        copied in two parts on a copy stream -- the first piece's chunks, then
+        the rest -- so the first forwards start after a fraction of the H2D
+        copy; every piece's per-chunk coverage counts are copied back as soon
+        as its replay is done, so report() sums them while later pieces run."""
         torch = self.torch
         L = _native.lib()
         K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
         g = self.gids[:n]
         main = torch.cuda.current_stream()
-        ready = torch.cuda.Event()
-        ready.record(main)
+        pieces = self._piece_bounds(K) if K else [(0, 0)]
+        all_ids = torch.cuda.Event()
+        if host_src is not None:
+            first = min(n, pieces[0][1] * self.l_in) if K else n
+            self.s_copy.wait_stream(main)       # earlier readers of self.gids
+            first_ids = torch.cuda.Event()
+            with torch.cuda.stream(self.s_copy):
+                self.gids[:first].copy_(host_src[:first], non_blocking=True)
+                first_ids.record(self.s_copy)
+                if n > first:
+                    self.gids[first:n].copy_(host_src[first:n], non_blocking=True)
+                all_ids.record(self.s_copy)
+            main.wait_event(first_ids)
+        else:
+            all_ids.record(main)
+        self._cov_events = []
         # K4: the LRU comparator depends only on the ids
         if self.lru is not None:
-            self.s_lru.wait_event(ready)
+            self.s_lru.wait_event(all_ids)
             with torch.cuda.stream(self.s_lru):
                 self._ev("lru", self.s_lru)
                 self.lru.reset()
@@ -139,31 +182,30 @@ class HotPath:
                 self._ev("lru", self.s_lru)
         prev = L.recmg_set_model_sm_budget(self.model_sms)
         try:
-            self._ev("table_ids", main)
-            if K and (self.caching is not None or self.prefetch is not None):
-                gk = g[:K * self.l_in].view(K, self.l_in)
-                tk = self.tid[:K * self.l_in].view(K, self.l_in)
-                if self.shard is None:
-                    _native.check(L.recmg_table_ids(
-                        _native.ptr(gk), K * self.l_in, _native.ptr(self.offsets),
-                        len(self.table_sizes), _native.ptr(tk), _native.stream_handle(torch)))
-                else:
-                    lk = self.lgid[:K * self.l_in].view(K, self.l_in)
-                    _native.check(L.recmg_shard_local_ids(
-                        _native.ptr(gk), K * self.l_in, _native.ptr(self.offsets),
-                        len(self.table_sizes), _native.ptr(self.table_local),
-                        _native.ptr(self.local_offsets), _native.ptr(lk), _native.ptr(tk),
-                        _native.stream_handle(torch)))
-                    gk = lk   # the forwards read shard-local ids
-            self._ev("table_ids", main)
-            self.s_replay.wait_event(ready)
+            self.s_replay.wait_event(all_ids)
             with torch.cuda.stream(self.s_replay):
                 self.buffer.reset()
             bits = self.bits[:K] if (K and self.caching is not None) else None
             pf = self.pf[:K] if (K and self.prefetch is not None) else None
-            pieces = self._piece_bounds(K) if K else [(0, 0)]
+            models = K > 0 and (self.caching is not None or self.prefetch is not None)
+            # table ids in (at most) two launches: the first piece's as soon as
+            # its ids are in, the rest once all ids are
+            split = pieces[0][1] if host_src is not None else K
+            if models:
+                self._ev("table_ids", main)
+                gk, tk = self._ids_of(g, 0, split)
+                self._ev("table_ids", main)
             for i, (k0, k1) in enumerate(pieces):
-                if k1 > k0:
+                if i == 1 and host_src is not None:
+                    main.wait_event(all_ids)
+                    if models:
+                        self._ev("table_ids", main)
+                        self._ids_of(g, split, K)
+                        self._ev("table_ids", main)
+                if k1 > k0 and models:
+                    gk = (self.lgid if self.shard is not None else self.gids)[
+                        :K * self.l_in].view(K, self.l_in)
+                    tk = self.tid[:K * self.l_in].view(K, self.l_in)
                     if self.caching is not None:
                         self._ev("caching_fwd", main)
                         self.caching.forward(gk[k0:k1], tk[k0:k1], logits=self.clog[k0:k1],
@@ -181,6 +223,13 @@ class HotPath:
                     self._ev("replay", self.s_replay)
                     self.buffer.run_chunks(g, k0, k1, i == len(pieces) - 1, bits, pf)
                     self._ev("replay", self.s_replay)
+                    if host_src is not None and k1 > k0:
+                        for r in range(2):   # contiguous rows: plain async D2H copies
+                            self.cov_host[r, k0:k1].copy_(self.buffer._cov[r, k0:k1],
+                                                          non_blocking=True)
+                        e = torch.cuda.Event()
+                        e.record(self.s_replay)
+                        self._cov_events.append((k0, k1, e))
         finally:
             L.recmg_set_model_sm_budget(prev)
         self._ev("tail", main)          # forwards done ...
@@ -192,9 +241,23 @@ class HotPath:
         self.n = n
 
     def report(self):
-        """Synchronise and return (BreakdownReport, lru (hits, misses) or None)."""
+        """Synchronise and return (BreakdownReport, lru (hits, misses) or None).
+        After launch(host_src=...) the float64 coverage is accumulated piece by
+        piece, in chunk order (runtime.py:276, 282), as the counts arrive."""
         from .runtime import BreakdownReport
-        r = self.buffer.result()
+        cov = None
+        if getattr(self, "_cov_events", None):
+            L = _native.lib()
+            acc = 0.0
+            base = self.cov_host.data_ptr()
+            stride = self.cov_host.stride(0)
+            for k0, k1, e in self._cov_events:
+                e.synchronize()
+                acc = L.recmg_coverage_accumulate(base + k0, base + stride + k0, k1 - k0, acc)
+            cov = acc / self.K if self.K else 0.0
+        r = self.buffer.result(with_coverage=cov is None)
+        if cov is not None:
+            r["coverage"] = cov
         rep = BreakdownReport(r["cache_hits"], r["prefetch_hits"], r["on_demand"],
                               r["prefetch_issued"], r["prefetch_useful"], r["coverage"],
                               r["evictions"], r["prefetch_inserts"])
@@ -208,8 +271,7 @@ class HotPath:
             raise ValueError("trace longer than the HotPath was sized for")
         src = host_gids if hasattr(host_gids, "numel") else self.torch.from_numpy(
             np.ascontiguousarray(host_gids, dtype=np.int32))
-        self.gids[:n].copy_(src, non_blocking=True)
-        self.launch(n)
+        self.launch(n, host_src=src)
         return self.report()
 
     def d2h_bytes(self):
