@@ -185,3 +185,21 @@ def test_no_cpu_fallback_without_gpu():
     t = rb.trace_from_gids(list(range(60)), [64])
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         rb.replay(t, rb.BufferConfig(8))
+
+
+@pytest.mark.parametrize("cfg", [
+    ([7] * 3, 3000, 1.2, 1.0, 4, 2),            # always sticky once the pool has an id
+    ([100_000] * 3, 40_000, 1.05, 0.4, 32, 9),  # V > 4096: the 2^24-bucket guide table
+    ([1], 100, 0.5, 0.5, 3, 1),                 # a single id
+    ([3, 9000, 1], 25_000, 0.0, 0.7, 64, 4),    # uniform popularity, a wide pool
+])
+def test_streamed_generator_equals_numpy_path(cfg):
+    """The streamed generator (TraceStream) and the numpy restatement of
+    generate_trace agree on edge-case configurations, block size 1 included."""
+    from paper_2511_08568_b200.trace import generate_trace_streamed
+    c = rb.TraceGenConfig(*cfg)
+    want = rb.generate_trace(c).gid_array
+    for block in (1, 4097, 1 << 20):
+        if block == 1 and len(want) > 5000:
+            continue
+        assert np.array_equal(generate_trace_streamed(c, block), want), block
