@@ -185,6 +185,33 @@ int recmg_embedding_bag(const recmg_buffer_cfg *cfg, const void *state, const in
                         const float *host_rows, int32_t dim, float *out, int64_t *src_counts,
                         void *stream);
 
+/* ---- K7 fused: pooled all-to-all over NVLink peer memory (DLRM mode) --- */
+/* EmbeddingBag(sum) of n_bags = batch x Tg bags (bag b*Tg + j = sample b,
+ * local table j) whose epilogue stores each pooled row directly into the
+ * receiving rank's output: sample b goes to rank b / (batch/world), row
+ * [b % (batch/world)][table_global[j]] of that rank's [batch/world, n_tables,
+ * dim] buffer (peer_out[rank'] = its CUDA-IPC-mapped pointer).  The last
+ * block then publishes `epoch` (> every earlier epoch) into slot [rank] of
+ * every receiver's flag array (peer_flags[rank']) at system scope, and the
+ * stream waits until all `world` slots of this rank's `flags` reach `epoch`:
+ * after the call (stream order) this rank's output holds every table's
+ * pooled row for its samples.  flags: world uint64 + one uint32 counter,
+ * zero-initialised (recmg_peer_alloc).  Replaces pooling + all_to_all_single. */
+int recmg_embedding_bag_a2a(const recmg_buffer_cfg *cfg, const void *state, const int32_t *gids,
+                            const int64_t *bag_offsets, int64_t n_bags, const float *buf_rows,
+                            const float *host_rows, int32_t dim, int32_t batch, int32_t world,
+                            int32_t rank, int32_t n_tables, const int32_t *table_global,
+                            float *const *peer_out, unsigned long long *const *peer_flags,
+                            unsigned long long *flags, uint64_t epoch, int64_t *src_counts,
+                            void *stream);
+/* Peer memory for the exchange: a dedicated zeroed cudaMalloc, its CUDA IPC
+ * handle (64 bytes, host), and its mapping in another rank's process.       */
+int recmg_peer_alloc(size_t bytes, void **dev_ptr);
+int recmg_peer_free(void *dev_ptr);
+int recmg_peer_handle(void *dev_ptr, uint8_t *host_handle64);
+int recmg_peer_open(const uint8_t *host_handle64, void **dev_ptr);
+int recmg_peer_close(void *dev_ptr);
+
 /* ---- models  (neural/model.py) ----------------------------------------- */
 enum { RECMG_MODEL_CACHING = 0, RECMG_MODEL_PREFETCH = 1 };
 enum {

@@ -50,7 +50,8 @@ EXPORTS = (
     "recmg_model_forward_profile", "recmg_rows_refresh", "recmg_embedding_bag",
     "recmg_simulate_ex", "recmg_model_forward_ex", "recmg_pcg64_uniforms", "recmg_trace_guide",
     "recmg_trace_generate_block", "recmg_shard_local_ids", "recmg_trace_parse_text",
-    "recmg_coverage_accumulate",
+    "recmg_coverage_accumulate", "recmg_embedding_bag_a2a", "recmg_peer_alloc",
+    "recmg_peer_free", "recmg_peer_handle", "recmg_peer_open", "recmg_peer_close",
 )
 
 
@@ -96,6 +97,14 @@ def lib():
                                         vp, vp, vp, sz, vp]),
         "recmg_coverage_mean": (ctypes.c_double, [vp, vp, i64]),
         "recmg_coverage_accumulate": (ctypes.c_double, [vp, vp, i64, ctypes.c_double]),
+        "recmg_embedding_bag_a2a": (ctypes.c_int, [cfgp, vp, vp, vp, i64, vp, vp, i32, i32, i32,
+                                                   i32, i32, vp, vp, vp, vp, ctypes.c_uint64,
+                                                   vp, vp]),
+        "recmg_peer_alloc": (ctypes.c_int, [sz, ctypes.POINTER(ctypes.c_void_p)]),
+        "recmg_peer_free": (ctypes.c_int, [vp]),
+        "recmg_peer_handle": (ctypes.c_int, [vp, ctypes.c_char_p]),
+        "recmg_peer_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+        "recmg_peer_close": (ctypes.c_int, [vp]),
         "recmg_replay_chunks": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64, i32,
                                                vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
         "recmg_set_model_sm_budget": (ctypes.c_int, [ctypes.c_int]),

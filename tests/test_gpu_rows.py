@@ -83,3 +83,54 @@ def test_dlrm_stage_single_rank_nccl():
         assert torch.equal(got, want.reshape(B, 6, D))
     finally:
         dist.destroy_process_group()
+
+
+def _a2a_worker(rank, world, port, out):
+    import os
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+    from paper_2511_08568_b200 import dlrm, shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    try:
+        t = rb.generate_trace(rb.TraceGenConfig([1500] * 7, 30_000, 1.05, 0.4, 32, 8))
+        V, D, B, P = t.total_ids, 64, 32, 3
+        host = torch.from_numpy(np.random.default_rng(1).standard_normal((V, D))
+                                .astype(np.float32)).pin_memory()
+        assign = shard.assign_tables(shard.table_access_counts(t), world)
+        mine = [tt for tt in range(7) if assign[tt] == rank]
+        bags = dlrm.build_bags(t, mine, B, P)
+        flat = bags.reshape(-1)
+        rep = BufferReplay(32 * 8, V, 4, 32, len(flat))
+        rows = RowStore(rep, host)
+        rep.run(to_device_gids(torch, flat))      # some rows resident in HBM, the rest host
+        rows.refresh()
+        ex = dlrm.PeerExchange(rows, t.table_sizes, assign, rank, world, B)
+        res = []
+        for _ in range(3):                        # both output buffers, reused
+            res.append(ex.forward(torch.from_numpy(bags).cuda()).clone())
+        torch.cuda.synchronize()
+        allb = dlrm.build_bags(t, list(range(7)), B, P)
+        want = F.embedding_bag(torch.from_numpy(allb.reshape(-1, P)), host, mode="sum")
+        want = want.reshape(B, 7, D)[rank * B // world:(rank + 1) * B // world]
+        out[rank] = all(torch.equal(r.cpu(), want) for r in res)
+        dist.barrier()
+        ex.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_fused_pooled_all_to_all_over_peer_memory(world):
+    """K7 fused (config 4): the pooling epilogue stores every pooled row into
+    its owner's buffer through CUDA-IPC-mapped peer memory and a per-sender
+    epoch flag completes the exchange; world 2 runs two processes on one GPU.
+    The result equals EmbeddingBag over all tables for the rank's samples."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    out = mp.Manager().dict()
+    mp.spawn(_a2a_worker, args=(world, port, out), nprocs=world, join=True)
+    assert all(out[r] for r in range(world))
