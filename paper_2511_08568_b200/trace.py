@@ -339,7 +339,8 @@ def read_trace(path: str) -> Trace:
         out = [g for i, raw in enumerate(lines[1:], start=2)
                if (g := _parse_line(raw, i, sizes, off)) is not None]
         return Trace(np.asarray(out, dtype=np.int64), sizes)
-    data.decode("utf-8")    # the reference reads text: invalid UTF-8 raises here too
+    if not data.isascii():
+        data.decode("utf-8")    # the reference reads text: invalid UTF-8 raises here too
     nl = data.find(b"\n")
     first = (data if nl < 0 else data[:nl]).decode("utf-8")
     if not data:
