@@ -175,6 +175,14 @@ __device__ __forceinline__ void load_phase_tma(uint8_t *smem, const uint8_t *blo
     ph ^= 1u;
 }
 
+// thread 0: TMA-copy `len` bytes of the blob at `off` to smem `dst`, arriving on bar
+// (the caller arms the barrier with the total of all pieces first)
+__device__ __forceinline__ void tma_piece(uint8_t *dst, const uint8_t *blob, int64_t off,
+                                          int64_t len, uint64_t *bar) {
+    for (int64_t o = 0; o < len; o += 32768)
+        umma::bulk_g2s(dst + o, blob + off + o, (uint32_t)imin64(32768, len - o), bar);
+}
+
 // the three split products for one B matrix: d (+)= a * b, K = 64 (4 k-steps)
 // SINGLE: the reduced-precision variant (RECMG_PREC_TC16) keeps only xh * wh
 template <bool SINGLE>
@@ -749,7 +757,26 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
 #pragma unroll
         for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
         pc.mark(9);
-        load_phase_tma(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid, &tma_bar, tphase);
+        if (caching) {
+            // decoder layout (shared memory kept small: the L1 that holds the
+            // folded-table rows is what is left of the 256 KB): att_dec |
+            // Wcomb_h | Wcomb_c resident at [0, 48 KB), then one 64 KB slot
+            // that holds Wh_d for GEMM1 and Wc_d for GEMM2 (TMA swaps)
+            umma::fence_proxy_async();
+            __syncthreads();
+            if (c.tid == 0) {
+                umma::mbar_expect_tx(&tma_bar, (uint32_t)(2 * tl.img64 + tl.img256 + tl.img64));
+                tma_piece(smem, a.blob, tl.phase_off[1] + tl.b_off[3], 2 * tl.img64, &tma_bar);
+                tma_piece(smem + 2 * tl.img64, a.blob, tl.phase_off[1] + tl.b_off[6], tl.img64,
+                          &tma_bar);
+                tma_piece(smem + tl.dslot, a.blob, tl.phase_off[1] + tl.b_off[2], tl.img256,
+                          &tma_bar);
+            }
+            wait_mma(&tma_bar, tphase);
+        } else {
+            load_phase_tma(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid, &tma_bar,
+                           tphase);
+        }
         float lsum;
         if (caching) {
             zero_operand(c, A_H_HI, A_H_LO);
@@ -760,7 +787,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);   // t == T: only finish comb_{T-1}
                 pc.mark(3);
-                if (t >= 1) wait_mma(&mbar2, phase2);   // C = ctx Wcomb_c of step t-1
+                if (t >= 1) {
+                    wait_mma(&mbar2, phase2);                  // C = ctx Wcomb_c of step t-1
+                    if (!last) wait_mma(&tma_bar, tphase);     // Wh_d back in the slot
+                }
                 tmem_writes_done();
                 pc.mark(4);
                 // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
@@ -770,14 +800,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     umma::fence_after();
                     if (!last)
                         mma3<SINGLE>(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase + tl.b_off[3], 64, false);
+                             sbase, 64, false);                          // att_dec
                     if (t >= 1)
                         mma3<SINGLE>(c.tbase + COL_C, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase + tl.b_off[4], 64, true);
+                             sbase + tl.img64, 64, true);                // Wcomb_h
                     umma::commit(&mbar);
                     if (!last) {
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase + tl.b_off[2], 256, true);
+                             sbase + tl.dslot, 256, true);               // Wh_d (slot)
                         umma::commit(&mbar2);
                     }
                 }
@@ -798,10 +828,17 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 if (last) break;
                 pc.mark(6);
+                // Z += h Wh_d is long done: swap Wc_d into the slot under the context
+                wait_mma(&mbar2, phase2);
+                if (c.tid == 0) {
+                    umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                    tma_piece(smem + tl.dslot, a.blob, tl.phase_off[1] + tl.b_off[5], tl.img256,
+                              &tma_bar);
+                }
                 float ctx[U];
                 attn_context(c, Hs, t + 1, s_part, L, ctx);
                 store_operand<SINGLE>(c, A_X_HI, A_X_LO, ctx);
-                wait_mma(&mbar2, phase2);   // Z += h Wh_d (long done; keeps the phases paired)
+                wait_mma(&tma_bar, tphase);   // Wc_d in the slot
                 tmem_writes_done();
                 pc.mark(7);
                 // GEMM2 on ctx_t: Z += ctx Wc (barrier 1, the cell needs it) ;
@@ -809,14 +846,21 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (c.tid == 0) {
                     umma::fence_after();
                     mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_X_HI, c.tbase + A_X_LO,
-                         sbase + tl.b_off[5], 256, true);
+                         sbase + tl.dslot, 256, true);                   // Wc_d (slot)
                     umma::commit(&mbar);
                     mma3<SINGLE>(c.tbase + COL_C, c.tbase + A_X_HI, c.tbase + A_X_LO,
-                         sbase + tl.b_off[6], 64, false);
+                         sbase + 2 * tl.img64, 64, false);               // Wcomb_c
                     umma::commit(&mbar2);
                 }
                 if (t + 1 < T) dstage.prefetch(c, pid_dec, __ldg(gid + t + 1));
                 wait_mma(&mbar, phase);
+                // Wc_d done (and so every earlier MMA): swap Wh_d back under the cell
+                // (the last step's GEMM1 has no Z product, so it is not needed then)
+                if (t + 1 < T && c.tid == 0) {
+                    umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                    tma_piece(smem + tl.dslot, a.blob, tl.phase_off[1] + tl.b_off[2], tl.img256,
+                              &tma_bar);
+                }
                 pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
                 store_operand<SINGLE>(c, A_H_HI, A_H_LO, h);
@@ -1069,8 +1113,13 @@ TcLayout tc_layout(const recmg_model_shape *m) {
     (void)T;
     const size_t spart = (size_t)(m->kind == RECMG_MODEL_CACHING ? PartsOf<RECMG_MODEL_CACHING>::value : PartsOf<RECMG_MODEL_PREFETCH>::value) * m->l_in * 128 * 4;
     t.spart_off = 176 * 1024;
+    t.img64 = 64 * 256;
+    t.img256 = 256 * 256;
+    t.dslot = 3 * t.img64;
+    if (m->kind == RECMG_MODEL_CACHING) t.spart_off = (size_t)(t.dslot + t.img256);  // 112 KB
     size_t wmax = 0;
     for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
+    if (m->kind == RECMG_MODEL_CACHING) wmax = (size_t)t.phase_len[0];   // decoder: 112 KB (slot)
     t.smem_bytes = wmax > t.spart_off + spart ? wmax : t.spart_off + spart;
     t.total = o;
     return t;
