@@ -242,7 +242,7 @@ def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways, sh
                       f"numpy float64 forwards on {cores} threads {t1 - t0:.2f}s + C replay "
                       f"(dense per-id layout, sequential as runtime.py) + 32-way LRU "
                       f"{t2 - t1:.2f}s",
-            "model_s": t1 - t0, "replay_s": t2 - t1}
+            "model_s": t1 - t0, "replay_s": t2 - t1, "_bits": bits, "_pf": pf}
 
 
 def measure_rows(args, hp, n, torch):
@@ -583,8 +583,22 @@ def main():
     if variant is not None:
         line["variant_tc16"] = variant
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32,
-                                            shard=sh)
+        cb = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32, shard=sh)
+        # the GPU's own decisions vs the float64 port on the same chunks
+        # (bit and decoded-id agreement rates)
+        rb_, rp_ = cb.pop("_bits"), cb.pop("_pf")
+        ks = len(rb_)
+        gb = hp.bits[:ks].cpu().numpy()
+        gp = hp.pf[:ks].cpu().numpy()
+        cb["decision_agreement"] = {
+            "chunks": ks, "caching_bits": float((gb == rb_).mean()),
+            "prefetch_ids": float((gp == rp_).mean()),
+            "prefetch_ids_within_1e-5_V": float((np.abs(gp.astype(np.int64) - rp_) <=
+                                                  max(1, int(1e-5 * t.total_ids))).mean()),
+            "note": "GPU tc32 decisions vs the float64 oracle port (same fp32 embedding "
+                    "rows); decode floor(po*(V-1)+0.5) scales a logit difference by V "
+                    "(SURVEY.md §7.2 #2), so exact id agreement falls as V grows"}
+        line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -604,6 +618,7 @@ def run_reference(args, rank, world, torch, dist):
         vals, last = [], None
         for _ in range(args.steps):
             last = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32, shard=sh)
+            last.pop("_bits"), last.pop("_pf")
             vals.append(last["value"])
         value = statistics.median(vals)
         print(json.dumps({
@@ -654,6 +669,7 @@ def run_reference(args, rank, world, torch, dist):
     last = None
     for _ in range(args.steps):
         last = cpu_baseline(t, cp, pp, emb["caching"], emb["prefetch"], args.cpu_sample, C32, 32)
+        last.pop("_bits"), last.pop("_pf")
         vals.append(last["value"])
     value = statistics.median(vals)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
