@@ -598,7 +598,8 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     constexpr int NT = C::NT;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar, mbar2;   // caching: mbar2 tracks the MMAs split off
-    __shared__ uint64_t tma_bar;       // prefetch decoder: async weight swaps
+    __shared__ uint64_t tma_bar;       // async weight loads / swaps
+    __shared__ uint64_t tma_bar2;      // prefetch decoder: reload of the weights s_part overlays
     __shared__ uint32_t tmem_base_s;
     __shared__ float lpart[PARTS][128];
     __shared__ int s_tile;
@@ -618,6 +619,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         umma::mbar_init(&mbar, 1);
         umma::mbar_init(&mbar2, 1);
         umma::mbar_init(&tma_bar, 1);
+        umma::mbar_init(&tma_bar2, 1);
     }
     if (c.warp == 0) umma::tmem_alloc<512>(&tmem_base_s);
     umma::fence_before();
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     umma::fence_after();
     c.tbase = tmem_base_s;
     c.lane_addr = c.tbase + ((uint32_t)(32 * c.quad) << 16);
-    uint32_t phase = 0, phase2 = 0, tphase = 0;
+    uint32_t phase = 0, phase2 = 0, tphase = 0, tphase2 = 0;
     const uint32_t sbase = umma::smem_u32(smem);
     const TcLayout &tl = a.tl;
     const PackedLayout &pl = a.pl;
@@ -653,7 +655,24 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
 
         // ====================== encoder (model.py:131-145) ======================
         pc.mark(9);
-        load_phase_tma(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid, &tma_bar, tphase);
+        if (caching) {
+            load_phase_tma(smem, a.blob, tl.phase_off[0], tl.phase_len[0], c.tid, &tma_bar,
+                           tphase);
+        } else {
+            // prefetch encoder layout (small shared memory = more L1 for the
+            // folded-table rows): Wh1 | att_enc resident at [0, 80 KB), one
+            // 64 KB slot holding Wh0 for layer 0 and Wx1 for layer 1 (TMA swaps)
+            umma::fence_proxy_async();
+            __syncthreads();
+            if (c.tid == 0) {
+                umma::mbar_expect_tx(&tma_bar, (uint32_t)(tl.img256 + tl.img64 + tl.img256));
+                tma_piece(smem, a.blob, tl.phase_off[0] + tl.b_off[2], tl.img256 + tl.img64,
+                          &tma_bar);
+                tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[0], tl.img256,
+                          &tma_bar);
+            }
+            wait_mma(&tma_bar, tphase);
+        }
 #pragma unroll
         for (int k = 0; k < U; k++) { cs0[k] = 0.0f; cs1[k] = 0.0f; }
         if (caching) {
@@ -706,32 +725,39 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 // Q = h1(t-1) att_enc (barrier 2) right behind layer 0: it only
                 // needs h1(t-1), so it runs under the layer-0 cell and the keys
                 // of step t-1 are ready before the layer-1 product finishes
+                if (t >= 1 && !last) wait_mma(&tma_bar, tphase);   // Wh0 back in the slot
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last) {
-                        // layer 0: Z = Pid + Ptab + h0 Wh0
+                        // layer 0: Z = Pid + Ptab + h0 Wh0 (slot)
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                             sbase + tl.b_off[0], 256, true);
+                             sbase + tl.eslot, 256, true);
                         umma::commit(&mbar);
                     }
                     if (t >= 1) {
                         mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase + tl.b_off[3], 64, false);
+                             sbase + tl.img256, 64, false);               // att_enc
                         umma::commit(&mbar2);
                     }
                 }
                 if (!last) {
                     wait_mma(&mbar, phase);
+                    if (c.tid == 0) {   // Wh0 done: Wx1 into the slot under the layer-0 cell
+                        umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                        tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[1],
+                                  tl.img256, &tma_bar);
+                    }
                     cell<false>(c, nullptr, cs0, h);
                     store_operand<SINGLE>(c, P_H0_HI, P_H0_LO, h);
+                    wait_mma(&tma_bar, tphase);                    // Wx1 in the slot
                     tmem_writes_done();
                     // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell)
                     if (c.tid == 0) {
                         umma::fence_after();
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                             sbase + tl.b_off[1], 256, false);
+                             sbase + tl.eslot, 256, false);        // Wx1 (slot)
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase + tl.b_off[2], 256, true);
+                             sbase, 256, true);                    // Wh1
                         umma::commit(&mbar);
                     }
                 }
@@ -744,6 +770,11 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 if (!last) {
                     wait_mma(&mbar, phase);
+                    if (t + 1 < L && c.tid == 0) {   // Wx1 done: Wh0 back for the next step
+                        umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                        tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[0],
+                                  tl.img256, &tma_bar);
+                    }
                     cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
                     store_operand<SINGLE>(c, P_H1_HI, P_H1_LO, h);
                     storeU(Hs, c, t, h);
@@ -874,6 +905,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 const bool last = (t == T);
                 // (DEC-A weights resident) Q = h1 att_dec ; Z[0:64) = h1 Wcomb_h + ctx Wcomb_c
                 pc.mark(3);
+                if (t >= 1) wait_mma(&tma_bar2, tphase2);   // att_dec | Wcomb reloaded over s_part
                 tmem_writes_done();
                 pc.mark(4);
                 if (c.tid == 0) {
@@ -915,7 +947,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
                 init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
                 if (t >= 1) wait_mma(&tma_bar, tphase);       // Wctx0 | Wh0 back in the swap region
+                umma::fence_proxy_async();   // s_part reads done before the TMA overwrites them
                 tmem_writes_done();
+                // s_part overlays att_dec | Wcomb_h | Wcomb_c (idle between GEMM1 and the
+                // next step's GEMM1): reload them now, under GEMM2 and both cells
+                if (c.tid == 0) {
+                    umma::mbar_expect_tx(&tma_bar2, (uint32_t)(3 * tl.img64));
+                    tma_piece(smem, a.blob, tl.phase_off[1] + tl.b_off[4], 3 * tl.img64, &tma_bar2);
+                }
                 pc.mark(7);
                 if (c.tid == 0) {
                     umma::fence_after();
@@ -1117,9 +1156,15 @@ TcLayout tc_layout(const recmg_model_shape *m) {
     t.img256 = 256 * 256;
     t.dslot = 3 * t.img64;
     if (m->kind == RECMG_MODEL_CACHING) t.spart_off = (size_t)(t.dslot + t.img256);  // 112 KB
+    // prefetch: encoder Wh1 | att_enc | slot (144 KB); decoder DEC-A (176 KB) with
+    // s_part overlaying att_dec | Wcomb_h | Wcomb_c, reloaded every step
+    t.eslot = t.img256 + t.img64;
+    if (m->kind == RECMG_MODEL_PREFETCH) t.spart_off = 0;
     size_t wmax = 0;
     for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
     if (m->kind == RECMG_MODEL_CACHING) wmax = (size_t)t.phase_len[0];   // decoder: 112 KB (slot)
+    if (m->kind == RECMG_MODEL_PREFETCH)
+        wmax = (size_t)(t.phase_len[1] > t.eslot + t.img256 ? t.phase_len[1] : t.eslot + t.img256);
     t.smem_bytes = wmax > t.spart_off + spart ? wmax : t.spart_off + spart;
     t.total = o;
     return t;
