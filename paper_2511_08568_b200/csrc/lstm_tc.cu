@@ -805,8 +805,9 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             }
             wait_mma(&tma_bar, tphase);
         } else {
-            load_phase_tma(smem, a.blob, tl.phase_off[1], tl.phase_len[1], c.tid, &tma_bar,
-                           tphase);
+            // prefetch: the rotating region starts with att_dec | Wcomb_h | Wcomb_c
+            load_phase_tma(smem, a.blob, tl.phase_off[1] + tl.b_off[4], 3 * tl.img64, c.tid,
+                           &tma_bar, tphase);
         }
         float lsum;
         if (caching) {
@@ -901,27 +902,38 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             zero_operand(c, P_H0_HI, P_H0_LO);
             zero_operand(c, P_H1_HI, P_H1_LO);
             zero_operand(c, P_CTX_HI, P_CTX_LO);
+            // One 128 KB weight region at [0, 128 KB) rotates through the step:
+            // att_dec | Wcomb_h | Wcomb_c (GEMM1) -> Wctx0 | Wh0 (GEMM2) ->
+            // Wx1 | Wh1 (layer 1), each load issued by TMA as soon as the previous
+            // occupant's MMAs completed and hidden under the attention / the cells;
+            // s_part sits above it, so shared memory is 158 KB (L1 92 KB)
+            const int64_t dec_a = tl.phase_off[1];
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);
-                // (DEC-A weights resident) Q = h1 att_dec ; Z[0:64) = h1 Wcomb_h + ctx Wcomb_c
+                // GEMM1: Q = h1 att_dec ; Z[0:64) = h1 Wcomb_h + ctx Wcomb_c
                 pc.mark(3);
-                if (t >= 1) wait_mma(&tma_bar2, tphase2);   // att_dec | Wcomb reloaded over s_part
+                if (t >= 1) wait_mma(&tma_bar2, tphase2);   // att_dec | Wcomb back in the region
                 tmem_writes_done();
                 pc.mark(4);
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last)
                         mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase + tl.b_off[4], 64, false);
+                             sbase, 64, false);                          // att_dec
                     if (t >= 1) {
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase + tl.b_off[5], 64, false);
+                             sbase + tl.img64, 64, false);               // Wcomb_h
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
-                             sbase + tl.b_off[6], 64, true);
+                             sbase + 2 * tl.img64, 64, true);            // Wcomb_c
                     }
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
+                // GEMM1 done: Wctx0 | Wh0 into the region under the head and attention
+                if (!last && c.tid == 0) {
+                    umma::mbar_expect_tx(&tma_bar, (uint32_t)(2 * tl.img256));
+                    tma_piece(smem, a.blob, dec_a + tl.b_off[7], 2 * tl.img256, &tma_bar);
+                }
                 pc.mark(5);
                 if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_Z, comb_b, head_w);
                 if (!last) {
@@ -936,43 +948,29 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     for (int p = 0; p < PARTS; p++) lsum += lpart[p][c.row];
                     emit_logit(a, chunk, T, t - 1, lsum, false);
                 }
-                if (last) {
-                    if (t >= 1) wait_mma(&tma_bar, tphase);   // the last DEC-A swap-back
-                    break;
-                }
+                if (last) break;
                 pc.mark(6);
                 float ctx[U];
                 attn_context(c, Hs, L, s_part, L, ctx);
                 store_operand<SINGLE>(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
                 init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
-                if (t >= 1) wait_mma(&tma_bar, tphase);       // Wctx0 | Wh0 back in the swap region
-                umma::fence_proxy_async();   // s_part reads done before the TMA overwrites them
+                wait_mma(&tma_bar, tphase);                      // Wctx0 | Wh0 in the region
                 tmem_writes_done();
-                // s_part overlays att_dec | Wcomb_h | Wcomb_c (idle between GEMM1 and the
-                // next step's GEMM1): reload them now, under GEMM2 and both cells
-                if (c.tid == 0) {
-                    umma::mbar_expect_tx(&tma_bar2, (uint32_t)(3 * tl.img64));
-                    tma_piece(smem, a.blob, tl.phase_off[1] + tl.b_off[4], 3 * tl.img64, &tma_bar2);
-                }
                 pc.mark(7);
                 if (c.tid == 0) {
                     umma::fence_after();
                     mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
-                         sbase + tl.b_off[7], 256, true);
+                         sbase, 256, true);                              // Wctx0
                     mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                         sbase + tl.b_off[8], 256, true);
+                         sbase + tl.img256, 256, true);                  // Wh0
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
-                // Wctx0 | Wh0 are dead until the next step: swap DEC-B (Wx1 | Wh1)
-                // into their region with TMA while the layer-0 cell runs;
-                // att_dec / Wcomb stay resident below it
+                // GEMM2 done: DEC-B (Wx1 | Wh1) into the region under the layer-0 cell
                 if (c.tid == 0) {
                     umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.phase_len[2]);
-                    for (int64_t o = 0; o < tl.phase_len[2]; o += 32768)
-                        umma::bulk_g2s(smem + tl.swap_off + o, a.blob + tl.phase_off[2] + o,
-                                       (uint32_t)imin64(32768, tl.phase_len[2] - o), &tma_bar);
+                    tma_piece(smem, a.blob, tl.phase_off[2], tl.phase_len[2], &tma_bar);
                 }
                 pc.mark(8);
                 cell<false>(c, nullptr, cs0, h);
@@ -984,21 +982,17 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (c.tid == 0) {
                     umma::fence_after();
                     mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                         sbase + tl.swap_off + tl.b_off[9], 256, false);
+                         sbase + tl.b_off[9], 256, false);
                     mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                         sbase + tl.swap_off + tl.b_off[10], 256, true);
+                         sbase + tl.b_off[10], 256, true);
                     umma::commit(&mbar);
                 }
                 pc.mark(10);
                 wait_mma(&mbar, phase);
-                // swap Wctx0 | Wh0 back (needed at the next step's layer 0)
+                // layer 1 done: att_dec | Wcomb back for the next step's GEMM1
                 if (c.tid == 0) {
-                    const int64_t len = tl.phase_len[1] - tl.swap_off;
-                    umma::mbar_expect_tx(&tma_bar, (uint32_t)len);
-                    for (int64_t o = 0; o < len; o += 32768)
-                        umma::bulk_g2s(smem + tl.swap_off + o,
-                                       a.blob + tl.phase_off[1] + tl.swap_off + o,
-                                       (uint32_t)imin64(32768, len - o), &tma_bar);
+                    umma::mbar_expect_tx(&tma_bar2, (uint32_t)(3 * tl.img64));
+                    tma_piece(smem, a.blob, dec_a + tl.b_off[4], 3 * tl.img64, &tma_bar2);
                 }
                 pc.mark(11);
                 cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
@@ -1159,12 +1153,11 @@ TcLayout tc_layout(const recmg_model_shape *m) {
     // prefetch: encoder Wh1 | att_enc | slot (144 KB); decoder DEC-A (176 KB) with
     // s_part overlaying att_dec | Wcomb_h | Wcomb_c, reloaded every step
     t.eslot = t.img256 + t.img64;
-    if (m->kind == RECMG_MODEL_PREFETCH) t.spart_off = 0;
+    if (m->kind == RECMG_MODEL_PREFETCH) t.spart_off = (size_t)(2 * t.img256);   // 128 KB
     size_t wmax = 0;
     for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
     if (m->kind == RECMG_MODEL_CACHING) wmax = (size_t)t.phase_len[0];   // decoder: 112 KB (slot)
-    if (m->kind == RECMG_MODEL_PREFETCH)
-        wmax = (size_t)(t.phase_len[1] > t.eslot + t.img256 ? t.phase_len[1] : t.eslot + t.img256);
+    if (m->kind == RECMG_MODEL_PREFETCH) wmax = (size_t)(t.eslot + t.img256);   // encoder 144 KB
     t.smem_bytes = wmax > t.spart_off + spart ? wmax : t.spart_off + spart;
     t.total = o;
     return t;
