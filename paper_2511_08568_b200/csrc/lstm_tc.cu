@@ -6,9 +6,9 @@
 // that is ~22 significant bits per product, i.e. fp32-class logits (the
 // 1e-3 parity bar; tests/test_gpu_model.py).  Elementwise math stays fp32.
 //
-// Tile = 128 chunks = 128 TMEM lanes; 256 threads: warp w serves TMEM lane
-// quadrant (w & 3) and hidden units [32*(w>>2), +32), so every chunk row is
-// owned by two threads.  TMEM (512 columns):
+// Tile = 128 chunks = 128 TMEM lanes; 512 threads: warp w serves TMEM lane
+// quadrant (w & 3) and hidden units [16*(w>>2), +16), so every chunk row is
+// owned by four threads.  TMEM (512 columns):
 //   [0,256)   Z   gate pre-activations, gate-interleaved (col 4j+g)
 //   [256,320) Q   attention query / enc_pre of the previous step
 //   [320,384) C   comb accumulator (caching) / h1 operand (prefetch)
@@ -38,10 +38,10 @@ constexpr uint32_t A_H_HI = COL_A + 0, A_H_LO = COL_A + 32, A_X_HI = COL_A + 64,
 constexpr uint32_t P_H0_HI = COL_A + 0, P_H0_LO = COL_A + 32, P_CTX_HI = COL_A + 64,
                    P_CTX_LO = COL_A + 96, P_H1_HI = COL_C, P_H1_LO = COL_C + 32;  // prefetch
 
-// threads per chunk row: the caching model runs 2 (256 threads, 32 hidden
-// units each), the prefetch model 4 (512 threads, 16 units each) -- measured
-template <int KIND> struct PartsOf { static constexpr int value = 2; };
-template <> struct PartsOf<RECMG_MODEL_PREFETCH> { static constexpr int value = 4; };
+// threads per chunk row: 4 (512 threads, 16 hidden units each) for both
+// models -- measured; with the smaller shared-memory layouts the caching model
+// also gains from the 16 warps (2 threads per row were best at 191 KB)
+template <int KIND> struct PartsOf { static constexpr int value = 4; };
 
 __device__ __forceinline__ float ftanh(float x) {
     return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
