@@ -822,6 +822,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (t >= 1) {
                     wait_mma(&mbar2, phase2);                  // C = ctx Wcomb_c of step t-1
                     if (!last) wait_mma(&tma_bar, tphase);     // Wh_d back in the slot
+                    wait_mma(&tma_bar2, tphase2);              // att_dec | Wcomb_h over s_part
                 }
                 tmem_writes_done();
                 pc.mark(4);
@@ -871,7 +872,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 attn_context(c, Hs, t + 1, s_part, L, ctx);
                 store_operand<SINGLE>(c, A_X_HI, A_X_LO, ctx);
                 wait_mma(&tma_bar, tphase);   // Wc_d in the slot
+                umma::fence_proxy_async();    // s_part reads done before the TMA overwrites them
                 tmem_writes_done();
+                // s_part overlays att_dec | Wcomb_h (idle until the next GEMM1): reload
+                if (c.tid == 0) {
+                    umma::mbar_expect_tx(&tma_bar2, (uint32_t)(2 * tl.img64));
+                    tma_piece(smem, a.blob, tl.phase_off[1] + tl.b_off[3], 2 * tl.img64,
+                              &tma_bar2);
+                }
                 pc.mark(7);
                 // GEMM2 on ctx_t: Z += ctx Wc (barrier 1, the cell needs it) ;
                 // C = ctx Wcomb_c (barrier 2, read by the next step's head)
@@ -1149,14 +1157,17 @@ TcLayout tc_layout(const recmg_model_shape *m) {
     t.img64 = 64 * 256;
     t.img256 = 256 * 256;
     t.dslot = 3 * t.img64;
-    if (m->kind == RECMG_MODEL_CACHING) t.spart_off = (size_t)(t.dslot + t.img256);  // 112 KB
+    // caching: the partial scores overlay att_dec | Wcomb_h (reloaded each step)
+    if (m->kind == RECMG_MODEL_CACHING) t.spart_off = 0;
     // prefetch: encoder Wh1 | att_enc | slot (144 KB); decoder DEC-A (176 KB) with
     // s_part overlaying att_dec | Wcomb_h | Wcomb_c, reloaded every step
     t.eslot = t.img256 + t.img64;
     if (m->kind == RECMG_MODEL_PREFETCH) t.spart_off = (size_t)(2 * t.img256);   // 128 KB
     size_t wmax = 0;
     for (int i = 0; i < 3; i++) wmax = wmax > (size_t)t.phase_len[i] ? wmax : (size_t)t.phase_len[i];
-    if (m->kind == RECMG_MODEL_CACHING) wmax = (size_t)t.phase_len[0];   // decoder: 112 KB (slot)
+    if (m->kind == RECMG_MODEL_CACHING)   // encoder 80 KB, decoder 112 KB (R1 + slot)
+        wmax = (size_t)(t.dslot + t.img256) > (size_t)t.phase_len[0] ? (size_t)(t.dslot + t.img256)
+                                                                     : (size_t)t.phase_len[0];
     if (m->kind == RECMG_MODEL_PREFETCH) wmax = (size_t)(t.eslot + t.img256);   // encoder 144 KB
     t.smem_bytes = wmax > t.spart_off + spart ? wmax : t.spart_off + spart;
     t.total = o;
