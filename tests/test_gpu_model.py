@@ -79,6 +79,29 @@ def test_attention_exponent_range(which, precision):
         _check(got, ref)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "tc32"])
+def test_batch_equals_single_bit_exact(precision):
+    """test_model.py:89-96 (batch == single at rel 1e-12), held bit-exactly:
+    a chunk's logits do not depend on its tile, its row in the tile or the
+    batch size (one chunk alone, a permuted batch, a ragged tail)."""
+    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 300 * 15 + 30, 1.05, 0.4, 32, 0))
+    K = rb.num_chunks(len(t))
+    gid = t.gid_array[:K * 15].reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    perm = np.random.default_rng(5).permutation(K)
+    for kind, seed, fwd in (("caching", 0, rb.forward_caching_batch),
+                            ("prefetch", 1, rb.forward_prefetch_batch)):
+        p = rb.init_params(kind, t.table_sizes, dim=64, seed=seed, init_scale=0.4)
+        full = fwd(p, gid, tid, precision).logits
+        shuf = fwd(p, gid[perm], tid[perm], precision).logits
+        assert np.array_equal(shuf, full[perm]), kind
+        for k in (0, 129, K - 1):
+            one = fwd(p, gid[k:k + 1], tid[k:k + 1], precision).logits
+            assert np.array_equal(one[0], full[k]), (kind, k)
+        tail = fwd(p, gid[K - 45:], tid[K - 45:], precision).logits
+        assert np.array_equal(tail, full[K - 45:]), kind
+
+
 def test_gpu_decisions_in_replay_path():
     """bits / decoded prefetch ids emitted by the kernel (runtime.py:192,
     model.py:250-258) vs the oracle's, through the replay entry point."""
