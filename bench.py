@@ -131,6 +131,20 @@ def prefetch_flops(L, T, d):
     return 2 * (21 * L * d * d + T * (27 * d * d + 2 * L * d + d))
 
 
+def caching_transcendentals(L, d):
+    # 11 L d + L^2 d + L^2 + L per chunk
+    return 11 * L * d + L * L * d + L * L + L
+
+
+def prefetch_transcendentals(L, T, d):
+    # 10 L d + T (L d + L + 11 d + 1) per chunk
+    return 10 * L * d + T * (L * d + L + 11 * d + 1)
+
+
+# MUFU: 16 results / clk / SM, 148 SMs, nominal max SM clock
+MUFU_PEAK_PER_S = 16 * 148 * 1.965e9
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -184,6 +198,20 @@ def load_profile_traffic():
             return json.load(f)
     except (OSError, ValueError):
         return None
+
+
+def fwd_figures(ms, flops, transc, prof, pieces):
+    """One forward's step total: tensor TFLOP/s (algorithmic), the MUFU
+    (transcendental) rate against its peak -- the second roofline SURVEY.md
+    §8(d) names for the LSTM -- and the DRAM rate of the ncu capture's
+    per-launch traffic over the measured per-launch time."""
+    out = {"ms": ms, "tflops": flops / (ms / 1e3) / 1e12,
+           "transcendentals_per_s": transc / (ms / 1e3),
+           "mufu_frac": transc / (ms / 1e3) / MUFU_PEAK_PER_S,
+           "mufu_peak_source": "16 / clk / SM x 148 SMs x 1965 MHz (SURVEY.md §8(d))"}
+    if prof.get("dram_bytes_per_launch"):
+        out["dram_gbs"] = prof["dram_bytes_per_launch"] / (ms / max(1, pieces) / 1e3) / 1e9
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -546,8 +574,12 @@ def main():
             "launches_per_step": max(1, args.pieces),
             "traffic": prof.get(dominant, {}).get("dram_bytes_per_launch"),
             "kernels": {
-                "caching_fwd": {"ms": mean["caching_fwd"], "tflops": fl_c / (mean["caching_fwd"] / 1e3) / 1e12},
-                "prefetch_fwd": {"ms": mean["prefetch_fwd"], "tflops": fl_p / (mean["prefetch_fwd"] / 1e3) / 1e12},
+                "caching_fwd": fwd_figures(mean["caching_fwd"], fl_c,
+                                           caching_transcendentals(15, args.dim) * K,
+                                           prof.get("caching_fwd", {}), args.pieces),
+                "prefetch_fwd": fwd_figures(mean["prefetch_fwd"], fl_p,
+                                            prefetch_transcendentals(15, 5, args.dim) * K,
+                                            prof.get("prefetch_fwd", {}), args.pieces),
                 "replay": {"ms": mean["replay"], "gbs": (ev_n * 4 + n) / (mean["replay"] / 1e3) / 1e9,
                            "bound": "hbm (7.33 B/access algorithmic); dependency-chain bound",
                            "overlapped": True},
