@@ -730,6 +730,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 if (!last) {
                     wait_mma(&mbar, phase);
+                    pc.mark(2);
                     if (c.tid == 0) {   // Wh0 done: Wx1 into the slot under the layer-0 cell
                         umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
                         tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[1],
@@ -737,8 +738,11 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     }
                     cell<false>(c, nullptr, cs0, h);
                     store_operand<SINGLE>(c, P_H0_HI, P_H0_LO, h);
+                    pc.mark(15);
                     wait_mma(&tma_bar, tphase);                    // Wx1 in the slot
+                    pc.mark(14);
                     tmem_writes_done();
+                    pc.mark(12);
                     // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell)
                     if (c.tid == 0) {
                         umma::fence_after();
@@ -750,14 +754,17 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     }
                 }
                 if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
+                pc.mark(13);
                 if (t >= 1) {
                     wait_mma(&mbar2, phase2);
                     float ep[U];
                     readU(c, COL_Q, ep);
                     store_keys(Es, c, t - 1, ep, rawmask);
                 }
+                pc.mark(10);
                 if (!last) {
                     wait_mma(&mbar, phase);
+                    pc.mark(11);
                     if (t + 1 < L && c.tid == 0) {   // Wx1 done: Wh0 back for the next step
                         umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
                         tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[0],

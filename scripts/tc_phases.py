@@ -12,8 +12,9 @@ import paper_2511_08568_b200 as rb
 from paper_2511_08568_b200 import _native
 from paper_2511_08568_b200.model import DeviceModel, init_params_device
 
-PF_NAMES = {1: "enc L0 MMA issue+wait", 2: "enc cell0+sync", 12: "enc L1 MMA issue", 14: "enc row prefetch",
-            13: "enc L1 MMA wait", 11: "enc keys+cell1 / dec L1 cell"}
+PF_NAMES = {1: "enc Wh0 swap wait+L0 MMA", 2: "enc cell0", 15: "enc Wx1 swap wait", 14: "enc sync",
+            12: "enc L1 issue+row prefetch", 13: "enc Q wait+keys", 10: "enc L1 MMA wait",
+            11: "enc cell1 / dec L1 cell"}
 NAMES = ["enc table init+sync", "enc MMA wait", "enc epilogue", "dec init+sync",
          "dec MMA1 wait", "dec head+scores+sync", "dec softmax/ctx+sync", "dec MMA2 wait",
          "dec cell", "weight loads", "pf L1 MMA wait", "pf L1 cell", "enc MMA issue", "enc row prefetch", "", "other"]
