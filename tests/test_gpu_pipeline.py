@@ -40,3 +40,27 @@ def test_replay_host_matches_device_and_oracle(pieces):
                           "prefetch_useful", "evictions", "prefetch_inserts")]
     assert rep_h.coverage == cov
     assert lru_h[0] == oracle.lru(t.gid_array, t.total_ids, C32, 32)
+
+
+def test_replay_host_edge_sizes_and_reuse():
+    """One HotPath reused for traces of every awkward length: shorter than one
+    chunk (all accesses are tail, served demand-only, runtime.py:278-280),
+    exactly one chunk, fewer chunks than pieces x 128, and a ragged tail;
+    each equals the one-shot replay() of the same prefix and the LRU
+    simulator, so no state leaks from a longer earlier replay."""
+    t = rb.generate_trace(rb.TraceGenConfig([700] * 8, 40_000, 1.05, 0.4, 32, 21))
+    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=0.4)
+    C = int(0.2 * t.unique_count)
+    C32 = C - C % 32
+    hp = HotPath(cp, pp, t.table_sizes, C32, len(t), ways=32, lru_capacity=C32, lru_ways=32,
+                 pieces=8)
+    for n in (40_000, 29, 30, 45, 1_000, 8 * 128 * 15 + 29, 40_000 - 7):
+        sub = rb.trace_from_gids(t.gid_array[:n], t.table_sizes)
+        rep, (h, m) = hp.replay_host(t.gid_array[:n].astype(np.int32))
+        ref = rb.replay(sub, rb.BufferConfig(C32, 4, 32), cp, pp)
+        assert rep == ref and (rep.evictions, rep.prefetch_inserts) == \
+            (ref.evictions, ref.prefetch_inserts), n
+        assert rep.total == n and h + m == n, n
+        assert m == rb.simulate(sub, rb.CacheConfig(C32, rb.Policy.LRU, 32),
+                                per_access=False).misses, n
