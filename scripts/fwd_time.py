@@ -12,12 +12,13 @@ from paper_2511_08568_b200.model import DeviceModel, init_params_device
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 7
+precision = sys.argv[3] if len(sys.argv) > 3 else "auto"
 t = rb.generate_trace(rb.TraceGenConfig([50000] * 256, n, 1.05, 0.4, 32, 2))
 K = rb.num_chunks(len(t))
 g = torch.from_numpy(t.gid_array[:K * 15].astype(np.int32).reshape(K, 15)).cuda()
 for kind, seed in (("caching", 0), ("prefetch", 1)):
     p, emb = init_params_device(kind, t.table_sizes, dim=64, seed=seed, init_scale=0.4)
-    dm = DeviceModel(p, emb)
+    dm = DeviceModel(p, emb, precision=precision)
     tid = dm.table_ids(g)
     out = torch.empty((K, dm.out_len), dtype=torch.float32, device="cuda")
     ms = []
