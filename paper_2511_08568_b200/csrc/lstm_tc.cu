@@ -77,6 +77,19 @@ __device__ __forceinline__ void rcp4_bounded(float &a, float &b, float &c, float
 // 1 / (1 + e^(-x)) and tanh = 1 - 2 / (1 + e^(2x)) denominators
 __device__ __forceinline__ float sig_den(float x) { return 1.0f + __expf(-x); }
 __device__ __forceinline__ float tanh_den(float x) { return 1.0f + __expf(2.0f * x); }
+// The gate pre-activations arrive pre-scaled (packing multiplies every gate
+// column of the LSTM weights, folded token tables, layer-1 biases and slot
+// projections by gate_scale): z' = -log2(e) z for i, f, o and 2 log2(e) z for
+// g, so each gate's denominator is one MUFU.EX2 with no FMUL in front.
+constexpr float kLog2e = 1.4426950408889634f;
+__host__ __device__ __forceinline__ float gate_scale(int g) {
+    return g == 2 ? 2.0f * kLog2e : -kLog2e;
+}
+__device__ __forceinline__ float ex2_den(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return 1.0f + r;
+}
 
 // Attention scores tanh(e + q) (model.py:118) use e^(2(e+q)) = e^(2e) e^(2q):
 // the encoder stores X = e^(2e) once per position, each decoder step
@@ -340,7 +353,7 @@ __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
                     const float4 bb = __ldg(b4 + j);
                     zi += bb.x; zf += bb.y; zg += bb.z; zo += bb.w;
                 }
-                float ig = sig_den(zi), fg = sig_den(zf), gd = tanh_den(zg), o = sig_den(zo);
+                float ig = ex2_den(zi), fg = ex2_den(zf), gd = ex2_den(zg), o = ex2_den(zo);
                 rcp4(ig, fg, gd, o);
                 const float gg = fmaf(-2.0f, gd, 1.0f);
                 cs[j] = fg * cs[j] + ig * gg;
@@ -1031,7 +1044,7 @@ __global__ void bimage_kernel(const float *raw, uint8_t *out, BSpec s, int d) {
          i += (int64_t)gridDim.x * blockDim.x) {
         const int n = (int)(i / 64), k = (int)(i % 64);
         const int col = s.gates ? ((n & 3) * d + (n >> 2)) : n;
-        const float w = raw[s.src + (int64_t)k * s.ld + col];
+        const float w = raw[s.src + (int64_t)k * s.ld + col] * (s.gates ? gate_scale(n & 3) : 1.0f);
         const __half hi = __float2half_rn(w);
         const __half lo = __float2half_rn(w - __half2float(hi));
         const uint32_t off = umma::kmajor_offset(n, k, 64);
@@ -1081,7 +1094,7 @@ __global__ void proj_fold_kernel(const float *E, int64_t rows, int d, const floa
         }
 #pragma unroll
         for (int q = 0; q < 32; q++)
-            if (r0 + q < rows) out[(r0 + q) * 4 * d + n] = acc[q];
+            if (r0 + q < rows) out[(r0 + q) * 4 * d + n] = acc[q] * gate_scale(g);
     }
 }
 
@@ -1169,10 +1182,32 @@ TcLayout tc_layout(const recmg_model_shape *m) {
     return t;
 }
 
+// x[i] *= gate_scale(i & 3) over gate-interleaved [.][4d] rows
+__global__ void gate_scale_kernel(float *x, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] *= gate_scale((int)(i & 3));
+}
+
 int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *embed_id,
                   const int64_t *offsets, void *packed_dense, void *tc_blob, cudaStream_t s) {
     int rc = model_pack(m, raw, packed_dense, s);
     if (rc) return rc;
+    {   // the gate rows the TC kernels read from the dense blob: layer >= 1
+        // biases (added in the cell) and the prefetch slot projections (Z init)
+        const PackedLayout p = packed_layout(m);
+        float *dense = (float *)packed_dense;
+        for (int k = 1; k < m->stacks; k++) {
+            gate_scale_kernel<<<1, 256, 0, s>>>(dense + p.enc_b[k], 4 * m->dim);
+            RECMG_LAUNCH_CHECK();
+            gate_scale_kernel<<<1, 256, 0, s>>>(dense + p.dec_b[k], 4 * m->dim);
+            RECMG_LAUNCH_CHECK();
+        }
+        if (m->kind == RECMG_MODEL_PREFETCH) {
+            gate_scale_kernel<<<4, 256, 0, s>>>(dense + p.slot_proj, (int64_t)m->l_out * 4 * m->dim);
+            RECMG_LAUNCH_CHECK();
+        }
+    }
     const RawLayout r = raw_layout(m);
     const TcLayout t = tc_layout(m);
     const int d = m->dim;
