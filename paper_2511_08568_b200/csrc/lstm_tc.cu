@@ -355,10 +355,11 @@ __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
                 }
                 float ig = ex2_den(zi), fg = ex2_den(zf), gd = ex2_den(zg), o = ex2_den(zo);
                 rcp4(ig, fg, gd, o);
-                const float gg = fmaf(-2.0f, gd, 1.0f);
+                // the cell state is kept scaled by 2 log2(e): c' = f c' + i (2 log2(e) g)
+                const float gg = fmaf(-4.0f * kLog2e, gd, 2.0f * kLog2e);
                 cs[j] = fg * cs[j] + ig * gg;
                 og[u] = o;
-                dc[u] = tanh_den(cs[j]);
+                dc[u] = ex2_den(cs[j]);
             }
             rcp4(dc[0], dc[1], dc[2], dc[3]);
 #pragma unroll
@@ -556,7 +557,7 @@ __device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
     for (int k = 0; k < U; k += 4) {
         float d[4];
 #pragma unroll
-        for (int i = 0; i < 4; i++) d[i] = tanh_den(v[k + i] + __ldg(comb_b + U * c.part + k + i));
+        for (int i = 0; i < 4; i++) d[i] = ex2_den(v[k + i] + __ldg(comb_b + U * c.part + k + i));
         rcp4(d[0], d[1], d[2], d[3]);
 #pragma unroll
         for (int i = 0; i < 4; i++)
@@ -1034,7 +1035,9 @@ struct BSpec {
     int64_t src;      // float offset in the raw blob of W[k0][0]
     int64_t ld;       // row stride of W (floats)
     int N;            // output columns
-    int gates;        // 1: B row n = 4j+g reads W column g*d+j ; 0: identity
+    int gates;        // 1: B row n = 4j+g reads W column g*d+j, scaled by gate_scale(g);
+                      // 0: identity; 2: identity, scaled by 2 log2(e) (W_comb: the head's
+                      // tanh denominators then need no FMUL)
     int64_t dst;      // byte offset of the hi image in the TC blob
 };
 
@@ -1043,8 +1046,9 @@ __global__ void bimage_kernel(const float *raw, uint8_t *out, BSpec s, int d) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int n = (int)(i / 64), k = (int)(i % 64);
-        const int col = s.gates ? ((n & 3) * d + (n >> 2)) : n;
-        const float w = raw[s.src + (int64_t)k * s.ld + col] * (s.gates ? gate_scale(n & 3) : 1.0f);
+        const int col = s.gates == 1 ? ((n & 3) * d + (n >> 2)) : n;
+        const float w = raw[s.src + (int64_t)k * s.ld + col] *
+                        (s.gates == 1 ? gate_scale(n & 3) : s.gates == 2 ? 2.0f * kLog2e : 1.0f);
         const __half hi = __float2half_rn(w);
         const __half lo = __float2half_rn(w - __half2float(hi));
         const uint32_t off = umma::kmajor_offset(n, k, 64);
@@ -1189,6 +1193,12 @@ __global__ void gate_scale_kernel(float *x, int64_t n) {
         x[i] *= gate_scale((int)(i & 3));
 }
 
+__global__ void scale_kernel(float *x, int64_t n, float sc) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] *= sc;
+}
+
 int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *embed_id,
                   const int64_t *offsets, void *packed_dense, void *tc_blob, cudaStream_t s) {
     int rc = model_pack(m, raw, packed_dense, s);
@@ -1207,6 +1217,8 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
             gate_scale_kernel<<<4, 256, 0, s>>>(dense + p.slot_proj, (int64_t)m->l_out * 4 * m->dim);
             RECMG_LAUNCH_CHECK();
         }
+        scale_kernel<<<1, 64, 0, s>>>(dense + p.comb_b, m->dim, 2.0f * kLog2e);   // head bias
+        RECMG_LAUNCH_CHECK();
     }
     const RawLayout r = raw_layout(m);
     const TcLayout t = tc_layout(m);
@@ -1222,17 +1234,17 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
         spec(0, 1, r.att_enc, d, 64, 0);
         spec(1, 2, r.dec_wh[0], 4 * d, 256, 1);
         spec(1, 3, r.att_dec, d, 64, 0);
-        spec(1, 4, r.comb_w, d, 64, 0);                       // rows 0..d-1: h part
+        spec(1, 4, r.comb_w, d, 64, 2);                       // rows 0..d-1: h part
         spec(1, 5, r.dec_wx[0] + 2 * d * 4 * d, 4 * d, 256, 1); // rows 2d..3d-1: ctx part
-        spec(1, 6, r.comb_w + d * d, d, 64, 0);               // rows d..2d-1: ctx part
+        spec(1, 6, r.comb_w + d * d, d, 64, 2);               // rows d..2d-1: ctx part
     } else {
         spec(0, 0, r.enc_wh[0], 4 * d, 256, 1);
         spec(0, 1, r.enc_wx[1], 4 * d, 256, 1);
         spec(0, 2, r.enc_wh[1], 4 * d, 256, 1);
         spec(0, 3, r.att_enc, d, 64, 0);
         spec(1, 4, r.att_dec, d, 64, 0);
-        spec(1, 5, r.comb_w, d, 64, 0);
-        spec(1, 6, r.comb_w + d * d, d, 64, 0);
+        spec(1, 5, r.comb_w, d, 64, 2);
+        spec(1, 6, r.comb_w + d * d, d, 64, 2);
         spec(1, 7, r.dec_wx[0] + 2 * d * 4 * d, 4 * d, 256, 1);
         spec(1, 8, r.dec_wh[0], 4 * d, 256, 1);
         spec(2, 9, r.dec_wx[1], 4 * d, 256, 1);
