@@ -252,7 +252,11 @@ int recmg_model_pack(const recmg_model_shape *shape, const float *dense_raw, voi
 /* TC32 packing also needs embed_id [total_ids x dim] fp32 and the table
  * offsets [n_tables+1] int64 (device): the layer-0 token projection
  * [E_id[r]; E_tab[tab(r)]] @ Wx + b is folded into one row per id r.  The
- * TC32 forward then ignores embed_id and tid.                              */
+ * TC32 forward then ignores embed_id and tid.  A TC-packed buffer serves
+ * RECMG_PREC_TC32 / TC16 only: its gate columns, folded rows, layer-1
+ * biases, slot projections and W_comb / comb bias are stored pre-scaled for
+ * exp2 (-log2 e, 2 log2 e), so RECMG_PREC_FP32 needs its own
+ * recmg_model_pack buffer.                                                  */
 int recmg_model_pack_tc(const recmg_model_shape *shape, const float *dense_raw,
                         const float *embed_id, const int64_t *table_offsets, void *packed,
                         void *stream);
