@@ -510,14 +510,23 @@ __device__ __forceinline__ void acc_ctx(float (&ctx)[4 * NQ], float e, const flo
     }
 }
 
+constexpr float kShiftMax = 40.0f;   // e^(-2 * 40) = 1.8e-35 > FLT_MIN
+
 // softmax over positions + context on this thread's units (model.py:120-123)
 template <int PARTS>
 __device__ __forceinline__ void attn_context(const Ctx<PARTS> &c, float *Hs, int npos,
-                                             const float *s_part, int L,
+                                             const float *s_part, int L, float vabs,
                                              float (&ctx)[Ctx<PARTS>::U]) {
     constexpr int NQ = Ctx<PARTS>::NQ;
-    float mx = -INFINITY;
-    for (int j = 0; j < npos; j++) mx = fmaxf(mx, full_score<PARTS>(s_part, L, j, c.row));
+    // softmax shift (autodiff.py:226-236 uses the max): every score is
+    // sum_u v_u tanh(.), so |s| <= vabs = sum_u |v_u| and e^(s - vabs) stays a
+    // normal float while vabs <= kShiftMax; the shift cancels in the ratio, so
+    // the max pass is skipped.  Larger |v| falls back to the max.
+    float mx = vabs;
+    if (vabs > kShiftMax) {
+        mx = -INFINITY;
+        for (int j = 0; j < npos; j++) mx = fmaxf(mx, full_score<PARTS>(s_part, L, j, c.row));
+    }
 #pragma unroll
     for (int k = 0; k < 4 * NQ; k++) ctx[k] = 0.0f;
     float sum = 0.0f;
@@ -643,6 +652,8 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     const float head_b = __ldg(a.dense + pl.head_b);
     float vsum = 0.0f;   // sum of this thread's att_v units (score_fast)
     for (int k = 0; k < U; k++) vsum += __ldg(att_v + U * c.part + k);
+    float vabs = 0.0f;   // sum over all d units of |att_v| (attn_context's shift)
+    for (int k = 0; k < 64; k++) vabs += fabsf(__ldg(att_v + k));
     const int64_t n_tiles = (a.batch + 127) / 128;
 
     // dynamic tile scheduler: a CTA that starts late (its SM busy with a
@@ -878,7 +889,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                               &tma_bar);
                 }
                 float ctx[U];
-                attn_context(c, Hs, t + 1, s_part, L, ctx);
+                attn_context(c, Hs, t + 1, s_part, L, vabs, ctx);
                 store_operand<SINGLE>(c, A_X_HI, A_X_LO, ctx);
                 wait_mma(&tma_bar, tphase);   // Wc_d in the slot
                 umma::fence_proxy_async();    // s_part reads done before the TMA overwrites them
@@ -968,7 +979,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (last) break;
                 pc.mark(6);
                 float ctx[U];
-                attn_context(c, Hs, L, s_part, L, ctx);
+                attn_context(c, Hs, L, s_part, L, vabs, ctx);
                 store_operand<SINGLE>(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
                 init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);

@@ -79,6 +79,28 @@ def test_attention_exponent_range(which, precision):
         _check(got, ref)
 
 
+@pytest.mark.parametrize("vscale", [1.0, 10.0])
+def test_softmax_shift_paths(vscale):
+    """The tc kernels shift the attention softmax by sum|att_v| (a bound on
+    every score) while that stays <= 40, and by the running max beyond
+    (lstm_tc.cu attn_context): both paths against the float64 oracle."""
+    t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 300 * 15 + 30, 1.05, 0.4, 32, 0))
+    K = rb.num_chunks(len(t))
+    gid = t.gid_array[:K * 15].reshape(K, 15)
+    tid = t.table_ids[:K * 15].reshape(K, 15)
+    for kind, seed in (("caching", 0), ("prefetch", 1)):
+        p = rb.init_params(kind, t.table_sizes, dim=64, seed=seed, init_scale=0.4)
+        p.arrays["att_v"] = (p.arrays["att_v"] * vscale).astype(p.arrays["att_v"].dtype)
+        assert (np.abs(p.arrays["att_v"]).sum() > 40.0) == (vscale > 1.0)
+        if kind == "caching":
+            got = rb.forward_caching_batch(p, gid, tid, "tc32").logits
+            ref = mo.caching_logits(p.arrays, 64, 1, gid, tid)
+        else:
+            got = rb.forward_prefetch_batch(p, gid, tid, "tc32").logits
+            ref = mo.prefetch_logits(p.arrays, 64, 2, 5, gid, tid)
+        _check(got, ref)
+
+
 @pytest.mark.parametrize("precision", ["fp32", "tc32"])
 def test_batch_equals_single_bit_exact(precision):
     """test_model.py:89-96 (batch == single at rel 1e-12), held bit-exactly:
