@@ -65,15 +65,6 @@ __device__ __forceinline__ void rcp4(float &a, float &b, float &c, float &d) {
     const float ia = rab * b, ib = rab * a, ic = rcd * d, id = rcd * c;
     a = ia; b = ib; c = ic; d = id;
 }
-// rcp4 without the clamps, for denominators known to be in [1, 2^31]
-// (the attention scores: 1 + e^(2e) e^(2q) with |2e|, |2q| <= kExpLim = 11)
-__device__ __forceinline__ void rcp4_bounded(float &a, float &b, float &c, float &d) {
-    const float ab = a * b, cd = c * d;
-    const float r = frcp(ab * cd);
-    const float rab = r * cd, rcd = r * ab;
-    const float ia = rab * b, ib = rab * a, ic = rcd * d, id = rcd * c;
-    a = ia; b = ib; c = ic; d = id;
-}
 // 1 / (1 + e^(-x)) and tanh = 1 - 2 / (1 + e^(2x)) denominators
 __device__ __forceinline__ float sig_den(float x) { return 1.0f + __expf(-x); }
 __device__ __forceinline__ float tanh_den(float x) { return 1.0f + __expf(2.0f * x); }
@@ -421,19 +412,22 @@ __device__ __forceinline__ void store_keys(float *Es, const Ctx<PARTS> &c, int j
 template <int NQ>
 __device__ __forceinline__ float score_fast(const float4 (&x)[NQ], const float (&qx)[4 * NQ],
                                             const float4 *v4) {
-    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+    // per 4 units: sum v_k / d_k as one fraction over d_a d_b d_c d_d (each
+    // d in [1, 2^32), so the product stays finite), one MUFU.RCP per 4 units
+    float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
     for (int u = 0; u < NQ; u++) {
         const float4 v = __ldg(v4 + u);
-        float a = fmaf(x[u].x, qx[4 * u + 0], 1.0f), b = fmaf(x[u].y, qx[4 * u + 1], 1.0f);
-        float cc = fmaf(x[u].z, qx[4 * u + 2], 1.0f), d = fmaf(x[u].w, qx[4 * u + 3], 1.0f);
-        rcp4_bounded(a, b, cc, d);
-        s0 = fmaf(v.x, a, s0);
-        s1 = fmaf(v.y, b, s1);
-        s2 = fmaf(v.z, cc, s2);
-        s3 = fmaf(v.w, d, s3);
+        const float a = fmaf(x[u].x, qx[4 * u + 0], 1.0f), b = fmaf(x[u].y, qx[4 * u + 1], 1.0f);
+        const float cc = fmaf(x[u].z, qx[4 * u + 2], 1.0f), d = fmaf(x[u].w, qx[4 * u + 3], 1.0f);
+        const float dab = a * b, dcd = cc * d;
+        const float nab = fmaf(v.x, b, v.y * a), ncd = fmaf(v.z, d, v.w * cc);
+        const float num = fmaf(nab, dcd, ncd * dab);
+        const float r = frcp(dab * dcd);
+        if (u & 1) s1 = fmaf(num, r, s1);
+        else s0 = fmaf(num, r, s0);
     }
-    return -2.0f * ((s0 + s1) + (s2 + s3));   // + sum_u v_u by the caller
+    return -2.0f * (s0 + s1);   // + sum_u v_u by the caller
 }
 
 // direct form: raw keys (raw) or keys stored as X = e^(2e) recovered by log
