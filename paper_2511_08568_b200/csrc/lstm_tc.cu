@@ -88,7 +88,7 @@ __device__ __forceinline__ float ex2_den(float x) {
 // quarter MUFU.RCP instead of ex2 + rcp.  Exponents beyond +-kExpLim fall
 // back to the direct form (raw e kept for that position / q out of range).
 // kExpLim = 11 bounds each denominator by 1 + e^22 < 2^32, so the product
-// of four stays finite and rcp4 needs no clamps (|e|, |q| < 4.5 at init
+// of four stays finite and score_fast needs no clamps (|e|, |q| < 4.5 at init
 // 0.4 / 0.6; at init 1.0 about 5% of positions take the direct form).
 constexpr float kExpLim = 11.0f;
 
