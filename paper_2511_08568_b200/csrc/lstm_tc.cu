@@ -411,13 +411,13 @@ __device__ __forceinline__ void store_keys(float *Es, const Ctx<PARTS> &c, int j
 // sum_u v_u tanh(e_u + q_u) over this thread's units for one position
 template <int NQ>
 __device__ __forceinline__ float score_fast(const float4 (&x)[NQ], const float (&qx)[4 * NQ],
-                                            const float4 *v4) {
+                                            const float4 (&vr)[NQ]) {
     // per 4 units: sum v_k / d_k as one fraction over d_a d_b d_c d_d (each
     // d in [1, 2^32), so the product stays finite), one MUFU.RCP per 4 units
     float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
     for (int u = 0; u < NQ; u++) {
-        const float4 v = __ldg(v4 + u);
+        const float4 v = vr[u];
         const float a = fmaf(x[u].x, qx[4 * u + 0], 1.0f), b = fmaf(x[u].y, qx[4 * u + 1], 1.0f);
         const float cc = fmaf(x[u].z, qx[4 * u + 2], 1.0f), d = fmaf(x[u].w, qx[4 * u + 3], 1.0f);
         const float dab = a * b, dcd = cc * d;
@@ -465,9 +465,12 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
         qx[k] = __expf(2.0f * q[k]);
     }
     const uint32_t slow = qok ? rawmask : 0xFFFFFFFFu;
+    float4 vr[NQ];   // this thread's att_v units, loaded once per step
+#pragma unroll
+    for (int u = 0; u < NQ; u++) vr[u] = __ldg(v4 + u);
     auto score = [&](const float4 (&x)[NQ], int j) {
         return ((slow >> j) & 1u) ? score_slow<NQ>(x, q, v4, (rawmask >> j) & 1u)
-                                  : vsum + score_fast<NQ>(x, qx, v4);
+                                  : vsum + score_fast<NQ>(x, qx, vr);
     };
     int j = 0;
     for (; j + 2 <= npos; j += 2) {
