@@ -76,6 +76,11 @@ constexpr float kLog2e = 1.4426950408889634f;
 __host__ __device__ __forceinline__ float gate_scale(int g) {
     return g == 2 ? 2.0f * kLog2e : -kLog2e;
 }
+__device__ __forceinline__ float ex2f(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float ex2_den(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -398,10 +403,10 @@ __device__ __forceinline__ void store_keys(float *Es, const Ctx<PARTS> &c, int j
     constexpr int U = Ctx<PARTS>::U;
     bool ok = true;
 #pragma unroll
-    for (int k = 0; k < U; k++) ok = ok && fabsf(2.0f * e[k]) <= kExpLim;
+    for (int k = 0; k < U; k++) ok = ok && fabsf(e[k]) <= 0.5f * kExpLim;   // |2e| <= kExpLim
     if (ok) {
 #pragma unroll
-        for (int k = 0; k < U; k++) e[k] = __expf(2.0f * e[k]);
+        for (int k = 0; k < U; k++) e[k] = ex2f(e[k] * (2.0f * kLog2e));   // = __expf(2e) bit for bit
     } else {
         rawmask |= 1u << j;
     }
@@ -461,8 +466,8 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
     bool qok = true;
 #pragma unroll
     for (int k = 0; k < U; k++) {
-        qok = qok && fabsf(2.0f * q[k]) <= kExpLim;
-        qx[k] = __expf(2.0f * q[k]);
+        qok = qok && fabsf(q[k]) <= 0.5f * kExpLim;
+        qx[k] = ex2f(q[k] * (2.0f * kLog2e));
     }
     const uint32_t slow = qok ? rawmask : 0xFFFFFFFFu;
     float4 vr[NQ];   // this thread's att_v units, loaded once per step
