@@ -564,15 +564,18 @@ __device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
     float v[U];
     readU(c, col, v);
     float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const float4 *cb4 = reinterpret_cast<const float4 *>(comb_b + U * c.part);
+    const float4 *hw4 = reinterpret_cast<const float4 *>(head_w + U * c.part);
 #pragma unroll
     for (int k = 0; k < U; k += 4) {
-        float d[4];
-#pragma unroll
-        for (int i = 0; i < 4; i++) d[i] = ex2_den(v[k + i] + __ldg(comb_b + U * c.part + k + i));
+        const float4 cb = __ldg(cb4 + k / 4), hw = __ldg(hw4 + k / 4);
+        float d[4] = {ex2_den(v[k] + cb.x), ex2_den(v[k + 1] + cb.y), ex2_den(v[k + 2] + cb.z),
+                      ex2_den(v[k + 3] + cb.w)};
         rcp4(d[0], d[1], d[2], d[3]);
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-            s[i] += fmaf(-2.0f, d[i], 1.0f) * __ldg(head_w + U * c.part + k + i);
+        s[0] += fmaf(-2.0f, d[0], 1.0f) * hw.x;
+        s[1] += fmaf(-2.0f, d[1], 1.0f) * hw.y;
+        s[2] += fmaf(-2.0f, d[2], 1.0f) * hw.z;
+        s[3] += fmaf(-2.0f, d[3], 1.0f) * hw.w;
     }
     return (s[0] + s[1]) + (s[2] + s[3]);
 }
