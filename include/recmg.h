@@ -51,7 +51,7 @@ enum { RECMG_POLICY_PRIORITY = 0, /* Alg. 1/2 priority-decay buffer (runtime.py:
        RECMG_POLICY_LRU = 1,      /* LRU comparator (cache_sim.py:92-106)              */
        RECMG_POLICY_LRU_PF = 2,   /* LRU + prefetch tags: replay_policy_only with a
                                      prefetcher (runtime.py:304-349); recmg_replay
-                                     ignores the bits; capacity <= 4096 ways      */
+                                     ignores the bits                             */
        RECMG_POLICY_LFU = 3,      /* cache_sim.py:109-137 (ties -> least recent)   */
        RECMG_POLICY_SRRIP = 4,    /* cache_sim.py:140-170; max rrpv in
                                      eviction_speed                                */
@@ -105,7 +105,7 @@ int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t
  *   pf[K*pf_stride]    prefetch gids per chunk, -1 padded (runtime.py:196-210);
  *                      NULL = no prefetcher
  *   counters           device recmg_counters, ACCUMULATED into (zero it first)
- *   cov_num, cov_den   device uint8[K] (nullable): |set(P_k) & set(W_k)| and
+ *   cov_num, cov_den   device uint16[K] (nullable): |set(P_k) & set(W_k)| and
  *                      |set(W_k)| so the host can form the float64 coverage in
  *                      chunk order (runtime.py:276,282) via recmg_coverage_mean
  *   access_class[n]    nullable: 0 cache hit, 1 prefetch hit, 2 on-demand
@@ -117,7 +117,7 @@ int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t
 int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                  int32_t l_in, int32_t l_out, int32_t window_ratio, const uint8_t *bits,
                  const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
-                 uint8_t *cov_num, uint8_t *cov_den, uint8_t *access_class, void *ws,
+                 uint16_t *cov_num, uint16_t *cov_den, uint8_t *access_class, void *ws,
                  size_t ws_bytes, void *stream);
 
 /* The same replay over chunks [k_begin, k_end) only (k_end = -1: all), with
@@ -128,21 +128,22 @@ int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
 int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                         int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
                         int64_t k_end, int32_t with_tail, const uint8_t *bits, const int32_t *pf,
-                        int32_t pf_stride, recmg_counters *counters, uint8_t *cov_num,
-                        uint8_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
+                        int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
+                        uint16_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
                         void *stream);
 
 /* Host: sequential float64 mean of num/den in chunk order (runtime.py:276,282). */
-double recmg_coverage_mean(const uint8_t *host_num, const uint8_t *host_den, int64_t K);
+double recmg_coverage_mean(const uint16_t *host_num, const uint16_t *host_den, int64_t K);
 /* Host: acc + the same left-to-right float64 sum over `count` chunks, for
  * summing the coverage piece by piece in chunk order as pieces complete.    */
-double recmg_coverage_accumulate(const uint8_t *host_num, const uint8_t *host_den, int64_t count,
+double recmg_coverage_accumulate(const uint16_t *host_num, const uint16_t *host_den, int64_t count,
                                  double acc);
 
 /* ---- policy-only simulation  (cache_sim.py:223-260, LRU) --------------- */
 int recmg_simulate_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, size_t *bytes);
 /* simulate(trace, CacheConfig(capacity, policy, ways)) for LRU, and for
- * LFU / SRRIP / OPTGEN with at most 4096 ways per set: hits/misses
+ * LFU / SRRIP / OPTGEN, any ways per set (sets wider than 4096 ways keep
+ * their ways in global memory, one CTA per set): hits/misses
  * accumulated into device int64[2]; per_access_hit[n] (nullable) as
  * SimResult.per_access_hit.  Use recmg_simulate_ex for OPTGEN keep bits.    */
 int recmg_simulate(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,

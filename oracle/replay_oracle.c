@@ -413,3 +413,32 @@ double oracle_coverage_sum(const uint8_t *num, const uint8_t *den, int64_t K)
     for (int64_t k = 0; k < K; k++) s += (double)num[k] / (double)den[k];
     return K ? s / (double)K : 0.0;
 }
+
+/* generate_trace's sequential pass  trace.py:144-160.  With probability
+ * `stickiness` the access reuses pool[floor(pool_coin * len)] (the pool holds
+ * the last `pool_size` distinct ids, most recent first), otherwise it takes
+ * the Zipf draw; the id then moves to the pool front (no-op when already
+ * there), the pool keeping at most pool_size entries.  `pool` / `len` carry
+ * the pool across consecutive blocks of one trace (start with *len = 0). */
+int oracle_pool_pass(const int64_t *zipf_gids, const double *sticky_coin,
+                     const double *pool_coin, int64_t n, double stickiness,
+                     int32_t pool_size, int64_t *pool, int32_t *len_io, int64_t *out)
+{
+    if (n < 0 || pool_size < 1 || !pool || !len_io) return -1;
+    int32_t len = *len_io;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t g = (len > 0 && sticky_coin[i] < stickiness)
+                        ? pool[(int64_t)(pool_coin[i] * (double)len)]
+                        : zipf_gids[i];
+        out[i] = g;
+        if (len > 0 && pool[0] == g) continue;
+        int32_t j = 0;
+        while (j < len && pool[j] != g) j++;
+        if (j == len && len < pool_size) len++;      /* new id: the pool grows   */
+        if (j == len) j = len - 1;                   /* full: the oldest drops   */
+        for (; j > 0; j--) pool[j] = pool[j - 1];    /* shift the front down     */
+        pool[0] = g;
+    }
+    *len_io = len;
+    return 0;
+}

@@ -10,12 +10,15 @@ from .cache_sim import CacheConfig, Policy, SimResult, simulate, simulate_optgen
 from .errors import (CheckpointError, EmbcacheError, InvalidConfigError,
                      MissingArtifactError, NumericalError, OutOfVocabularyError,
                      TraceParseError, TraceValidationError, VocabularyMismatchError)
+from .labeler import (LABEL_CAPACITY_FRACTION, LabeledDataset, caching_label_array,
+                      label_caching, label_prefetch, prefetch_target_array, split_dataset)
 from .model import (CACHING, PREFETCH, DeviceModel, ModelParameters, batch_arrays,
-                    decode_indices, forward_caching, forward_caching_batch, forward_prefetch,
-                    forward_prefetch_batch, init_params, normalize_gids)
+                    decode_indices, device_model, forward_caching, forward_caching_batch,
+                    forward_prefetch, forward_prefetch_batch, init_params,
+                    invalidate_device_models, normalize_gids)
 from .runtime import (EVICTION_SPEED, BreakdownReport, BufferConfig, PriorityBuffer,
                       correctness_vs_window, coverage, gpu_buffer_populate, load_embeddings,
-                      replay, replay_policy_only, write_breakdown_csv)
+                      optgen_miss_oracle, replay, replay_policy_only, write_breakdown_csv)
 from .trace import (EmbeddingIndex, SequenceSample, Trace, TraceGenConfig, chunk,
                     TraceStream, generate_trace, generate_trace_streamed, index_of_global,
                     make_index, num_chunks, read_trace, read_trace_binary, table_offsets,

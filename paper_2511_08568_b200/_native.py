@@ -203,8 +203,8 @@ def pool_pass(zipf_gids: np.ndarray, sticky: np.ndarray, pool_coin: np.ndarray,
 
 
 def coverage_mean(num: np.ndarray, den: np.ndarray) -> float:
-    num = np.ascontiguousarray(num, dtype=np.uint8)
-    den = np.ascontiguousarray(den, dtype=np.uint8)
+    num = np.ascontiguousarray(num, dtype=np.uint16)
+    den = np.ascontiguousarray(den, dtype=np.uint16)
     return float(lib().recmg_coverage_mean(num.ctypes.data, den.ctypes.data, len(num)))
 
 

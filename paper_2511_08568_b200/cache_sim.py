@@ -1,8 +1,9 @@
 """Cache simulators (cache_sim.py of the reference) on the GPU: LRU (the
 32-way comparator, K4), LFU, SRRIP and the offline optimum (optgen / Belady
 with keep decisions) as policies of the replay engine's shared-memory set
-kernel (set = gid % set_count, cache_sim.py:33-35).  LFU / SRRIP / OPTGEN
-support up to 4096 ways per set (fully associative: capacity <= 4096).
+kernel (set = gid % set_count, cache_sim.py:33-35), any capacity: sets of up
+to 4096 ways replay in shared memory, wider ones (fully associative at a
+realistic capacity) in global memory.
 """
 from __future__ import annotations
 

@@ -35,9 +35,8 @@ bool plan_replay(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in, int32_t l
     if (!geometry_of(cfg, &p.g)) return false;
     if (cfg->policy != RECMG_POLICY_PRIORITY && cfg->policy != RECMG_POLICY_LRU_PF) return false;
     if (cfg->policy == RECMG_POLICY_PRIORITY && cfg->eviction_speed < 1) return false;
-    if (cfg->policy == RECMG_POLICY_LRU_PF && p.g.W > kSmemMaxWays) return false;
     if (n < 0 || l_in < 1 || l_out < 1 || window_ratio < 1 || pf_stride < 0) return false;
-    if ((int64_t)window_ratio * l_out > 255) return false;  // uint8 coverage counts
+    if ((int64_t)window_ratio * l_out > 65535) return false;  // uint16 coverage counts
     p.K = recmg_num_chunks(n, l_in, l_out, window_ratio);
     if (k_begin < 0) k_begin = 0;
     if (k_end < 0 || k_end > p.K) k_end = p.K;
@@ -59,8 +58,8 @@ bool plan_replay(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in, int32_t l
 int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                  int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
                  int64_t k_end, int with_tail, const uint8_t *bits, const int32_t *pf,
-                 int32_t pf_stride, recmg_counters *counters, uint8_t *cov_num,
-                 uint8_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
+                 int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
+                 uint16_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
                  cudaStream_t s) {
     if (!pf) pf_stride = 0;
     Arena a{(char *)ws, ws_bytes, 0};
@@ -188,7 +187,7 @@ int recmg_replay_workspace_bytes(const recmg_buffer_cfg *cfg, int64_t n, int32_t
 int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                  int32_t l_in, int32_t l_out, int32_t window_ratio, const uint8_t *bits,
                  const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
-                 uint8_t *cov_num, uint8_t *cov_den, uint8_t *access_class, void *ws,
+                 uint16_t *cov_num, uint16_t *cov_den, uint8_t *access_class, void *ws,
                  size_t ws_bytes, void *stream) {
     return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, 0, -1, 1, bits, pf,
                         pf_stride, counters, cov_num, cov_den, access_class, ws, ws_bytes,
@@ -198,15 +197,15 @@ int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
 int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                         int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
                         int64_t k_end, int32_t with_tail, const uint8_t *bits, const int32_t *pf,
-                        int32_t pf_stride, recmg_counters *counters, uint8_t *cov_num,
-                        uint8_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
+                        int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
+                        uint16_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
                         void *stream) {
     return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, k_begin, k_end,
                         with_tail, bits, pf, pf_stride, counters, cov_num, cov_den,
                         access_class, ws, ws_bytes, as_stream(stream));
 }
 
-double recmg_coverage_mean(const uint8_t *num, const uint8_t *den, int64_t K) {
+double recmg_coverage_mean(const uint16_t *num, const uint16_t *den, int64_t K) {
     // runtime.py:276 accumulates len(P & W)/len(W) left to right in float64,
     // runtime.py:282 divides by the chunk count.
     double acc = 0.0;
@@ -214,7 +213,7 @@ double recmg_coverage_mean(const uint8_t *num, const uint8_t *den, int64_t K) {
     return K ? acc / (double)K : 0.0;
 }
 
-double recmg_coverage_accumulate(const uint8_t *num, const uint8_t *den, int64_t count,
+double recmg_coverage_accumulate(const uint16_t *num, const uint16_t *den, int64_t count,
                                  double acc) {
     for (int64_t k = 0; k < count; k++) acc += (double)num[k] / (double)den[k];
     return acc;
@@ -222,10 +221,10 @@ double recmg_coverage_accumulate(const uint8_t *num, const uint8_t *den, int64_t
 
 static bool sim_policy_ok(const recmg_buffer_cfg *cfg, const Geometry &g) {
     switch (cfg->policy) {
-        case RECMG_POLICY_LRU: return true;
+        case RECMG_POLICY_LRU:
         case RECMG_POLICY_LFU:
-        case RECMG_POLICY_OPTGEN: return g.W <= kSmemMaxWays;
-        case RECMG_POLICY_SRRIP: return g.W <= kSmemMaxWays && cfg->eviction_speed >= 0;
+        case RECMG_POLICY_OPTGEN: return true;
+        case RECMG_POLICY_SRRIP: return cfg->eviction_speed >= 0;
         default: return false;
     }
 }

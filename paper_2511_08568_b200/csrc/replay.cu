@@ -10,14 +10,15 @@
 //   EVICT = victim argmin (priority, gid); every resident p>0 ages by one
 //           (populate, runtime.py:100-112), applied per set.
 //
-// Narrow sets (W <= 32): one warp per set, way w in lane w (registers).  The
-// warp consumes its event segment 32 events at a time: membership of all 32
-// events against the 32 tags in one pass, then every event before the first
-// residency-changing miss is applied in bulk (hits never change residency,
-// so this is exactly the sequential order), then that one miss is resolved.
-// Wide sets (W > 32, incl. the reference's fully associative buffer): one
-// warp per set, ways in global memory (L1/L2 resident), an id->slot map for
-// lookups, and the same 32-event batching with __match_any_sync grouping.
+// Sets of up to kSmemMaxWays (4096) ways: one warp per set, the set's ways
+// and a gid -> way hash index in shared memory (replay_smem_kernel).  The warp
+// consumes its event segment 64 events at a time: membership of every event,
+// then every event before the first residency-changing miss is applied in
+// bulk (hits never change residency, so this is exactly the sequential
+// order), then that one miss is resolved.  Wider sets (the reference's fully
+// associative buffer at a realistic capacity): one CTA per set, ways in
+// global memory, an id -> slot map, the same batching by warp 0 and the
+// victim scan by the whole CTA (replay_wide_kernel).
 #include "replay.cuh"
 
 namespace recmg {
@@ -127,8 +128,8 @@ __device__ __forceinline__ int64_t access_of_event(int64_t pos, int64_t Ec, int6
 // prefetch statistics, one thread per chunk  (runtime.py:272-276)
 __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t k0, int64_t nk,
                                       int32_t l_in, int32_t l_win, const int32_t *__restrict__ pf,
-                                      int32_t pf_stride, uint8_t *__restrict__ cov_num,
-                                      uint8_t *__restrict__ cov_den,
+                                      int32_t pf_stride, uint16_t *__restrict__ cov_num,
+                                      uint16_t *__restrict__ cov_den,
                                       recmg_counters *__restrict__ ctr) {
     const int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t K = k0 + nk;
@@ -157,8 +158,8 @@ __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t 
                 num += (in && !dup);
             }
         }
-        if (cov_num) cov_num[k] = (uint8_t)num;
-        if (cov_den) cov_den[k] = (uint8_t)den;
+        if (cov_num) cov_num[k] = (uint16_t)num;
+        if (cov_den) cov_den[k] = (uint16_t)den;
     }
     issued = __reduce_add_sync(0xFFFFFFFFu, (unsigned)issued);
     useful = __reduce_add_sync(0xFFFFFFFFu, (unsigned)useful);
@@ -280,6 +281,18 @@ struct EventRing {
 // residency-changing miss, __match_any_sync groups the hit-run by way and the
 // group leader applies the run's effect on its way (S: tag clear / hit
 // class, U/P: last write wins), then the miss is resolved serially.
+// LFU way metadata: the reference count (saturating at 2^27 - 1 -- only a
+// block hit that often in ONE residency could tie wrongly) above the clock of
+// the last use (36 bits, 6.9e10 events); victim = min (count, clock), i.e.
+// least recently used among the least frequently used (cache_sim.py:109-137).
+constexpr int kLfuShift = 36;
+constexpr int64_t kLfuCountMax = (int64_t(1) << 27) - 1;
+__device__ __forceinline__ int64_t lfu_meta(int64_t m, int64_t add, int64_t clk) {
+    int64_t c = (m >> kLfuShift) + add;
+    c = c > kLfuCountMax ? kLfuCountMax : c;
+    return (c << kLfuShift) | (clk & ((int64_t(1) << kLfuShift) - 1));
+}
+
 constexpr uint64_t kHtEmpty = ~0ull;
 
 struct SetView {
@@ -384,7 +397,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
     constexpr int64_t kClockMask = (int64_t(1) << 62) - 1;
     // simulate() policies (cache_sim.py:92-249), serve events only:
     //   LRU    meta = clock of the last use                victim min clock
-    //   LFU    meta = freq << 40 | clock of the last use   victim min (freq, clock)
+    //   LFU    meta = lfu_meta(count, clock of the last use)  victim min (count, clock)
     //   SRRIP  meta = rrpv                                 victim first way with
     //          rrpv >= max after aging (max_rrpv in a.es)
     //   OPTGEN meta = next use of the last access          victim max next use,
@@ -458,7 +471,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 nu = a.next_use[a.vals ? a.vals[base + lane] : base + lane];
             if (inrun && lane == leader) {
                 const int64_t clk = clock_base + base + leader;
-                if (LFU) v.meta[way] = (((v.meta[way] >> 40) + __popc(peers)) << 40) | clk;
+                if (LFU) v.meta[way] = lfu_meta(v.meta[way], __popc(peers), clk);
                 else if (SRRIP) v.meta[way] = 0;
                 else if (OPT) v.meta[way] = nu;
                 else v.meta[way] = clk;
@@ -562,7 +575,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                     if (lane == 0) {
                         const int last = nf - 1;
                         const int64_t clk = clock_base + pos + last;
-                        if (LFU) v.meta[way] = (((v.meta[way] >> 40) + nf) << 40) | clk;
+                        if (LFU) v.meta[way] = lfu_meta(v.meta[way], nf, clk);
                         else if (SRRIP) v.meta[way] = 0;
                         else if (OPT) v.meta[way] = a.next_use[a.vals ? a.vals[pos + last] : pos + last];
                         else v.meta[way] = clk;
@@ -712,7 +725,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 v.tags[target] = (int32_t)gc;
                 int64_t m;
                 if (PRIO) m = (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
-                else if (LFU) m = (int64_t(1) << 40) | (clock_base + pos + cut);
+                else if (LFU) m = lfu_meta(0, 1, clock_base + pos + cut);
                 else if (SRRIP) m = a.es > 1 ? a.es - 1 : 0;
                 else if (OPT) m = a.next_use[a.vals ? a.vals[pos + cut] : pos + cut];
                 else m = (clock_base + pos + cut) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0);
@@ -747,172 +760,278 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
 }
 
 // ---------------------------------------------------------------------------
-// Wide sets: one warp per set, W > kSmemMaxWays ways in global memory.
+// Wide sets (W > kSmemMaxWays, e.g. the reference's fully associative buffer
+// at a realistic capacity): one CTA per set, ways in global memory and an
+// id -> slot map for membership.  Warp 0 consumes the event segment 32 events
+// at a time exactly as the shared-memory kernel does (membership, cut at the
+// first residency-changing miss, the hit-run grouped by slot and applied by
+// the group's last lane, the miss resolved); a miss into a full set hands
+// the victim search -- an O(W) scan of the set's ways, plus the decay of
+// populate() / the SRRIP ageing -- to the whole CTA, then warp 0 inserts.
+// Every policy of the engine: PRIORITY (runtime.py:100-112), LRU_PF
+// (runtime.py:318-339), LRU / LFU / SRRIP / OPTGEN (cache_sim.py:92-249).
+constexpr int kWideThreads = 512;
+
 template <int POLICY, bool CLASS>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(kWideThreads)
 replay_wide_kernel(ReplayArgs a) {
+    constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
+    constexpr bool LRUPF = (POLICY == RECMG_POLICY_LRU_PF);
+    constexpr bool LFU = (POLICY == RECMG_POLICY_LFU);
+    constexpr bool SRRIP = (POLICY == RECMG_POLICY_SRRIP);
+    constexpr bool OPT = (POLICY == RECMG_POLICY_OPTGEN);
+    constexpr int64_t kClockMask = (int64_t(1) << 62) - 1;
+    constexpr int kWarps = kWideThreads / 32;
     const unsigned FULL = 0xFFFFFFFFu;
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t set = blockIdx.x;
     const int64_t W = a.W;
     int32_t *tags = a.st.tags + set * W;
     int64_t *meta = a.st.meta + set * W;
     int32_t *slot_of = a.st.slot_of;
-    int32_t count = a.st.count[set];
     const int64_t clock_base = a.st.header[0];
     int64_t lo, hi;
     seg_range(a, set, lo, hi);
+
+    __shared__ __align__(16) uint32_t ring_buf[kRingSlots * kRingBlk];
+    __shared__ unsigned long long s_key[kWarps];
+    __shared__ int64_t s_slot[kWarps];
+    __shared__ int64_t s_victim, s_dlt;
+    __shared__ int s_cmd;
+
+    // warp 0's replay state
+    int32_t count = a.st.count[set];
     unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
     const unsigned lt = (1u << lane) - 1u;
     int64_t free_hint = 0;
-
-    __shared__ __align__(16) uint32_t ring_buf[kRingSlots * kRingBlk];
+    int64_t pos = lo;
+    uint32_t pend_e = 0;     // the miss waiting for a victim, at event pos + pend_cut
+    int pend_cut = 0;
     EventRing ring;
-    ring.init(ring_buf, a.ev + lo, hi - lo, lane);
-    for (int64_t pos = lo; pos < hi;) {
-        const int nb = (int)imin64(32, hi - pos);
-        const bool valid = lane < nb;
-        ring.ensure(pos - lo, nb);
-        const uint32_t e = valid ? ring.at(pos - lo + lane) : 0u;
-        const int32_t g = (int32_t)ev_gid(e);
-        const uint32_t ty = ev_type(e);
-        const bool real = valid && (uint32_t)g != kGidMask;
-        const int32_t slot = real ? slot_of[g] : -1;
-        const bool member = slot >= 0;
-        unsigned missmask;
-        if (POLICY == RECMG_POLICY_PRIORITY)
-            missmask = __ballot_sync(FULL, real && !member && (ty == EV_SERVE || ty == EV_PREFETCH));
-        else
-            missmask = __ballot_sync(FULL, real && !member);
-        const int cut = missmask ? (__ffs(missmask) - 1) : nb;
-        const bool inrun = member && lane < cut;
-        // group the run's events by slot
-        const unsigned peers = __match_any_sync(FULL, inrun ? (unsigned)slot : (0x80000000u | lane));
-        const int owner = 31 - __clz(peers);
-        if (POLICY == RECMG_POLICY_PRIORITY) {
-            const unsigned Smask = __ballot_sync(FULL, inrun && ty == EV_SERVE);
-            const unsigned UPmask = __ballot_sync(FULL, inrun && ty != EV_SERVE);
-            const unsigned U1mask = __ballot_sync(FULL, inrun && ty == EV_UPD1);
-            int64_t m0 = 0;
-            bool flag0 = false;
-            if (inrun && lane == owner) {
-                m0 = meta[slot];
-                flag0 = (m0 >> 32) & 1;
-                const unsigned sp = peers & Smask, up = peers & UPmask;
-                int32_t p = (int32_t)(m0 & 0xFFFFFFFF);
-                bool f = flag0;
-                if (sp) {
-                    const unsigned c = __popc(sp);
-                    if (f) { ph += 1; ch += c - 1; f = false; }
-                    else ch += c;
-                }
-                if (up) {
-                    const int last = 31 - __clz(up);
-                    p = a.es + (((U1mask >> last) & 1u) ? 1 : 0);
-                }
-                if (sp || up) meta[slot] = (int64_t)(uint32_t)p | ((int64_t)f << 32);
-            }
-            if (CLASS) {
-                const bool f0 = __shfl_sync(FULL, flag0, owner);
-                if (inrun && ty == EV_SERVE) {
-                    const bool first = ((peers & Smask) & lt) == 0;
-                    write_class(a, pos + lane, (f0 && first) ? 1 : 0);
-                }
-            }
-        } else {
-            if (inrun && lane == owner) {
-                meta[slot] = clock_base + pos + owner;
-                lhits += __popc(peers);
-            }
-            if (a.per_access_hit && lane < cut)
-                a.per_access_hit[a.vals ? a.vals[pos + lane] : pos + lane] = 1;
-        }
-        __syncwarp();
+    if (warp == 0) ring.init(ring_buf, a.ev + lo, hi - lo, lane);
 
-        if (cut < nb) {
-            const uint32_t ec = __shfl_sync(FULL, e, cut);
-            const int32_t gc = (int32_t)ev_gid(ec);
-            const uint32_t tc = ev_type(ec);
-            if (POLICY == RECMG_POLICY_PRIORITY) {
-                if (tc == EV_SERVE) {
-                    od++;
-                    if (CLASS && lane == 0) write_class(a, pos + cut, 2);
-                } else {
-                    ins++;
-                }
-            } else {
-                od++;
-                if (a.per_access_hit && lane == 0)
-                    a.per_access_hit[a.vals ? a.vals[pos + cut] : pos + cut] = 0;
-            }
-            int64_t target = -1;
-            if (count >= W) {
-                // victim: min (priority, gid) [priority policy] or min clock [LRU]
-                unsigned long long best = ~0ull;
-                int64_t bslot = -1;
-                for (int64_t w = lane; w < W; w += 32) {
-                    const int32_t t = tags[w];
-                    if (t < 0) continue;
-                    const int64_t m = meta[w];
-                    unsigned long long key;
-                    if (POLICY == RECMG_POLICY_PRIORITY)
-                        key = ((unsigned long long)(uint32_t)m << 32) | (uint32_t)t;
-                    else
-                        key = (unsigned long long)m;
-                    if (key < best) { best = key; bslot = w; }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
-                    const int64_t os = __shfl_xor_sync(FULL, bslot, o);
-                    if (ob < best) { best = ob; bslot = os; }
-                }
-                if (POLICY == RECMG_POLICY_PRIORITY) {
-                    for (int64_t w = lane; w < W; w += 32) {
-                        if (tags[w] < 0) continue;
-                        const int64_t m = meta[w];
-                        if ((int32_t)(m & 0xFFFFFFFF) > 0) meta[w] = m - 1;
+    auto access_at = [&](int64_t p) -> int64_t { return a.vals ? (int64_t)a.vals[p] : p; };
+    auto insert_meta = [&](uint32_t tc, int64_t p) -> int64_t {
+        if (PRIO) return (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
+        if (LFU) return lfu_meta(0, 1, clock_base + p);
+        if (SRRIP) return a.es > 1 ? a.es - 1 : 0;
+        if (OPT) return a.next_use[access_at(p)];
+        return (clock_base + p) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0);
+    };
+
+    while (true) {
+        if (warp == 0) {
+            int cmd = 0;
+            while (pos < hi) {
+                const int nb = (int)imin64(32, hi - pos);
+                const bool valid = lane < nb;
+                ring.ensure(pos - lo, nb);
+                const uint32_t e = valid ? ring.at(pos - lo + lane) : 0u;
+                const int32_t g = (int32_t)ev_gid(e);
+                const uint32_t ty = ev_type(e);
+                bool real = valid && (uint32_t)g != kGidMask;
+                if (LRUPF) real = real && (ty == EV_SERVE || ty == EV_PREFETCH);
+                const int32_t slot = real ? slot_of[g] : -1;
+                const bool member = slot >= 0;
+                unsigned missmask;
+                if (PRIO || LRUPF)
+                    missmask = __ballot_sync(FULL, real && !member && (ty == EV_SERVE || ty == EV_PREFETCH));
+                else
+                    missmask = __ballot_sync(FULL, real && !member);
+                const int cut = missmask ? (__ffs(missmask) - 1) : nb;
+                const bool inrun = member && lane < cut;
+                const unsigned peers = __match_any_sync(FULL, inrun ? (unsigned)slot : (0x80000000u | lane));
+                const int owner = 31 - __clz(peers);
+                if (PRIO) {
+                    const unsigned Smask = __ballot_sync(FULL, inrun && ty == EV_SERVE);
+                    const unsigned UPmask = __ballot_sync(FULL, inrun && ty != EV_SERVE);
+                    const unsigned U1mask = __ballot_sync(FULL, inrun && ty == EV_UPD1);
+                    bool flag0 = false;
+                    if (inrun && lane == owner) {
+                        const int64_t m0 = meta[slot];
+                        flag0 = (m0 >> 32) & 1;
+                        const unsigned sp = peers & Smask, up = peers & UPmask;
+                        int32_t p = (int32_t)(m0 & 0xFFFFFFFF);
+                        bool f = flag0;
+                        if (sp) {
+                            const unsigned c = __popc(sp);
+                            if (f) { ph += 1; ch += c - 1; f = false; }
+                            else ch += c;
+                        }
+                        if (up) {
+                            const int last = 31 - __clz(up);
+                            p = a.es + (((U1mask >> last) & 1u) ? 1 : 0);
+                        }
+                        if (sp || up) meta[slot] = (int64_t)(uint32_t)p | ((int64_t)f << 32);
                     }
+                    if (CLASS) {
+                        const bool f0 = __shfl_sync(FULL, flag0, owner);
+                        if (inrun && ty == EV_SERVE) {
+                            const bool first = ((peers & Smask) & lt) == 0;
+                            write_class(a, pos + lane, (f0 && first) ? 1 : 0);
+                        }
+                    }
+                } else if (LRUPF) {
+                    const unsigned Smask = __ballot_sync(FULL, inrun && ty == EV_SERVE);
+                    bool flag0 = false;
+                    if (inrun && lane == owner) {
+                        const unsigned sp = peers & Smask;
+                        if (sp) {
+                            const int64_t m0 = meta[slot];
+                            flag0 = (m0 >> 62) & 1;
+                            const unsigned c = __popc(sp);
+                            if (flag0) { ph += 1; ch += c - 1; }
+                            else ch += c;
+                            meta[slot] = clock_base + pos + (31 - __clz(sp));
+                        }
+                    }
+                    if (CLASS) {
+                        const bool f0 = __shfl_sync(FULL, flag0, owner);
+                        if (inrun && ty == EV_SERVE) {
+                            const bool first = ((peers & Smask) & lt) == 0;
+                            write_class(a, pos + lane, (f0 && first) ? 1 : 0);
+                        }
+                    }
+                } else {
+                    if (inrun && lane == owner) {
+                        const int64_t clk = clock_base + pos + owner;
+                        if (LFU) meta[slot] = lfu_meta(meta[slot], __popc(peers), clk);
+                        else if (SRRIP) meta[slot] = 0;
+                        else if (OPT) meta[slot] = a.next_use[access_at(pos + owner)];
+                        else meta[slot] = clk;
+                        lhits += __popc(peers);
+                    }
+                    if (a.per_access_hit && lane < cut) a.per_access_hit[access_at(pos + lane)] = 1;
                 }
                 __syncwarp();
-                if (lane == 0) {
-                    slot_of[tags[bslot]] = -1;
-                    tags[bslot] = -1;
+                if (cut == nb) {
+                    pos += nb;
+                    continue;
                 }
-                count--;
-                nev++;
-                target = bslot;
-            } else {
+                const uint32_t ec = __shfl_sync(FULL, e, cut);
+                const int32_t gc = (int32_t)ev_gid(ec);
+                const uint32_t tc = ev_type(ec);
+                if (PRIO || LRUPF) {
+                    if (tc == EV_SERVE) {
+                        od++;
+                        if (CLASS && lane == 0) write_class(a, pos + cut, 2);
+                    } else {
+                        ins++;
+                    }
+                } else {
+                    od++;
+                    if (a.per_access_hit && lane == 0) a.per_access_hit[access_at(pos + cut)] = 0;
+                }
+                if (count >= W) {          // the CTA finds the victim
+                    pend_e = ec;
+                    pend_cut = cut;
+                    cmd = 1;
+                    break;
+                }
                 // first free slot at or after the hint (slots below it are
                 // occupied: inside a launch a slot is only freed by an
-                // eviction, which the same miss refills immediately)
+                // eviction, which the same miss refills at once)
                 int64_t found = -1;
-                for (int64_t base = free_hint; base < W && found < 0; base += 32) {
-                    const int64_t w = base + lane;
+                for (int64_t b = free_hint; b < W && found < 0; b += 32) {
+                    const int64_t w = b + lane;
                     const unsigned fm = __ballot_sync(FULL, w < W && tags[w] < 0);
-                    if (fm) found = base + __ffs(fm) - 1;
+                    if (fm) found = b + __ffs(fm) - 1;
                 }
-                target = found;
                 free_hint = found + 1;
+                if (lane == 0) {
+                    tags[found] = gc;
+                    meta[found] = insert_meta(tc, pos + cut);
+                    slot_of[gc] = (int32_t)found;
+                }
+                count++;
+                __syncwarp();
+                pos += cut + 1;
             }
-            __syncwarp();
+            if (lane == 0) s_cmd = cmd;
+        }
+        __syncthreads();
+        if (s_cmd == 0) break;
+
+        // ---- victim search over the W ways, the whole CTA ------------------
+        int64_t dlt = 0;
+        if (SRRIP) {
+            // age until some way reaches max (cache_sim.py:158-165): by max - top
+            int64_t mx = 0;
+            for (int64_t w = tid; w < W; w += kWideThreads)
+                if (tags[w] >= 0) mx = meta[w] > mx ? meta[w] : mx;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const int64_t om = __shfl_xor_sync(FULL, mx, o);
+                mx = om > mx ? om : mx;
+            }
+            if (lane == 0) s_slot[warp] = mx;
+            __syncthreads();
+            if (tid == 0) {
+                int64_t m = 0;
+                for (int i = 0; i < kWarps; i++) m = s_slot[i] > m ? s_slot[i] : m;
+                s_dlt = (int64_t)a.es - m;
+            }
+            __syncthreads();
+            dlt = s_dlt;
+        }
+        unsigned long long best = ~0ull;
+        int64_t bslot = -1;
+        for (int64_t w = tid; w < W; w += kWideThreads) {
+            const int32_t t = tags[w];
+            if (t < 0) continue;
+            const int64_t m = meta[w];
+            unsigned long long key;
+            if (PRIO) key = ((unsigned long long)(uint32_t)m << 32) | (uint32_t)t;
+            else if (OPT) key = ((unsigned long long)((int64_t(1) << 31) - m) << 32) | (uint32_t)t;
+            else if (SRRIP) {
+                const int64_t r = m + (dlt > 0 ? dlt : 0);
+                if (dlt > 0) meta[w] = r;
+                key = r >= a.es ? (unsigned long long)w : ~0ull;   // first such way
+            } else if (LFU) key = (unsigned long long)m;
+            else key = (unsigned long long)(m & kClockMask);
+            if (key < best) { best = key; bslot = w; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+            const int64_t os = __shfl_xor_sync(FULL, bslot, o);
+            if (ob < best) { best = ob; bslot = os; }
+        }
+        if (lane == 0) { s_key[warp] = best; s_slot[warp] = bslot; }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long b = s_key[0];
+            int64_t bs = s_slot[0];
+            for (int i = 1; i < kWarps; i++)
+                if (s_key[i] < b) { b = s_key[i]; bs = s_slot[i]; }
+            s_victim = bs;
+        }
+        if (PRIO) {
+            // populate(): every resident with p > 0 ages by one (runtime.py:107-108)
+            for (int64_t w = tid; w < W; w += kWideThreads) {
+                if (tags[w] < 0) continue;
+                const int64_t m = meta[w];
+                if ((int32_t)(m & 0xFFFFFFFF) > 0) meta[w] = m - 1;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int64_t v = s_victim;
             if (lane == 0) {
-                tags[target] = gc;
-                if (POLICY == RECMG_POLICY_PRIORITY)
-                    meta[target] = (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
-                else
-                    meta[target] = clock_base + pos + cut;
-                slot_of[gc] = (int32_t)target;
+                const int32_t gc = (int32_t)ev_gid(pend_e);
+                slot_of[tags[v]] = -1;
+                tags[v] = gc;
+                meta[v] = insert_meta(ev_type(pend_e), pos + pend_cut);
+                slot_of[gc] = (int32_t)v;
             }
-            count++;
+            nev++;
             __syncwarp();
-            pos += cut + 1;
-        } else {
-            pos += nb;
+            pos += pend_cut + 1;
         }
     }
+    if (warp != 0) return;
     if (lane == 0) a.st.count[set] = count;
-    if (POLICY == RECMG_POLICY_PRIORITY) {
+    if (PRIO || LRUPF) {
         ch = __reduce_add_sync(FULL, (unsigned)ch);
         ph = __reduce_add_sync(FULL, (unsigned)ph);
         if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
@@ -1085,14 +1204,24 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         }
 #undef RECMG_SMEM_LAUNCH
     } else {
-        if (policy != RECMG_POLICY_PRIORITY && policy != RECMG_POLICY_LRU)
-            return RECMG_E_INVALID_CONFIG;   // the other policies: <= 4096 ways per set
+#define RECMG_WIDE_LAUNCH(P, C) \
+    replay_wide_kernel<P, C><<<(unsigned)nsets, kWideThreads, 0, s>>>(a)
         if (policy == RECMG_POLICY_PRIORITY) {
-            if (cls) replay_wide_kernel<RECMG_POLICY_PRIORITY, true><<<(unsigned)nsets, 32, 0, s>>>(a);
-            else replay_wide_kernel<RECMG_POLICY_PRIORITY, false><<<(unsigned)nsets, 32, 0, s>>>(a);
+            if (cls) RECMG_WIDE_LAUNCH(RECMG_POLICY_PRIORITY, true);
+            else RECMG_WIDE_LAUNCH(RECMG_POLICY_PRIORITY, false);
+        } else if (policy == RECMG_POLICY_LRU_PF) {
+            if (cls) RECMG_WIDE_LAUNCH(RECMG_POLICY_LRU_PF, true);
+            else RECMG_WIDE_LAUNCH(RECMG_POLICY_LRU_PF, false);
+        } else if (policy == RECMG_POLICY_LFU) {
+            RECMG_WIDE_LAUNCH(RECMG_POLICY_LFU, false);
+        } else if (policy == RECMG_POLICY_SRRIP) {
+            RECMG_WIDE_LAUNCH(RECMG_POLICY_SRRIP, false);
+        } else if (policy == RECMG_POLICY_OPTGEN) {
+            RECMG_WIDE_LAUNCH(RECMG_POLICY_OPTGEN, false);
         } else {
-            replay_wide_kernel<RECMG_POLICY_LRU, false><<<(unsigned)nsets, 32, 0, s>>>(a);
+            RECMG_WIDE_LAUNCH(RECMG_POLICY_LRU, false);
         }
+#undef RECMG_WIDE_LAUNCH
     }
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;

@@ -16,8 +16,8 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
                                     uint8_t *__restrict__ access_class);
 __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t k0, int64_t nk,
                                       int32_t l_in, int32_t l_win, const int32_t *__restrict__ pf,
-                                      int32_t pf_stride, uint8_t *__restrict__ cov_num,
-                                      uint8_t *__restrict__ cov_den,
+                                      int32_t pf_stride, uint16_t *__restrict__ cov_num,
+                                      uint16_t *__restrict__ cov_den,
                                       recmg_counters *__restrict__ ctr);
 __global__ void state_reset_kernel(StateView st, int64_t SW, int64_t S, int64_t V);
 __global__ void clock_bump_kernel(int64_t *header, int64_t by);

@@ -48,7 +48,7 @@ class BufferReplay:
             ctypes.byref(sz)), "replay_workspace_bytes")
         self._ws = _native.device_bytes(self.torch, sz.value)
         K = num_chunks(key[0], self.l_in, self.l_out, self.window_ratio)
-        self._cov = self.torch.empty((2, max(K, 1)), dtype=self.torch.uint8, device="cuda")
+        self._cov = self.torch.empty((2, max(K, 1)), dtype=self.torch.int16, device="cuda")
         self._ws_key = key
 
     def reset(self):
@@ -85,8 +85,8 @@ class BufferReplay:
             self._ws.numel(), _native.stream_handle(self.torch)), "replay_chunks")
 
     def cov_host(self):
-        """(num, den) uint8 arrays of the last run, copied to the host."""
-        c = self._cov[:, :self.K].cpu().numpy()
+        """(num, den) uint16 arrays of the last run, copied to the host."""
+        c = self._cov[:, :self.K].cpu().numpy().view(np.uint16)
         return c[0], c[1]
 
     def result(self, with_coverage=True):
@@ -105,7 +105,7 @@ class BufferReplay:
 
 class SetSim:
     """recmg_simulate_ex: LRU / LFU / SRRIP / OPTGEN over set = gid % S
-    (cache_sim.py:92-249); LRU for any ways, the others up to 4096 ways."""
+    (cache_sim.py:92-249), any ways per set."""
 
     POLICIES = {"lru": _native.POLICY_LRU, "lfu": _native.POLICY_LFU,
                 "srrip": _native.POLICY_SRRIP, "optgen": _native.POLICY_OPTGEN}

@@ -92,7 +92,7 @@ class HotPath:
         prio = torch.cuda.Stream.priority_range()[1] if replay_priority else 0
         self.s_replay = torch.cuda.Stream(priority=prio)
         self.s_copy = torch.cuda.Stream()
-        self.cov_host = torch.empty((2, max(self.K_max, 1)), dtype=torch.uint8, pin_memory=True)
+        self.cov_host = torch.empty((2, max(self.K_max, 1)), dtype=torch.int16, pin_memory=True)
         self._cov_events = []
         self.s_lru = torch.cuda.Stream(priority=prio)
         self.events = None
@@ -250,10 +250,10 @@ class HotPath:
             L = _native.lib()
             acc = 0.0
             base = self.cov_host.data_ptr()
-            stride = self.cov_host.stride(0)
+            stride = self.cov_host.stride(0) * 2
             for k0, k1, e in self._cov_events:
                 e.synchronize()
-                acc = L.recmg_coverage_accumulate(base + k0, base + stride + k0, k1 - k0, acc)
+                acc = L.recmg_coverage_accumulate(base + 2 * k0, base + stride + 2 * k0, k1 - k0, acc)
             cov = acc / self.K if self.K else 0.0
         r = self.buffer.result(with_coverage=cov is None)
         if cov is not None:
@@ -276,4 +276,4 @@ class HotPath:
 
     def d2h_bytes(self):
         """Bytes read back per replay_host: counters, LRU pair, coverage num/den."""
-        return 8 * 8 + (16 if self.lru is not None else 0) + 2 * self.K
+        return 8 * 8 + (16 if self.lru is not None else 0) + 2 * 2 * self.K

@@ -20,7 +20,7 @@ from . import _native
 from .cache_sim import CacheConfig, Policy, simulate
 from .engine import BufferReplay, LruSim, to_device_gids
 from .errors import InvalidConfigError, VocabularyMismatchError
-from .model import CACHING, PREFETCH, DeviceModel, ModelParameters
+from .model import CACHING, PREFETCH, ModelParameters, device_model
 from .trace import chunk, num_chunks
 
 EVICTION_SPEED = 4
@@ -200,10 +200,12 @@ def _check_vocab(params: ModelParameters | None, trace):
 
 
 def _gpu_bits(torch, params, gids_dev, K, l_in, dm=None):
-    """_model_bits (runtime.py:181-193) on the GPU: bits = logit >= 0."""
+    """_model_bits (runtime.py:181-193) on the GPU: bits = logit >= 0.  The
+    model runs over the replay's chunk length l_in (the reference's forwards
+    take any length)."""
     if K == 0:
         return None
-    dm = dm or DeviceModel(params)
+    dm = dm or device_model(params, l_in)
     g = gids_dev[:K * l_in].view(K, l_in)
     t = dm.table_ids(g)
     bits = torch.empty((K, l_in), dtype=torch.uint8, device="cuda")
@@ -212,10 +214,12 @@ def _gpu_bits(torch, params, gids_dev, K, l_in, dm=None):
 
 
 def _gpu_prefetches(torch, params, gids_dev, K, l_in, dm=None):
-    """_model_prefetches (runtime.py:196-210) on the GPU, decode in fp64."""
+    """_model_prefetches (runtime.py:196-210) on the GPU, decode in fp64.  The
+    model reads l_in accesses and always emits its own params.l_out ids
+    (model.py:199-212), whatever the replay's l_out (window length)."""
     if K == 0:
         return None
-    dm = dm or DeviceModel(params)
+    dm = dm or device_model(params, l_in)
     g = gids_dev[:K * l_in].view(K, l_in)
     t = dm.table_ids(g)
     pf = torch.empty((K, params.l_out), dtype=torch.int32, device="cuda")
@@ -325,10 +329,7 @@ def replay_policy_only(trace, cache_cfg: CacheConfig, prefetch_params=None, pref
     if prefetch_fn is not None:
         pf = torch.from_numpy(hpf).cuda() if hpf is not None else None
     else:
-        p = prefetch_params
-        if p.l_in != l_in or p.l_out != l_out:
-            p = ModelParameters(p.kind, p.table_sizes, p.dim, p.stacks, l_in, l_out, p.arrays)
-        pf = _gpu_prefetches(torch, p, gdev, K, l_in)
+        pf = _gpu_prefetches(torch, prefetch_params, gdev, K, l_in)
     eng = BufferReplay(cache_cfg.capacity, trace.total_ids, 1, None, n, l_in, l_out,
                        window_ratio, pf.shape[1] if pf is not None else 0,
                        policy=_native.POLICY_LRU_PF)
@@ -337,6 +338,26 @@ def replay_policy_only(trace, cache_cfg: CacheConfig, prefetch_params=None, pref
     return BreakdownReport(r["cache_hits"], r["prefetch_hits"], r["on_demand"],
                            r["prefetch_issued"], r["prefetch_useful"], r["coverage"],
                            r["evictions"], r["prefetch_inserts"])
+
+
+def optgen_miss_oracle(trace, gpu_capacity: int, l_out: int = 5):
+    """runtime.py:352-366: a prefetch_fn emitting each window's first l_out
+    misses of the offline-optimal cache at the labeling capacity
+    (floor(0.8 * gpu_capacity), labeler.py:17,30-37); the optimum runs on the
+    GPU (simulate_optgen)."""
+    import math
+    from .cache_sim import simulate_optgen
+    from .labeler import LABEL_CAPACITY_FRACTION
+    cap = max(1, math.floor(LABEL_CAPACITY_FRACTION * gpu_capacity))
+    hits = np.asarray(simulate_optgen(trace, cap).per_access_hit, dtype=np.uint8)
+
+    def fn(sample):
+        start = sample.origin + len(sample.input)
+        misses = [a.global_id for off, a in enumerate(sample.window)
+                  if not hits[start + off]]
+        return misses[:l_out]
+
+    return fn
 
 
 def correctness_vs_window(trace, prefetch_params: ModelParameters, ratios, l_in=None,
@@ -353,10 +374,8 @@ def correctness_vs_window(trace, prefetch_params: ModelParameters, ratios, l_in=
     if K == 0:
         raise InvalidConfigError("trace too short for the largest window")
     torch = _native.torch_cuda()
-    p = prefetch_params
-    if p.l_in != l_in or p.l_out != l_out:
-        p = ModelParameters(p.kind, p.table_sizes, p.dim, p.stacks, l_in, l_out, p.arrays)
-    pf = _gpu_prefetches(torch, p, to_device_gids(torch, gids), K, l_in).cpu().numpy()
+    pf = _gpu_prefetches(torch, prefetch_params, to_device_gids(torch, gids), K,
+                         l_in).cpu().numpy()
     out = {}
     for r in ratios:
         w = r * l_out
@@ -390,5 +409,6 @@ def write_breakdown_csv(rows, path, latency_fn=None):
 
 __all__ = ["EVICTION_SPEED", "BufferConfig", "BreakdownReport", "PriorityBuffer",
            "load_embeddings", "gpu_buffer_populate", "coverage", "replay",
-           "replay_policy_only", "correctness_vs_window", "write_breakdown_csv",
+           "replay_policy_only", "optgen_miss_oracle", "correctness_vs_window",
+           "write_breakdown_csv",
            "CACHING", "PREFETCH", "LruSim"]

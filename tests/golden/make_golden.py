@@ -407,16 +407,107 @@ def make_config1():
     print(f"config1.npz written {time.time() - t0:.1f}s")
 
 
+def config1_inputs():
+    """Config-1 trace and the reference decisions stored in config1.npz."""
+    cfg = embcache.TraceGenConfig([2000] * 8, 1_000_000, 1.05, 0.4, 32, 0)
+    t = embcache.generate_trace(cfg)
+    z = np.load(os.path.join(HERE, "config1.npz"))
+    assert str(z["sha"]) == sha(t.gid_array)
+    shape = tuple(int(x) for x in z["bits_shape"])
+    bits = np.unpackbits(z["bits_packed"])[:shape[0] * shape[1]].reshape(shape)
+    return t, bits, z["pf"].astype(np.int64)
+
+
+def make_wide():
+    """Buffers wider than 4096 ways (the GPU's global-memory set kernel):
+    the reference fully associative replay on the config-1 trace at 30% / 40%
+    of its unique ids (es = 4 and es = C) with the config-1 reference
+    decisions, a 2-set x 4160-way per-set composition, the fully associative
+    LRU / LFU / optgen comparators and the labeler at 80% of those buffers;
+    SRRIP and the LRU+prefetch baseline on a smaller trace."""
+    t0 = time.time()
+    t, bits, pf = config1_inputs()
+    U = t.unique_count
+    out = {"sha": np.array(sha(t.gid_array))}
+    fa_cases, fa_counts, fa_cov = [], [], []
+    for frac in (0.3, 0.4):
+        C = int(np.floor(frac * U))
+        for es in (4, C):
+            c, cov = ref_replay(t, C, es, bits, pf)
+            fa_cases.append([C, es])
+            fa_counts.append(c)
+            fa_cov.append(cov)
+            print(f"wide FA C={C} es={es}: {c} {time.time() - t0:.1f}s")
+    out["fa_cases"] = np.array(fa_cases)
+    out["fa_counts"] = np.array(fa_counts)
+    out["fa_coverage"] = np.array(fa_cov)
+    out["sa_case"] = np.array([8320, 4160, 4])
+    out["sa_counts"] = np.array(per_set_replay(t, 8320, 4160, 4, bits, pf))
+    print(f"wide 2x4160 per-set {time.time() - t0:.1f}s")
+    C = int(np.floor(0.4 * U))
+    pol = {}
+    for name, policy in (("lru", cache_sim.Policy.LRU), ("lfu", cache_sim.Policy.LFU),
+                         ("optgen", cache_sim.Policy.OPTGEN)):
+        r = cache_sim.simulate(t, cache_sim.CacheConfig(C, policy))
+        out[f"{name}_hits"] = np.array(r.hits)
+        out[f"{name}_pa_sha"] = np.array(sha(np.array(r.per_access_hit)))
+        if r.keep_decisions is not None:
+            out[f"{name}_keep_sha"] = np.array(sha(np.array(r.keep_decisions)))
+        print(f"wide FA {name} C={C}: hits {r.hits} {time.time() - t0:.1f}s")
+    # labeler.py:43-83 at 80% of the 20% buffer (2528 ways, shared-memory
+    # kernel) and of the 40% buffer (5056 ways, global-memory kernel)
+    from embcache import labeler
+    samples = embcache.chunk(t)
+    for name, gc in (("c20", int(np.floor(0.2 * U))), ("c40", C)):
+        lc = labeler.label_caching(t, samples, gc)
+        lab = np.array([s.cache_labels for s in lc.samples], dtype=np.uint8)
+        lp = labeler.label_prefetch(t, samples, gc, l_out=5)
+        tg = np.array([[a.global_id for a in s.prefetch_targets] for s in lp.samples],
+                      dtype=np.int64)
+        org = np.array([s.origin for s in lp.samples], dtype=np.int64)
+        out[f"label_{name}_cap"] = np.array([gc, lc.label_capacity])
+        out[f"label_{name}_caching_sha"] = np.array(sha(lab))
+        out[f"label_{name}_caching_ones"] = np.array(int(lab.sum()))
+        out[f"label_{name}_prefetch_sha"] = np.array(sha(tg))
+        out[f"label_{name}_prefetch_origin_sha"] = np.array(sha(org))
+        out[f"label_{name}_prefetch_dropped"] = np.array(lp.dropped)
+        print(f"labels {name}: cap {lc.label_capacity} ones {int(lab.sum())} "
+              f"dropped {lp.dropped} {time.time() - t0:.1f}s")
+    # SRRIP / LFU / LRU+prefetch past 4096 ways on a smaller trace
+    ts = embcache.generate_trace(embcache.TraceGenConfig([3000] * 4, 120_000, 1.05, 0.4, 32, 21))
+    out["small_gids"] = ts.gid_array.astype(np.int32)
+    out["small_table_sizes"] = np.array(ts.table_sizes)
+    for name, policy in (("srrip", cache_sim.Policy.SRRIP), ("lfu", cache_sim.Policy.LFU),
+                         ("lru", cache_sim.Policy.LRU), ("optgen", cache_sim.Policy.OPTGEN)):
+        r = cache_sim.simulate(ts, cache_sim.CacheConfig(4160, policy))
+        out[f"small_{name}_per_access"] = np.packbits(np.array(r.per_access_hit, dtype=np.uint8))
+        out[f"small_{name}_hits"] = np.array(r.hits)
+        print(f"small FA {name}: hits {r.hits} {time.time() - t0:.1f}s")
+    oracle = rt.optgen_miss_oracle(ts, 6000, l_out=5)
+    s_samples = embcache.chunk(ts)
+    lists = [oracle(s) for s in s_samples]
+    out["small_lrupf_pf"] = pad(lists, 5).astype(np.int32)
+    lp = rt.replay_policy_only(ts, cache_sim.CacheConfig(4200, cache_sim.Policy.LRU),
+                               prefetch_fn=lambda s: lists[s.origin // 15])
+    out["small_lrupf_counts"] = np.array([lp.cache_hits, lp.prefetch_hits, lp.on_demand,
+                                          lp.prefetch_issued, lp.prefetch_useful])
+    out["small_lrupf_coverage"] = np.array(lp.coverage)
+    out["meta"] = np.array(json.dumps(META))
+    np.savez_compressed(os.path.join(HERE, "wide.npz"), **out)
+    print(f"wide.npz written {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-config1", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
     jobs = {"small": make_small, "models": make_models, "traces": make_traces,
-            "config1": make_config1, "hot": make_hot, "artifacts": make_artifacts}
+            "config1": make_config1, "hot": make_hot, "artifacts": make_artifacts,
+            "wide": make_wide}
     for name, fn in jobs.items():
         if a.only and name != a.only:
             continue
-        if name == "config1" and a.skip_config1:
+        if name in ("config1", "wide") and a.skip_config1:
             continue
         fn()

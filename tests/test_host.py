@@ -139,8 +139,8 @@ def test_pcg64_jump_ahead_matches_numpy():
 
 def test_coverage_mean_is_sequential_float64():
     rng = np.random.default_rng(0)
-    num = rng.integers(0, 6, 5000).astype(np.uint8)
-    den = rng.integers(1, 16, 5000).astype(np.uint8)
+    num = rng.integers(0, 600, 5000).astype(np.uint16)
+    den = rng.integers(600, 1600, 5000).astype(np.uint16)
     acc = 0.0
     for a, b in zip(num, den):
         acc += int(a) / int(b)

@@ -126,3 +126,43 @@ def test_oracle_hot_runs_vs_reference():
         cap, ways = int(case[1]), int(case[2])
         h, p = oracle.lru(gids, 400, cap, ways, per_access=True)
         assert h == hits and np.array_equal(p, pa), case
+
+
+def test_trace_oracle_matches_reference_hashes():
+    """oracle.trace_oracle (the reference arm's workload generator, no product
+    import) reproduces the reference generate_trace outputs."""
+    import hashlib
+    import json
+    from oracle import trace_oracle
+    z = golden("traces.npz")
+    i = 0
+    while f"cfg{i}" in z:
+        ts, n, s, p, pool, seed = json.loads(str(z[f"cfg{i}"]))
+        g = trace_oracle.generate_gids(ts, n, s, p, pool, seed)
+        assert hashlib.sha256(g.astype(np.int64).tobytes()).hexdigest() == str(z[f"sha{i}"])
+        assert np.unique(g).size == int(z[f"unique{i}"])
+        for block in (997, 1 << 20):
+            gb = np.concatenate(list(trace_oracle.generate_gid_blocks(ts, n, s, p, pool, seed,
+                                                                      block)))
+            assert np.array_equal(gb, g)
+        i += 1
+    c1 = golden("config1.npz")
+    g = trace_oracle.generate_gids([2000] * 8, 1_000_000, 1.05, 0.4, 32, 0)
+    assert hashlib.sha256(g.astype(np.int64).tobytes()).hexdigest() == str(c1["sha"])
+
+
+def test_oracle_wide_buffers_match_reference():
+    """The C oracle at the fully associative capacities past 4096 ways
+    (tests/golden/wide.npz, reference replay with the config-1 decisions)."""
+    from oracle import trace_oracle
+    z = golden("wide.npz")
+    c1 = golden("config1.npz")
+    g = trace_oracle.generate_gids([2000] * 8, 1_000_000, 1.05, 0.4, 32, 0)
+    K = int(c1["bits_shape"][0])
+    bits = np.unpackbits(c1["bits_packed"])[:K * 15].reshape(K, 15)
+    pf = c1["pf"].astype(np.int64)
+    for case, cnt, cov in zip(z["fa_cases"], z["fa_counts"], z["fa_coverage"]):
+        C, es = (int(x) for x in case)
+        ref, c = oracle.replay(g, 16000, C, 0, es, bits=bits, pf=pf)
+        assert [ref[k] for k in oracle.COUNTER_NAMES] == list(cnt), case
+        assert c == float(cov)
