@@ -15,20 +15,25 @@ generator, bit-exact), caching model d=64 / 1 stack, prefetch model d=64 /
 2 stacks (reference init_params, init_scale 0.4 so the decisions are not
 degenerate), buffer = 20% of unique ids rounded down to 32 ways, es = 4.
 
-N > 1 (torchrun): weak scaling, table-sharded: every rank owns its own
-256-table shard and its own 25 M-access slice (seed 2 + rank), no collective
-on the data path; counters are summed at the end.
-
+N > 1 (the default workload is then config 3): `--gpus N` starts N ranks
+itself (torch.distributed.run on 127.0.0.1) unless already under torchrun.
 --config 3: the 856-table x 100k-row, 500 M-access trace (seed 3), drawn by
 the streamed bit-exact generator (TraceStream) and table-sharded over
 --shards ranks (default: the world size) greedily by access count; every
-rank runs its shard's sub-trace with shard-local models (strong scaling).
-On one GPU, --shards 8 --shard-index r measures rank r's share of the
-8-GPU job alone.
+rank runs its shard's sub-trace with shard-local models (strong scaling),
+no collective on the data path, counters summed at the end.  On one GPU,
+--shards 8 --shard-index r measures rank r's share of the 8-GPU job alone.
+--config 2 under N ranks: weak scaling, every rank its own 256-table,
+25 M-access trace (seed 2 + rank).
+
+After the timed region every rank checks its step's counters against the C
+oracle replaying the whole (shard) trace with the GPU's own decisions
+(`parity` in the line).
 
 --impl reference: the reference's CPU algorithm (the oracle port: numpy
-float64 forwards + the C replay restatement, oracle/) on a bounded sample of
-the same workload, rank 0 only.
+float64 forwards + the C replay restatement, oracle/; its trace from the
+oracle's generator, nothing from the product package) on a bounded sample
+of the same workload, rank 0 only.
 """
 from __future__ import annotations
 
@@ -74,11 +79,18 @@ def parse():
     ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
     ap.add_argument("--pieces", type=int, default=8, help="replay pipeline pieces")
     ap.add_argument("--model-sms", type=int, default=136, help="SMs the forwards may use")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--config", type=int, default=None, choices=[2, 3],
+                    help="workload: 2 (single-GPU config, the N=1 default) or 3 (856 tables, "
+                         "500 M accesses, table-sharded: the N>1 default)")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the full-trace counter check against the C oracle")
     ap.add_argument("--shards", type=int, default=0, help="config 3: table shards (0 = world)")
     ap.add_argument("--shard-index", type=int, default=0,
                     help="config 3 on one process: which shard to run")
     args = ap.parse_args()
+    if args.config is None:
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        args.config = 2 if world <= 1 else 3
     if args.config == 3:
         d = {"accesses": 25_000_000, "tables": 256, "rows": 50_000}
         c3 = {"accesses": 500_000_000, "tables": 856, "rows": 100_000}
@@ -215,62 +227,42 @@ def fwd_figures(ms, flops, transc, prof, pieces):
 
 
 # --------------------------------------------------------------------------
-def cpu_baseline(t, cparams, pparams, emb_c, emb_p, n_sample, capacity, ways, shard=None):
-    """The reference algorithm on the host cores (oracle port), on the first
-    n_sample accesses: float64 numpy forwards in batches of 256 (runtime.py:
-    181-210), fp64 decode, the C replay restatement in the reference's dense
-    per-id layout (runtime.py:41-112, 220-283) and the 32-way LRU."""
+def cpu_baseline(gids, table_sizes, args, capacity, label):
+    """The reference algorithm on the host cores (oracle.cpu_baseline: the
+    float64 forwards on every core, the sequential C replay and the LRU) on
+    the first --cpu-sample accesses of `gids` (global ids)."""
+    from oracle import cpu_baseline as cb
+    return cb.run(gids, table_sizes, args.dim, args.init_scale, args.cpu_sample, capacity, 32,
+                  label=label)
+
+
+def parity_check(gids, total_ids, hp, rep, lru, capacity):
+    """The step's counters against the C oracle (checker only, after the
+    timed region): the oracle replays the whole trace with the GPU's own
+    decisions (runtime.py:220-283, per-set buffer) and runs the 32-way LRU
+    (cache_sim.py:92-106); every counter, the coverage and the LRU misses
+    must be equal."""
     import oracle
-    from oracle import model_oracle as mo
-    from paper_2511_08568_b200.trace import num_chunks
-    gids = t.gid_array[:n_sample]
-    K = num_chunks(len(gids))
-    uniq, inv = np.unique(gids[:K * 15], return_inverse=True)
-    tid = t.table_ids[:K * 15].reshape(K, 15)
-    rows = uniq
-    if shard is not None:   # shard-local embed_id rows / embed_table rows
-        rows = shard.to_local(uniq)[0]
-        tid = shard.table_local[tid]
-    ac = dict(cparams.arrays)
-    ap = dict(pparams.arrays)
-    ac["embed_id"] = emb_c[rows].double().cpu().numpy() if hasattr(emb_c, "cpu") else emb_c[rows]
-    ap["embed_id"] = emb_p[rows].double().cpu().numpy() if hasattr(emb_p, "cpu") else emb_p[rows]
-    lg = inv.reshape(K, 15)
-    V = t.total_ids
-    oracle.lib()
-    cores = len(os.sched_getaffinity(0))
-    bits = np.empty((K, 15), dtype=np.uint8)
-    pf = np.empty((K, 5), dtype=np.int64)
-
-    def batches(b0, b1):
-        # runtime.py:181-210 in batches of 256 chunks
-        for b in range(b0, b1, 256):
-            e = min(b + 256, b1)
-            lc = mo.caching_logits(ac, cparams.dim, cparams.stacks, lg[b:e], tid[b:e])
-            bits[b:e] = lc >= 0
-            lp = mo.prefetch_logits(ap, pparams.dim, pparams.stacks, 5, lg[b:e], tid[b:e])
-            pf[b:e] = mo.decode_gids(mo.sigmoid(lp), V)
-
-    # all host cores: one thread per core over contiguous ranges of batches,
-    # BLAS single-threaded inside each (numpy releases the GIL in its kernels)
-    from concurrent.futures import ThreadPoolExecutor
-    from threadpoolctl import threadpool_limits
-    step = max(256, (K // cores + 255) // 256 * 256)
-    with threadpool_limits(limits=1), ThreadPoolExecutor(max_workers=cores) as pool:
-        list(pool.map(lambda b: batches(b, min(b + 256, K)), range(0, min(K, 256 * cores), 256)))
-        t0 = time.perf_counter()     # (the warm-up above: thread pool, page faults)
-        list(pool.map(lambda b: batches(b, min(b + step, K)), range(0, K, step)))
-        t1 = time.perf_counter()
-    rep, _ = oracle.replay(gids, V, capacity, ways, 4, bits=bits, pf=pf, dense=True)
-    oracle.lru(gids, V, capacity, ways)
-    t2 = time.perf_counter()
-    return {"value": len(gids) / (t2 - t0), "unit": UNIT,
-            "cores": cores, "kind": "port",
-            "sample": f"first {len(gids)} accesses of the {'shard' if shard is not None else 'rank-0 config-2'} trace ({K} chunks): "
-                      f"numpy float64 forwards on {cores} threads {t1 - t0:.2f}s + C replay "
-                      f"(dense per-id layout, sequential as runtime.py) + 32-way LRU "
-                      f"{t2 - t1:.2f}s",
-            "model_s": t1 - t0, "replay_s": t2 - t1, "_bits": bits, "_pf": pf}
+    t0 = time.perf_counter()
+    K = hp.K
+    bits = hp.bits[:K].cpu().numpy()
+    pf = hp.pf[:K].cpu().numpy().astype(np.int64)
+    ref, cov = oracle.replay(gids, total_ids, capacity, 32, 4, bits=bits, pf=pf)
+    lru_hits = oracle.lru(gids, total_ids, capacity, 32)
+    got = {"cache_hits": rep.cache_hits, "prefetch_hits": rep.prefetch_hits,
+           "on_demand": rep.on_demand, "prefetch_issued": rep.prefetch_issued,
+           "prefetch_useful": rep.prefetch_useful, "evictions": rep.evictions,
+           "prefetch_inserts": rep.prefetch_inserts}
+    want = {k: ref[k] for k in got}
+    out = {"counters_equal": got == want, "coverage_equal": rep.coverage == cov,
+           "lru_misses_equal": lru is not None and lru[1] == len(gids) - lru_hits,
+           "accesses": int(len(gids)), "chunks": int(K),
+           "checker": "oracle/replay_oracle.c on the GPU's own decisions, whole trace",
+           "check_s": time.perf_counter() - t0}
+    if not (out["counters_equal"] and out["coverage_equal"] and out["lru_misses_equal"]):
+        out["gpu"] = got
+        out["oracle"] = want
+    return out
 
 
 def measure_rows(args, hp, n, torch):
@@ -382,6 +374,8 @@ def build_state(args, rank, torch):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -393,7 +387,8 @@ def main():
         # GPU (NCCL refuses two ranks per device) to exercise the N > 1 path
         backend = os.environ.get("RECMG_DIST_BACKEND", "nccl")
         local = local % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -419,6 +414,8 @@ def main():
     hp = HotPath(DeviceModel(cp, emb_c, decode_ids=dec), DeviceModel(pp, emb_p, decode_ids=dec),
                  t.table_sizes, C32, n, ways=32, eviction_speed=4, lru_capacity=C32, lru_ways=32,
                  pieces=args.pieces, model_sms=args.model_sms, shard=sh)
+    del emb_c, emb_p      # folded into the packed tables (tc32): free the fp32 rows
+    torch.cuda.empty_cache()
     host = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
     hp.gids[:n].copy_(host)
     torch.cuda.synchronize()
@@ -528,6 +525,18 @@ def main():
     if not args.no_rows and rank == 0:   # 6.6 GB of pinned rows: one rank measures K5/K6
         rows_line = measure_rows(args, hp, n, torch)
 
+    # ---- counters vs the C oracle over the whole trace (checker, untimed) ------
+    parity = None
+    if not args.no_parity:
+        parity = parity_check(t.gid_array, t.total_ids, hp, rep, lru, C32)
+        ok = parity["counters_equal"] and parity["coverage_equal"] and parity["lru_misses_equal"]
+        flag = torch.tensor([0 if ok else 1], dtype=torch.int64, device="cuda")
+        if dist:
+            if dist.get_backend() != "nccl":
+                flag = flag.cpu()
+            dist.all_reduce(flag, op=dist.ReduceOp.SUM)
+        parity["ranks_failing"] = int(flag.item())
+
     # ---- reduce over ranks ---------------------------------------------------
     vals = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device="cuda")
     ctr = torch.tensor([rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
@@ -591,7 +600,8 @@ def main():
         "higher_is_better": True, "scaling": "strong" if args.config == 3 else "weak",
         "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
-        "config": dict(workload(args, 0), pipeline_pieces=args.pieces, model_sms=args.model_sms),
+        "config": workload(args, 0),
+        "tuning": {"pipeline_pieces": args.pieces, "model_sms": args.model_sms},
         "quality": {"on_demand": c[2], "lru32_misses": c[7],
                     "on_demand_vs_lru32": (c[2] / c[7]) if c[7] else None,
                     "cache_hits": c[0], "prefetch_hits": c[1], "prefetch_issued": c[3],
@@ -614,8 +624,12 @@ def main():
         line["rows"] = rows_line
     if variant is not None:
         line["variant_tc16"] = variant
-    if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32, shard=sh)
+    if parity is not None:
+        line["parity"] = parity
+    if not args.no_cpu_baseline:
+        label = ("rank-0 config-2 trace" if args.config == 2 else
+                 f"shard {0 if world > 1 else args.shard_index} sub-trace of config 3")
+        cb = cpu_baseline(t.gid_array, t.table_sizes, args, C32, label)
         # the GPU's own decisions vs the float64 port on the same chunks
         # (bit and decoded-id agreement rates)
         rb_, rp_ = cb.pop("_bits"), cb.pop("_pf")
@@ -636,77 +650,54 @@ def main():
         dist.destroy_process_group()
 
 
+def reference_workload(args, idx):
+    """The reference arm's inputs from the oracle alone (no product import):
+    the config's trace by the oracle generator (oracle/trace_oracle.py, the
+    reference generate_trace restated and pinned to its hashes), for config 3
+    table-sharded exactly as the GPU arm does (LPT by access count) and
+    reduced to shard `idx`'s order-preserving sub-trace."""
+    from oracle import trace_oracle as to
+    sizes = [args.rows] * args.tables
+    if args.config == 2:
+        g = to.generate_gids(sizes, args.accesses, 1.05, 0.4, 32, 2)
+    else:
+        parts, counts = [], np.zeros(args.tables, dtype=np.int64)
+        blocks = []
+        for b in to.generate_gid_blocks(sizes, args.accesses, 1.05, 0.4, 32, 3):
+            counts += np.bincount(b // args.rows, minlength=args.tables)
+            blocks.append(b.astype(np.int32))
+        mine = to.assign_tables(counts, args.shards_eff) == idx
+        for b in blocks:
+            parts.append(b[mine[b // args.rows]])
+        del blocks
+        g = np.concatenate(parts).astype(np.int64)
+    U = int(np.count_nonzero(np.bincount(g, minlength=sum(sizes))))
+    C = int(math.floor(0.2 * U))
+    return g, sizes, C - C % 32
+
+
 def run_reference(args, rank, world, torch, dist):
-    """--impl reference: the reference CPU algorithm (oracle port) on rank 0."""
+    """--impl reference: the reference CPU algorithm (oracle port) on rank 0,
+    on a bounded sample of the same workload: float64 forwards on every host
+    core + the sequential replay and LRU (oracle/cpu_baseline.py)."""
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    import paper_2511_08568_b200 as rb
-    if args.config == 3:
-        # shard --shard-index of the streamed config-3 trace, models drawn on the host
-        t, _, _, C32, cp, emb_c, pp, emb_p, _, sh = build_state_config3(
-            args, args.shard_index, torch, device=False)
-        vals, last = [], None
-        for _ in range(args.steps):
-            last = cpu_baseline(t, cp, pp, emb_c, emb_p, args.cpu_sample, C32, 32, shard=sh)
-            last.pop("_bits"), last.pop("_pf")
-            vals.append(last["value"])
-        value = statistics.median(vals)
-        print(json.dumps({
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": args.cpu_sample / value * 1000.0,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
-            "config": workload(args, 0), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "port",
-                             "sample": last["sample"]},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}), flush=True)
-        if dist:
-            dist.destroy_process_group()
-        return
-    # the full rank-0 trace: the buffer capacity is 20% of ITS unique ids
-    t = rb.generate_trace(rb.TraceGenConfig([args.rows] * args.tables, args.accesses,
-                                            1.05, 0.4, 32, 2))
-    # The reference's float64 weights (init_params, model.py:83-100) for the
-    # rows the sample touches: one uniform double per PCG64 draw, so embed_id
-    # row g is draws [g*d, (g+1)*d) and the dense arrays start at draw V*d.
-    from paper_2511_08568_b200.model import _shapes
-    V, d = t.total_ids, args.dim
-    uniq = np.unique(t.gid_array[:args.cpu_sample])
-    emb, dense = {}, {}
-    for kind, seed in (("caching", 0), ("prefetch", 1)):
-        full = np.zeros((int(uniq.max()) + 1, d))
-        for g in uniq:
-            b = np.random.PCG64(seed)
-            b.advance(int(g) * d)
-            full[g] = np.random.Generator(b).uniform(-args.init_scale, args.init_scale, d)
-        b = np.random.PCG64(seed)
-        b.advance(V * d)
-        rng = np.random.Generator(b)
-        shp = _shapes(kind, V, len(t.table_sizes), d, 1 if kind == "caching" else 2, 5)
-        dense[kind] = {nm: rng.uniform(-args.init_scale, args.init_scale, size=s)
-                       for nm, s in shp.items() if nm != "embed_id"}
-        emb[kind] = full
-    C = int(math.floor(0.2 * t.unique_count))
-    C32 = C - C % 32
-
-    class P:
-        pass
-    cp, pp = P(), P()
-    cp.arrays, cp.dim, cp.stacks = dense["caching"], d, 1
-    pp.arrays, pp.dim, pp.stacks = dense["prefetch"], d, 2
-    vals = []
-    last = None
+    idx = 0 if world > 1 else args.shard_index
+    gids, sizes, C32 = reference_workload(args, idx)
+    label = ("rank-0 config-2 trace" if args.config == 2 else
+             f"shard {idx} sub-trace of config 3")
+    vals, last = [], None
     for _ in range(args.steps):
-        last = cpu_baseline(t, cp, pp, emb["caching"], emb["prefetch"], args.cpu_sample, C32, 32)
+        last = cpu_baseline(gids, sizes, args, C32, label)
         last.pop("_bits"), last.pop("_pf")
         vals.append(last["value"])
     value = statistics.median(vals)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": args.cpu_sample / value * 1000.0,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.config == 3 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
             "config": workload(args, 0), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"],
@@ -716,6 +707,19 @@ def run_reference(args, rank, world, torch, dist):
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args):
+    """--gpus N without torchrun: start N ranks (torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1) and return their exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

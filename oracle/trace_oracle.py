@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import heapq
+import os
 
 import numpy as np
 
@@ -55,7 +56,8 @@ def generate_gids(table_sizes, total_accesses, zipf_exponent=1.1, markov_stickin
 
 
 def generate_gid_blocks(table_sizes, total_accesses, zipf_exponent=1.1, markov_stickiness=0.0,
-                        correlation_pool_size=32, rng_seed=0, block=1 << 24):
+                        correlation_pool_size=32, rng_seed=0, block=1 << 24,
+                        threads=None):
     """generate_gids block by block (bounded memory for 5e8 accesses): the
     three random() streams of generate_trace start at outputs 0, n and 2n of
     the PCG64 state right after the permutation (choice with p draws one
@@ -79,14 +81,23 @@ def generate_gid_blocks(table_sizes, total_accesses, zipf_exponent=1.1, markov_s
         b.advance(offset)
         return np.random.Generator(b)
 
-    gz, gs, gp = stream(0), stream(n), stream(2 * n)
+    def draws(i0):
+        c = min(block, n - i0)
+        zipf = rank_to_gid[cdf.searchsorted(stream(i0).random(c), side="right")]
+        return zipf.astype(np.int64), stream(n + i0).random(c), stream(2 * n + i0).random(c)
+
+    # the draws of a wave of blocks run on the host cores (numpy releases the
+    # GIL in random() and searchsorted()); the pool pass stays sequential
+    from concurrent.futures import ThreadPoolExecutor
+    workers = threads or max(1, min(32, len(os.sched_getaffinity(0))))
     pool = np.zeros(correlation_pool_size, dtype=np.int64)
     plen = np.zeros(1, dtype=np.int32)
-    for i0 in range(0, n, block):
-        c = min(block, n - i0)
-        zipf = rank_to_gid[cdf.searchsorted(gz.random(c), side="right")].astype(np.int64)
-        yield _pool_pass(zipf, gs.random(c), gp.random(c), markov_stickiness,
-                         correlation_pool_size, pool, plen)
+    starts = list(range(0, n, block))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        for w0 in range(0, len(starts), workers):
+            for zipf, sticky, poolc in ex.map(draws, starts[w0:w0 + workers]):
+                yield _pool_pass(zipf, sticky, poolc, markov_stickiness,
+                                 correlation_pool_size, pool, plen)
 
 
 def table_offsets(table_sizes) -> np.ndarray:
