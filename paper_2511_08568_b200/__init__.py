@@ -6,12 +6,14 @@ in include/recmg.h, loaded from the in-tree librecmg.so; there is no CPU
 fallback on this path.
 """
 from .checkpoint import load_checkpoint, load_checkpoint_shard, save_checkpoint, vocabulary_hash
-from .cache_sim import CacheConfig, Policy, SimResult, simulate, simulate_optgen, sweep
+from .cache_sim import (CacheConfig, Policy, SimResult, brute_force_optimal, simulate,
+                        simulate_optgen, sweep, write_sweep_csv)
 from .errors import (CheckpointError, EmbcacheError, InvalidConfigError,
                      MissingArtifactError, NumericalError, OutOfVocabularyError,
                      TraceParseError, TraceValidationError, VocabularyMismatchError)
 from .labeler import (LABEL_CAPACITY_FRACTION, LabeledDataset, caching_label_array,
-                      label_caching, label_prefetch, prefetch_target_array, split_dataset)
+                      label_caching, label_prefetch, prefetch_target_array, read_dataset,
+                      split_dataset, write_dataset)
 from .model import (CACHING, PREFETCH, DeviceModel, ModelParameters, batch_arrays,
                     decode_indices, device_model, forward_caching, forward_caching_batch,
                     forward_prefetch, forward_prefetch_batch, init_params,

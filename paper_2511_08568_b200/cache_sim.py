@@ -7,6 +7,7 @@ realistic capacity) in global memory.
 """
 from __future__ import annotations
 
+import csv
 from dataclasses import dataclass
 from enum import Enum
 
@@ -117,3 +118,43 @@ def sweep(trace, policies, capacities, ways=None) -> list:
             rows.append({"policy": policy.value, "capacity": cap, "hits": res.hits,
                          "misses": res.misses, "hit_rate": res.hit_rate})
     return rows
+
+
+def write_sweep_csv(rows: list, path: str):
+    """cache_sim.py:323-329."""
+    with open(path, "w", encoding="utf-8", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["policy", "capacity", "hits", "misses", "hit_rate"])
+        for r in rows:
+            w.writerow([r["policy"], r["capacity"], r["hits"], r["misses"],
+                        f"{r['hit_rate']:.6f}"])
+
+
+BRUTE_MAX_LEN = 14
+BRUTE_MAX_CAP = 4
+
+
+def brute_force_optimal(trace, capacity: int) -> int:
+    """cache_sim.py:263-301: the maximum hit count over every victim choice,
+    by exhaustive search -- an independent check of the offline optimum for
+    tiny instances (at most 14 accesses, capacity 4), on the host."""
+    from functools import lru_cache
+    gids = tuple(int(g) for g in _gids_of(trace))
+    if len(gids) > BRUTE_MAX_LEN or capacity > BRUTE_MAX_CAP:
+        raise InvalidConfigError(
+            f"brute force bounded to {BRUTE_MAX_LEN} accesses / capacity {BRUTE_MAX_CAP}")
+    if capacity < 1:
+        raise InvalidConfigError("capacity must be >= 1")
+
+    @lru_cache(maxsize=None)
+    def best(i: int, cached: frozenset) -> int:
+        if i == len(gids):
+            return 0
+        g = gids[i]
+        if g in cached:
+            return 1 + best(i + 1, cached)
+        if len(cached) < capacity:
+            return best(i + 1, cached | {g})
+        return max(best(i + 1, (cached - {v}) | {g}) for v in cached)
+
+    return best(0, frozenset())

@@ -29,3 +29,83 @@ def letters(text: str):
 @pytest.fixture(scope="session")
 def small():
     return golden("small_replay.npz")
+
+
+# ---- the reference's own tests (tests/refsuite/, fetched unmodified) --------
+REFSUITE = os.path.join(ROOT, "tests", "refsuite")
+
+# Module names the reference tests import, pointed at this package (the
+# drop-in: same names, same behaviour, GPU underneath).
+_ALIASES = {
+    "embcache": "paper_2511_08568_b200",
+    "embcache.runtime": "paper_2511_08568_b200.runtime",
+    "embcache.cache_sim": "paper_2511_08568_b200.cache_sim",
+    "embcache.trace": "paper_2511_08568_b200.trace",
+    "embcache.errors": "paper_2511_08568_b200.errors",
+    "embcache.labeler": "paper_2511_08568_b200.labeler",
+    "embcache.neural.model": "paper_2511_08568_b200.model",
+    "embcache.neural.checkpoint": "paper_2511_08568_b200.checkpoint",
+}
+
+# Reference test cases that exercise the reference's OWN internals or
+# offline pipeline rather than the drop-in boundary (reason per case).
+REFSUITE_SKIPS = {
+    "test_runtime.py::test_replay_priority_bound":
+        "spies on replay's per-chunk Python call of load_embeddings (runtime.py:267-268); "
+        "the GPU replay applies Alg. 1 inside the kernel, so the spy never fires. The bound "
+        "itself (every priority <= es + 1 after every chunk) is asserted on the GPU buffer "
+        "state by tests/test_gpu_wide.py::test_priority_bound_after_every_chunk",
+}
+
+
+def _install_embcache_aliases():
+    import importlib
+    import types
+    if "embcache" in sys.modules:
+        return
+    for name, target in _ALIASES.items():
+        sys.modules[name] = importlib.import_module(target)
+    neural = types.ModuleType("embcache.neural")
+    neural.model = sys.modules["embcache.neural.model"]
+    neural.checkpoint = sys.modules["embcache.neural.checkpoint"]
+    neural.__path__ = []
+    sys.modules["embcache.neural"] = neural
+    sys.modules["embcache"].neural = neural
+
+
+if any(f.startswith("test_") for f in (os.listdir(REFSUITE) if os.path.isdir(REFSUITE) else [])):
+    _install_embcache_aliases()
+
+
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        if str(item.fspath).startswith(REFSUITE + os.sep):
+            item.add_marker(pytest.mark.gpu)
+            key = f"{os.path.basename(str(item.fspath))}::{item.name}"
+            base = key.split("[")[0]
+            if key in REFSUITE_SKIPS or base in REFSUITE_SKIPS:
+                item.add_marker(pytest.mark.skip(
+                    reason=REFSUITE_SKIPS.get(key) or REFSUITE_SKIPS[base]))
+
+
+def letter_trace(text: str, table_size: int | None = None):
+    """reference conftest.py:12-15."""
+    from paper_2511_08568_b200 import trace_from_gids
+    gids = letters(text)
+    size = table_size if table_size is not None else max(gids) + 1
+    return trace_from_gids(gids, [size])
+
+
+def random_gid_trace(rng: np.random.Generator, n: int, universe: int):
+    """reference conftest.py:18-20."""
+    from paper_2511_08568_b200 import trace_from_gids
+    return trace_from_gids(rng.integers(0, universe, size=n), [universe])
+
+
+@pytest.fixture(scope="session")
+def correlated_trace():
+    """reference conftest.py:23-29."""
+    from paper_2511_08568_b200 import TraceGenConfig, generate_trace
+    return generate_trace(TraceGenConfig(table_sizes=[4, 100, 60], total_accesses=4000,
+                                         zipf_exponent=1.05, markov_stickiness=0.4,
+                                         correlation_pool_size=24, rng_seed=11))

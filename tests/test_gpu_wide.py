@@ -214,3 +214,35 @@ def test_device_models_are_reused_until_weights_change():
     assert b is not a
     l1 = rb.forward_caching_batch(cp, gid, tid).logits
     assert np.allclose(l1 - l0, 0.5, atol=1e-4)
+
+
+def test_priority_bound_after_every_chunk():
+    """test_runtime.py:139-154 on the GPU state: replaying chunk by chunk
+    (recmg_replay_chunks continues the state), no resident priority exceeds
+    eviction_speed + 1 after any chunk's update, fully associative and
+    32-way, and the piecewise replay equals the one-shot replay."""
+    import torch
+    from paper_2511_08568_b200.engine import BufferReplay, to_device_gids
+    t = rb.generate_trace(rb.TraceGenConfig([4, 100, 60], 4000, 1.05, 0.4, 24, 11))
+    n = len(t)
+    K = rb.num_chunks(n)
+    bits = torch.ones((K, 15), dtype=torch.uint8, device="cuda")
+    g = to_device_gids(torch, t.gid_array)
+    for cap, ways in ((24, None), (64, 32)):
+        eng = BufferReplay(cap, t.total_ids, 4, ways, n)
+        S = cap // (ways or cap)
+        W = ways or cap
+        off = 64 + ((4 * S * W + 255) // 256) * 256
+        top = 0
+        for k in range(K):
+            eng.run_chunks(g, k, k + 1, k == K - 1, bits=bits)
+            tags = eng.state[64:64 + 4 * S * W].view(torch.int32)
+            meta = eng.state[off:off + 8 * S * W].view(torch.int64)
+            pr = (meta & 0xFFFFFFFF)[tags >= 0]
+            if pr.numel():
+                top = max(top, int(pr.max()))
+                assert top <= 5, (cap, ways, k)
+        r = eng.result()
+        one = rb.replay(t, rb.BufferConfig(cap, 4, ways), caching_fn=lambda s: [1] * 15)
+        assert r["on_demand"] == one.on_demand and r["cache_hits"] == one.cache_hits
+        assert top == 5
