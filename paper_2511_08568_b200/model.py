@@ -115,10 +115,69 @@ def init_params_device(kind, table_sizes, dim=32, stacks=None, l_in=15, l_out=5,
     return ModelParameters(kind, list(table_sizes), dim, stacks, l_in, l_out, arrays), emb
 
 
+TC_DIM = 64   # the tcgen05 kernels' hidden size; smaller models run zero-padded
+
+
+def _pad_blocks(a, rows_in, rows_out, cols_in, cols_out, row_blocks=1, col_blocks=1):
+    """Zero-pad a [row_blocks*rows_in, col_blocks*cols_in] array block-wise to
+    [row_blocks*rows_out, col_blocks*cols_out] (each block in its top-left)."""
+    a = np.asarray(a).reshape(row_blocks * rows_in, col_blocks * cols_in)
+    out = np.zeros((row_blocks * rows_out, col_blocks * cols_out), dtype=a.dtype)
+    for i in range(row_blocks):
+        for j in range(col_blocks):
+            out[i * rows_out:i * rows_out + rows_in, j * cols_out:j * cols_out + cols_in] = \
+                a[i * rows_in:(i + 1) * rows_in, j * cols_in:(j + 1) * cols_in]
+    return out
+
+
+def pad_params(params: ModelParameters, D: int = TC_DIM, with_embed: bool = True):
+    """The same model at hidden size D >= params.dim with every extra unit
+    zero-weighted (model.py:54-80 shapes; gate blocks i,f,g,o of d columns
+    become blocks of D; [E_id; E_tab] / [x; ctx] / [h; ctx] row blocks keep
+    their offsets per block).  Exact: an extra unit's gates are 0 -> i = f =
+    o = 1/2, g = 0, so its cell and hidden state stay 0 from the zero
+    initial state, its attention key, query and value are 0, att_v / comb /
+    head weights on it are 0, so every logit equals the d-unit model's."""
+    d = params.dim
+    if D == d:
+        return params
+    A = params.arrays
+    pad = {}
+    for name, arr in A.items():
+        if name == "embed_id" and not with_embed:
+            continue
+        if name in ("embed_id", "embed_table"):
+            pad[name] = _pad_blocks(arr, arr.shape[0], arr.shape[0], d, D)
+        elif name in ("att_enc", "att_dec"):
+            pad[name] = _pad_blocks(arr, d, D, d, D)
+        elif name in ("att_v", "head_w"):
+            pad[name] = _pad_blocks(arr, d, D, 1, 1)
+        elif name == "comb_w":
+            pad[name] = _pad_blocks(arr, d, D, d, D, row_blocks=2)
+        elif name == "comb_b":
+            pad[name] = _pad_blocks(arr, 1, 1, d, D).reshape(D)
+        elif name == "head_b":
+            pad[name] = np.array(arr, copy=True)
+        elif name == "slot_embed":
+            pad[name] = _pad_blocks(arr, arr.shape[0], arr.shape[0], d, D, col_blocks=2)
+        elif name.endswith("_wx"):
+            blocks = 2 if name == "enc0_wx" else (3 if name == "dec0_wx" else 1)
+            pad[name] = _pad_blocks(arr, d, D, d, D, row_blocks=blocks, col_blocks=4)
+        elif name.endswith("_wh"):
+            pad[name] = _pad_blocks(arr, d, D, d, D, col_blocks=4)
+        elif name.endswith("_b"):
+            pad[name] = _pad_blocks(arr, 1, 1, d, D, col_blocks=4).reshape(4 * D)
+        else:
+            raise InvalidConfigError(f"cannot pad parameter {name!r}")
+    return ModelParameters(params.kind, list(params.table_sizes), D, params.stacks, params.l_in,
+                           params.l_out, pad)
+
+
 class DeviceModel:
     """A model's weights resident in HBM in a kernel layout.
 
-    precision "tc32" (default when the shape allows: d = 64): every GEMM on
+    precision "tc32" (default when the shape allows: d <= 64, smaller d
+    zero-padded to 64 by pad_params, which is exact): every GEMM on
     the tcgen05 tensor cores as the fp16 hi/lo 3-product split, fp32
     accumulation (recmg_model_pack_tc / RECMG_PREC_TC32; csrc/lstm_tc.cu);
     the layer-0 token projection is folded into per-id tables, so the
@@ -137,6 +196,21 @@ class DeviceModel:
         self.params = params
         self.kind = params.kind
         self.decode_ids = int(decode_ids)
+        self.dim = int(params.dim)
+        if precision in ("auto", "tc32", "tc16") and params.dim < TC_DIM:
+            # smaller hidden sizes (the reference default is 32, model.py:34)
+            # run on the d = 64 tcgen05 kernels zero-padded (pad_params: exact)
+            padded = pad_params(params, TC_DIM, with_embed=embed_id is None)
+            probe = _native.ModelShape(
+                _native.MODEL_CACHING if params.kind == CACHING else _native.MODEL_PREFETCH,
+                TC_DIM, int(params.stacks), int(params.l_in), int(params.l_out),
+                len(params.table_sizes), int(params.total_ids))
+            if L.recmg_model_packed_bytes(ctypes.byref(probe), _native.PREC_TC32):
+                if embed_id is not None:
+                    embed_id = torch.nn.functional.pad(embed_id, (0, TC_DIM - params.dim))
+                params = padded
+                if precision == "auto":
+                    precision = "tc32"
         self.shape = _native.ModelShape(
             _native.MODEL_CACHING if params.kind == CACHING else _native.MODEL_PREFETCH,
             int(params.dim), int(params.stacks), int(params.l_in), int(params.l_out),
@@ -149,7 +223,7 @@ class DeviceModel:
         if precision == "auto":
             precision = "tc32" if tc_bytes else "fp32"
         if precision in ("tc32", "tc16") and not tc_bytes:
-            raise InvalidConfigError(f"{precision} needs dim 64, l_in/l_out <= 16 and the "
+            raise InvalidConfigError(f"{precision} needs dim <= 64, l_in/l_out <= 16 and the "
                                      "default stacks")
         if precision not in ("tc32", "tc16", "fp32"):
             raise InvalidConfigError(f"unknown precision {precision!r}")

@@ -35,20 +35,25 @@ def test_models_vs_reference_fixture():
         assert np.abs(res.value - probs).max() < 1e-5
 
 
+@pytest.mark.parametrize("dim", [32, 64])
 @pytest.mark.parametrize("precision", ["fp32", "tc32"])
 @pytest.mark.parametrize("scale", [0.08, 0.4, 0.6])
-def test_config1_shapes_vs_oracle(scale, precision):
-    """d = 64, config-1 layout, 300 chunks (a ragged tile) of a config-1 style trace."""
+def test_config1_shapes_vs_oracle(scale, precision, dim):
+    """d = 64 and the reference default d = 32 (model.py:34; tc32 runs it
+    zero-padded on the d = 64 tcgen05 kernels), config-1 layout, 300 chunks
+    (a ragged tile) of a config-1 style trace."""
+    from paper_2511_08568_b200 import model as mdl
     t = rb.generate_trace(rb.TraceGenConfig([2000] * 8, 300 * 15 + 30, 1.05, 0.4, 32, 0))
     K = rb.num_chunks(len(t))
     gid = t.gid_array[:K * 15].reshape(K, 15)
     tid = t.table_ids[:K * 15].reshape(K, 15)
-    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=scale)
-    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=scale)
+    cp = rb.init_params("caching", t.table_sizes, dim=dim, seed=0, init_scale=scale)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=dim, seed=1, init_scale=scale)
+    assert mdl.device_model(cp, precision=precision).precision == precision
     lc = rb.forward_caching_batch(cp, gid, tid, precision).logits
     lp = rb.forward_prefetch_batch(pp, gid, tid, precision).logits
-    rc = mo.caching_logits(cp.arrays, 64, 1, gid, tid)
-    rp = mo.prefetch_logits(pp.arrays, 64, 2, 5, gid, tid)
+    rc = mo.caching_logits(cp.arrays, dim, 1, gid, tid)
+    rp = mo.prefetch_logits(pp.arrays, dim, 2, 5, gid, tid)
     _check(lc, rc)
     _check(lp, rp)
     # decisions: bit flips only where the reference logit is ~0

@@ -203,3 +203,23 @@ def test_streamed_generator_equals_numpy_path(cfg):
         if block == 1 and len(want) > 5000:
             continue
         assert np.array_equal(generate_trace_streamed(c, block), want), block
+
+
+def test_pad_params_is_exact_in_float64():
+    """pad_params (d < 64 models on the d = 64 tcgen05 kernels): the float64
+    forwards of the padded model equal the d-unit model's."""
+    from oracle import model_oracle as mo
+    from paper_2511_08568_b200.model import pad_params
+    sizes = [40, 25, 60]
+    rng = np.random.default_rng(3)
+    gid = rng.integers(0, 125, (33, 15))
+    tid = np.searchsorted(np.cumsum([0] + sizes), gid, side="right") - 1
+    for d in (8, 32):
+        cp = rb.init_params("caching", sizes, dim=d, seed=0, init_scale=0.6)
+        pp = rb.init_params("prefetch", sizes, dim=d, seed=1, init_scale=0.6)
+        a = mo.caching_logits(cp.arrays, d, 1, gid, tid)
+        b = mo.caching_logits(pad_params(cp).arrays, 64, 1, gid, tid)
+        assert np.max(np.abs(a - b)) < 1e-12
+        a = mo.prefetch_logits(pp.arrays, d, 2, 5, gid, tid)
+        b = mo.prefetch_logits(pad_params(pp).arrays, 64, 2, 5, gid, tid)
+        assert np.max(np.abs(a - b)) < 1e-12
