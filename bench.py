@@ -79,7 +79,8 @@ def parse():
     ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
     ap.add_argument("--pieces", type=int, default=8, help="replay pipeline pieces")
     ap.add_argument("--model-sms", type=int, default=136, help="SMs the forwards may use")
-    ap.add_argument("--config", type=int, default=None, choices=[2, 3],
+    ap.add_argument("--batch", type=int, default=512, help="config 4: samples per batch")
+    ap.add_argument("--config", type=int, default=None, choices=[2, 3, 4],
                     help="workload: 2 (single-GPU config, the N=1 default) or 3 (856 tables, "
                          "500 M accesses, table-sharded: the N>1 default)")
     ap.add_argument("--no-dropin", action="store_true",
@@ -108,6 +109,22 @@ def parse():
 
 
 def workload(args, rank):
+    if args.config == 4:
+        return {
+            "workload": f"config4: DLRM embedding stage on the config-2 trace (256 tables x 50k "
+                        f"rows, 25M accesses) in serving batches of {args.batch} samples x "
+                        f"{args.tables} tables x pooling {args.pool} (trace order; the trace has "
+                        "no query boundaries, SPEC.md:104); per batch: caching + prefetch LSTM "
+                        "forwards, 32-way priority-buffer replay, K5 refresh of changed buffer "
+                        f"rows from pinned host memory ({args.row_dim} fp32), K6 EmbeddingBag(sum); "
+                        "the next batch's forwards overlap this batch's replay/K5/K6; one GPU "
+                        "(no all-to-all)",
+            "batch_samples": args.batch, "tables": args.tables, "rows_per_table": args.rows,
+            "pooling": args.pool, "row_dim": args.row_dim, "accesses": args.accesses,
+            "zipf": 1.05, "stickiness": 0.4, "pool": 32, "trace_seed": 2, "dim": args.dim,
+            "init_scale": args.init_scale, "ways": 32, "eviction_speed": 4, "window_ratio": 3,
+            "l2": "inputs larger than L2 (6.6 GB of host rows, GBs of folded tables)",
+        }
     if args.config == 3:
         return {
             "workload": f"config3: synthetic Zipf trace, {args.tables} tables x {args.rows} rows, "
@@ -435,6 +452,11 @@ def main():
         raise SystemExit("--config 3 under torchrun runs one shard per rank (--shards = world)")
     if args.impl == "reference":
         return run_reference(args, rank, world, torch, dist)
+    if args.config == 4:
+        if world > 1:
+            raise SystemExit("--config 4 runs on one GPU here (the all-to-all is tested, "
+                             "tests/test_gpu_rows.py)")
+        return run_config4(args, torch)
 
     import paper_2511_08568_b200 as rb
     from paper_2511_08568_b200 import _native
@@ -695,6 +717,132 @@ def main():
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_config4(args, torch):
+    """Config 4 on one GPU: the hot path in DLRM serving batches with the
+    embedding stage (K5 refresh + K6 pooling) after each batch's replay."""
+    import paper_2511_08568_b200 as rb
+    from paper_2511_08568_b200 import _native
+    from paper_2511_08568_b200.engine import RowStore
+    from paper_2511_08568_b200.model import DeviceModel, init_params_device
+    from paper_2511_08568_b200.pipeline import HotPath
+    t0 = time.time()
+    t = rb.generate_trace(rb.TraceGenConfig([args.rows] * args.tables, args.accesses, 1.05, 0.4,
+                                            32, 2))
+    n = len(t)
+    U = t.unique_count
+    C = int(math.floor(0.2 * U))
+    C32 = C - C % 32
+    cp, emb_c = init_params_device("caching", t.table_sizes, dim=args.dim, seed=0,
+                                   init_scale=args.init_scale)
+    pp, emb_p = init_params_device("prefetch", t.table_sizes, dim=args.dim, seed=1,
+                                   init_scale=args.init_scale)
+    D, P = args.row_dim, args.pool
+    per_batch = args.batch * args.tables * P
+    Kb = -(-per_batch // 15)                     # chunks per serving batch
+    V = t.total_ids
+    host = torch.empty((V, D), dtype=torch.float32, pin_memory=True)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(123)
+    for r0 in range(0, V, 1 << 20):
+        r1 = min(V, r0 + (1 << 20))
+        host[r0:r1].copy_(torch.randn((r1 - r0, D), device="cuda", generator=gen))
+    torch.cuda.synchronize()
+    st = {}
+
+    def hook(k0, k1, last):
+        a0, a1 = 15 * k0, (n if last else 15 * k1)
+        nb = -(-(a1 - a0) // P)
+        off = st["offsets"].get(a1 - a0)
+        if off is None:   # the last batch's length (prepared before the timed steps)
+            off = torch.arange(0, nb * P + 1, P, dtype=torch.int64, device="cuda")
+            off[-1] = a1 - a0
+            st["offsets"][a1 - a0] = off
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        evs[0].record()
+        st["rows"].refresh()
+        evs[1].record()
+        st["rows"].pool(st["hp"].gids[a0:a1], off, st["out"][:nb])
+        evs[2].record()
+        st["ev"].append(evs)
+
+    hp = HotPath(DeviceModel(cp, emb_c), DeviceModel(pp, emb_p), t.table_sizes, C32, n, ways=32,
+                 eviction_speed=4, lru_capacity=C32, lru_ways=32, model_sms=args.model_sms,
+                 piece_chunks=Kb, piece_hook=hook)
+    del emb_c, emb_p
+    rows = RowStore(hp.buffer, host)
+    st.update(hp=hp, rows=rows, ev=[], offsets={},
+              out=torch.empty((-(-per_batch // P) + 8, D), dtype=torch.float32, device="cuda"))
+    full = -(-(15 * Kb) // P)
+    off = torch.arange(0, full * P + 1, P, dtype=torch.int64, device="cuda")
+    off[-1] = 15 * Kb
+    st["offsets"][15 * Kb] = off
+    src = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
+    hp.gids[:n].copy_(src)
+    setup_s = time.time() - t0
+    for _ in range(args.warmup):
+        hp.launch(n)
+    torch.cuda.synchronize()
+    st["ev"] = []
+    rows.copied.zero_()
+    rows.src.zero_()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(0)
+    launches0 = _native.lib().recmg_launch_count()
+    start.record()
+    for _ in range(args.steps):
+        hp.enable_stage_timing(True)
+        hp.launch(n)
+    end.record()
+    torch.cuda.synchronize()
+    launches = _native.lib().recmg_launch_count() - launches0
+    clk = clocks.stop()
+    ms = start.elapsed_time(end) / args.steps
+    rep, lru = hp.report()
+    nbatch = len(hp._piece_bounds(hp.K))
+    k5 = [e[0].elapsed_time(e[1]) for e in st["ev"]]
+    k6 = [e[1].elapsed_time(e[2]) for e in st["ev"]]
+    copied = int(rows.copied.item()) // args.steps
+    hb, hh = (int(x) // args.steps for x in rows.src.cpu().numpy())
+    # PCIe H2D reference: pinned cudaMemcpy of 1 GiB, best of 5
+    srcb = host.view(-1)[: (1 << 28)]
+    dst = torch.empty_like(srcb, device="cuda")
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); dst.copy_(srcb, non_blocking=True); e1.record(); torch.cuda.synchronize()
+        best = max(best, srcb.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del dst
+    k5_ms, k6_ms = sum(k5) / args.steps, sum(k6) / args.steps
+    line = {
+        "metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (reference generator, bit-exact) + reference init_params weights + "
+                "N(0,1) host rows",
+        "config": workload(args, 0),
+        "tuning": {"model_sms": args.model_sms, "chunks_per_batch": Kb},
+        "batches_per_step": nbatch, "ms_per_batch": ms / nbatch,
+        "quality": {"on_demand": rep.on_demand, "prefetch_inserts": rep.prefetch_inserts,
+                    "lru32_misses": lru[1], "cache_hits": rep.cache_hits,
+                    "prefetch_hits": rep.prefetch_hits},
+        "k5": {"ms_per_step": k5_ms, "ms_per_batch": k5_ms / nbatch,
+               "rows_copied_per_step": copied, "bytes_per_step": copied * D * 4,
+               "demand_plus_insert_bytes_per_step": (rep.on_demand + rep.prefetch_inserts) * D * 4,
+               "pcie_gbs": copied * D * 4 / (k5_ms / 1e3) / 1e9 if k5_ms else None,
+               "pcie_h2d_peak_gbs": best, "pcie_frac": (copied * D * 4 / (k5_ms / 1e3) / 1e9) / best
+               if k5_ms else None,
+               "note": "rows of slots whose occupant changed during the batch (a slot refilled "
+                       "twice in one batch is copied once), read over PCIe by UVA zero-copy"},
+        "k6": {"ms_per_step": k6_ms, "ms_per_batch": k6_ms / nbatch, "bags_per_batch": full,
+               "rows_from_hbm_per_step": hb, "rows_from_host_per_step": hh,
+               "hbm_gbs": (hb * D * 4 + n * 4 + full * nbatch * D * 4) / (k6_ms / 1e3) / 1e9,
+               "host_pcie_gbs": hh * D * 4 / (k6_ms / 1e3) / 1e9},
+        "stages_ms": {k: v for k, v in hp.stage_times().items()} if hp.events else None,
+        "gpu_launches": int(launches // args.steps), "clocks": clk, "setup_s": setup_s,
+    }
+    print(json.dumps(line), flush=True)
 
 
 def reference_workload(args, idx):

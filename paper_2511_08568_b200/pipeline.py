@@ -26,20 +26,25 @@ from .trace import num_chunks
 
 
 class HotPath:
-    STAGES = ("table_ids", "caching_fwd", "prefetch_fwd", "replay", "lru", "tail")
+    STAGES = ("table_ids", "caching_fwd", "prefetch_fwd", "replay", "lru", "tail", "hook")
 
     def __init__(self, caching: ModelParameters | DeviceModel | None,
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
                  n_max: int, ways: int | None = 32, eviction_speed: int = 4,
                  lru_capacity: int | None = None, lru_ways: int | None = 32, l_in: int = 15,
                  l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 136,
-                 shard=None, replay_priority: bool = True):
+                 shard=None, replay_priority: bool = True, piece_chunks: int | None = None,
+                 piece_hook=None):
         """pieces > 1 pipelines the replay: chunks are scored in `pieces`
         ranges on the main stream while earlier ranges replay on a side stream
         (recmg_replay_chunks continues the buffer state, so the result is the
         same as one replay); the LRU comparator runs on a third stream from
         the start.  The TC forwards then use `model_sms` SMs, leaving the rest
-        to the replay CTAs.
+        to the replay CTAs.  piece_chunks fixes the piece length in chunks (a
+        serving batch) instead of dividing the trace into `pieces`;
+        piece_hook(k0, k1, last) runs on the replay stream right after each
+        piece's replay (the DLRM embedding stage: K5 row refresh + K6 pooling
+        of that batch), so it overlaps the next piece's forwards.
 
         shard (shard.TableShard): the models are a table shard's, packed over
         its local vocabulary (shard.init_params_shard, DeviceModel with
@@ -85,7 +90,9 @@ class HotPath:
         if lru_capacity:
             self.lru = LruSim(lru_capacity, self.total_ids, lru_ways, self.n_max)
         self.pieces = max(1, int(pieces))
-        self.model_sms = int(model_sms) if self.pieces > 1 else 148
+        self.piece_chunks = int(piece_chunks) if piece_chunks else None
+        self.piece_hook = piece_hook
+        self.model_sms = int(model_sms) if (self.pieces > 1 or self.piece_chunks) else 148
         # the replay and the LRU run under the forwards on the SMs they leave;
         # high priority makes the block scheduler hand freed SMs to them first
         # (at every forward launch boundary), so the replay does not lag
@@ -117,6 +124,9 @@ class HotPath:
         return out
 
     def _piece_bounds(self, K):
+        if self.piece_chunks:
+            b = list(range(0, K, self.piece_chunks)) + [K]
+            return [(b[i], b[i + 1]) for i in range(len(b) - 1)]
         if self.pieces <= 1 or K < 128 * self.pieces:
             return [(0, K)]
         step = (K // self.pieces + 127) // 128 * 128
@@ -223,6 +233,10 @@ class HotPath:
                     self._ev("replay", self.s_replay)
                     self.buffer.run_chunks(g, k0, k1, i == len(pieces) - 1, bits, pf)
                     self._ev("replay", self.s_replay)
+                    if self.piece_hook is not None:
+                        self._ev("hook", self.s_replay)
+                        self.piece_hook(k0, k1, i == len(pieces) - 1)
+                        self._ev("hook", self.s_replay)
                     if host_src is not None and k1 > k0:
                         for r in range(2):   # contiguous rows: plain async D2H copies
                             self.cov_host[r, k0:k1].copy_(self.buffer._cov[r, k0:k1],
