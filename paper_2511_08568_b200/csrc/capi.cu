@@ -77,10 +77,23 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     if (p.E == 0) return RECMG_OK;
     if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
     StateView st = state_view(state, cfg, p.g);
-    build_events_kernel<<<(unsigned)imin64((p.E + 255) / 256, 16 * kSmCount), 256, 0, s>>>(
-        gids, n, l_in, bits, pf, pf_stride, p.K, p.k0, p.nk, p.tail ? 1 : 0, (uint32_t)p.g.S,
-        p.ev, p.vv, counters, access_class);
-    RECMG_LAUNCH_CHECK();
+    const uint32_t magic = set_magic((uint32_t)p.g.S);
+    int64_t i_begin = 0;
+    if (l_in <= 16 && p.nk > 0) {   // thread per chunk, then the tail below
+        build_chunk_events_kernel<16><<<(unsigned)imin64((p.nk + 127) / 128, 16 * kSmCount), 128,
+                                        0, s>>>(gids, l_in, bits, pf, pf_stride, p.K, p.k0, p.nk,
+                                                (uint32_t)p.g.S, magic, p.ev, p.vv, counters,
+                                                access_class);
+        RECMG_LAUNCH_CHECK();
+        i_begin = p.nk * p.Ec;
+    }
+    if (p.E > i_begin) {
+        build_events_kernel<<<(unsigned)imin64((p.E - i_begin + 255) / 256, 16 * kSmCount), 256, 0,
+                              s>>>(gids, n, l_in, bits, pf, pf_stride, p.K, p.k0, p.nk,
+                                   p.tail ? 1 : 0, (uint32_t)p.g.S, magic, i_begin, p.ev, p.vv,
+                                   counters, access_class);
+        RECMG_LAUNCH_CHECK();
+    }
     uint32_t *ev = p.ev, *vv = p.vv;
     ReplayArgs ra;
     memset(&ra, 0, sizeof(ra));
@@ -89,6 +102,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
         if (rc) return rc;
         ra.seg_start = p.pb.seg_start;
         ra.seg_end = p.pb.seg_end;
+        ra.heavy = p.g.wide ? nullptr : p.pb.heavy;
     }
     ra.ev = ev;
     ra.vals = vv;
@@ -340,6 +354,7 @@ int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *g
         if (rc) return rc;
         ra.seg_start = p.pb.seg_start;
         ra.seg_end = p.pb.seg_end;
+        ra.heavy = g.wide ? nullptr : p.pb.heavy;
     }
     ra.ev = k;
     ra.vals = v;

@@ -24,6 +24,9 @@ namespace recmg {
 
 constexpr int kSmCount = 148;  // B200: 2 dies x 74 SMs
 constexpr int64_t kSmemMaxWays = 4096;  // sets up to this many ways replay in shared memory
+// sets whose event segment is far above the mean are replayed by the first
+// CTAs of the launch (so the longest dependency chains start first)
+constexpr int kHeavySets = 32;
 
 // Event word: [type:2][gid:30]
 enum : uint32_t { EV_SERVE = 0u, EV_UPD0 = 1u, EV_UPD1 = 2u, EV_PREFETCH = 3u };

@@ -214,6 +214,20 @@ __global__ void seg_bounds_kernel(const uint32_t *__restrict__ k, int64_t N, uin
     if (i == N - 1 || set_of_event(k[i + 1], S) != s) end[s] = (uint32_t)(i + 1);
 }
 
+// Sets whose segment is much longer than the mean (Zipf skew: one set can
+// hold half of a shard's events): listed so the replay launch starts them
+// first instead of in set order behind thousands of short sets.
+__global__ void heavy_sets_kernel(const uint32_t *__restrict__ start,
+                                  const uint32_t *__restrict__ end, int64_t S, uint32_t thr,
+                                  int32_t *__restrict__ heavy) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    if (end[s] > start[s] && end[s] - start[s] >= thr) {
+        const int i = atomicAdd(heavy, 1);
+        if (i < kHeavySets) heavy[1 + i] = (int32_t)s;
+    }
+}
+
 int partition_passes(int64_t S) {
     int bits = 0;
     while ((int64_t(1) << bits) < S + 1) bits++;  // buckets 0..S
@@ -232,6 +246,7 @@ void partition_plan(Arena &a, PartitionBuffers &pb, int64_t N, int64_t S, bool v
     pb.partial = a.take<uint32_t>(scan_workspace_elems(M));
     pb.seg_start = a.take<uint32_t>((size_t)S + 1);
     pb.seg_end = a.take<uint32_t>((size_t)S + 1);
+    pb.heavy = a.take<int32_t>(1 + kHeavySets);
 }
 
 int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaStream_t s) {
@@ -266,6 +281,12 @@ int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaSt
     vals = vin;
     seg_bounds_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(keys, N, (uint32_t)S,
                                                                   pb.seg_start, pb.seg_end);
+    RECMG_LAUNCH_CHECK();
+    RECMG_CUDA_TRY(cudaMemsetAsync(pb.heavy, 0, sizeof(int32_t), s));
+    const int64_t mean = N / (S > 0 ? S : 1);
+    const uint32_t thr = (uint32_t)(mean * 8 > 4096 ? mean * 8 : 4096);
+    heavy_sets_kernel<<<(unsigned)((S + 255) / 256), 256, 0, s>>>(pb.seg_start, pb.seg_end, S,
+                                                                   thr, pb.heavy);
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
 }

@@ -10,6 +10,7 @@ struct PartitionBuffers {
     uint32_t *alt_keys = nullptr, *alt_vals = nullptr;
     uint32_t *hist = nullptr, *offs = nullptr, *partial = nullptr;
     uint32_t *seg_start = nullptr, *seg_end = nullptr;  // [S+1]
+    int32_t *heavy = nullptr;  // [1 + kHeavySets]: count, then the heaviest sets
 };
 
 int partition_passes(int64_t S);

@@ -34,15 +34,29 @@ namespace recmg {
 // position that no other way of the set can pass in between), so it is
 // counted here and emitted as an empty event.  Under Zipf skew with a sticky
 // pool this removes most of the hottest set's events.
+//
+// set = gid % S with one multiply-high: q = umulhi(g, M), M = ceil(2^32 / S),
+// is floor(g / S) or one more for every g < 2^30 (g*M/2^32 - g/S < 1/4), so
+// r = g - q*S needs at most one correction (M = ceil(2^32/S) needs S >= 2).
+__device__ __forceinline__ uint32_t set_of(uint32_t g, uint32_t S, uint32_t M) {
+    if (S == 1) return 0;
+    const uint32_t q = __umulhi(g, M);
+    const int64_t r = (int64_t)g - (int64_t)q * S;
+    return (uint32_t)(r < 0 ? r + S : r);
+}
+
 __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n, int32_t l_in,
                                     const uint8_t *__restrict__ bits,
                                     const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
                                     int64_t k0, int64_t nk, int with_tail, uint32_t S,
+                                    uint32_t M, int64_t i_begin,
                                     uint32_t *__restrict__ ev, uint32_t *__restrict__ vals,
                                     recmg_counters *__restrict__ ctr,
                                     uint8_t *__restrict__ access_class) {
     // events of chunks [k0, k0+nk) (+ the tail when with_tail, i.e. k0+nk == K);
-    // local event i has global position k0*Ec + i
+    // local event i has global position k0*Ec + i; this launch builds events
+    // [i_begin, E) (the thread-per-chunk kernel below builds the chunks' ones
+    // when l_in <= 16, this one the tail)
     const int64_t Ec = 2 * (int64_t)l_in + pf_stride;
     const int64_t chunk_ev = nk * Ec;
     const int64_t E = chunk_ev + (with_tail ? (n - K * l_in) : 0);
@@ -56,12 +70,60 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
         int64_t q = acc - 1;
         while (q >= block_start && (uint32_t)gids[q] != g) q--;
         if (q < block_start) return false;
-        const uint32_t set = g % S;
+        const uint32_t set = set_of(g, S, M);
         for (int64_t p = q + 1; p < acc; p++)
-            if ((uint32_t)gids[p] % S == set) return false;
+            if (set_of((uint32_t)gids[p], S, M) == set) return false;
         return true;
     };
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
+    // Across chunks (Zipf skew puts one id's accesses in nearly every chunk):
+    // the serve at `acc`, the first access to its set in block [bs, ...), is
+    // a guaranteed untagged hit when the previous chunk's last access to the
+    // set names the same id and none of that chunk's prefetches into the set
+    // names another id -- between the two, the set only sees that chunk's
+    // updates (no residency change) and prefetches of the id itself (resident:
+    // priority only, tag unchanged), runtime.py:83-137.
+    auto cross_serve = [&](int64_t bs, int64_t acc) {
+        const int64_t kp = bs / l_in - 1;        // the previous chunk
+        if (kp < 0) return false;
+        const uint32_t g = (uint32_t)gids[acc];
+        const uint32_t set = set_of(g, S, M);
+        for (int64_t p = bs; p < acc; p++)
+            if (set_of((uint32_t)gids[p], S, M) == set) return false;
+        int64_t q = bs - 1;
+        while (q >= kp * l_in && set_of((uint32_t)gids[q], S, M) != set) q--;
+        if (q < kp * l_in || (uint32_t)gids[q] != g) return false;
+        if (pf) {
+            const int32_t *row = pf + kp * pf_stride;
+            for (int j = 0; j < pf_stride && row[j] >= 0; j++)
+                if (set_of((uint32_t)row[j], S, M) == set && (uint32_t)row[j] != g) return false;
+        }
+        return true;
+    };
+    // The (last) keep-bit update of id g in chunk k is dead -- overwritten
+    // before any eviction in its set reads priorities -- when the first event
+    // of the set after it is a prefetch of g (priority = es if resident), or,
+    // with no prefetch into the set, when chunk k+1 touches the set and only
+    // with g: those serves are hits (no eviction) and chunk k+1's last update
+    // of g overwrites the priority (runtime.py:100-112, 126-137).  If g is not
+    // resident the update is a no-op either way.
+    auto dead_update = [&](int64_t k, uint32_t g) {
+        const uint32_t set = set_of(g, S, M);
+        if (pf) {
+            const int32_t *row = pf + k * pf_stride;
+            for (int j = 0; j < pf_stride && row[j] >= 0; j++)
+                if (set_of((uint32_t)row[j], S, M) == set) return (uint32_t)row[j] == g;
+        }
+        if (k + 1 >= K) return false;
+        bool touched = false;
+        for (int64_t p = (k + 1) * l_in; p < (k + 2) * l_in; p++) {
+            const uint32_t x = (uint32_t)gids[p];
+            if (set_of(x, S, M) != set) continue;
+            if (x != g) return false;
+            touched = true;
+        }
+        return touched;
+    };
+    for (int64_t i = i_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
          i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t e;
         if (i < chunk_ev) {
@@ -69,7 +131,7 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
             const int64_t k = k0 + kk;
             if (r < l_in) {
                 const int64_t acc = k * l_in + r;
-                if (dup_serve(k * l_in, acc)) {
+                if (dup_serve(k * l_in, acc) || cross_serve(k * l_in, acc)) {
                     e = ev_make(EV_SERVE, kGidMask);
                     collapsed++;
                     if (access_class) access_class[acc] = 0;
@@ -85,8 +147,9 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
                 bool later = false;
                 for (int64_t q = j + 1; q < l_in; q++) later |= (gids[k * l_in + q] == gj);
                 uint32_t b = bits ? (uint32_t)bits[k * l_in + j] : 0u;
-                e = later ? ev_make(EV_UPD0, kGidMask)
-                          : ev_make(b ? EV_UPD1 : EV_UPD0, (uint32_t)gj);
+                e = (later || dead_update(k, (uint32_t)gj))
+                        ? ev_make(EV_UPD0, kGidMask)
+                        : ev_make(b ? EV_UPD1 : EV_UPD0, (uint32_t)gj);
             } else {
                 // -1 pads a row: that entry and everything after it is empty
                 const int32_t *row = pf + k * pf_stride;
@@ -97,7 +160,7 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
             }
         } else {
             const int64_t acc = K * l_in + (i - chunk_ev);
-            if (dup_serve(K * l_in, acc)) {
+            if (dup_serve(K * l_in, acc) || cross_serve(K * l_in, acc)) {
                 e = ev_make(EV_SERVE, kGidMask);
                 collapsed++;
                 if (access_class) access_class[acc] = 0;
@@ -112,6 +175,121 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
     if ((threadIdx.x & 31) == 0 && collapsed)
         atomicAdd((unsigned long long *)&ctr->cache_hits, (unsigned long long)collapsed);
 }
+
+// The same events, one thread per chunk (l_in <= LM): the chunk's ids and
+// sets, and those of its neighbours, are held in registers, so the
+// within-chunk / cross-chunk collapsing rules above cost register compares
+// instead of per-event scans through global memory.
+template <int LM>
+__global__ void __launch_bounds__(128)
+build_chunk_events_kernel(const int32_t *__restrict__ gids, int32_t l_in,
+                          const uint8_t *__restrict__ bits, const int32_t *__restrict__ pf,
+                          int32_t pf_stride, int64_t K, int64_t k0, int64_t nk, uint32_t S,
+                          uint32_t M, uint32_t *__restrict__ ev, uint32_t *__restrict__ vals,
+                          recmg_counters *__restrict__ ctr, uint8_t *__restrict__ access_class) {
+    const int64_t Ec = 2 * (int64_t)l_in + pf_stride;
+    unsigned collapsed = 0;
+    for (int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < nk;
+         kk += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = k0 + kk;
+        uint32_t g[LM], st[LM], pg[LM], ps[LM], ng[LM], ns[LM];
+#pragma unroll
+        for (int r = 0; r < LM; r++) {
+            st[r] = ps[r] = ns[r] = 0xFFFFFFFFu;   // no set
+            g[r] = pg[r] = ng[r] = 0;
+            if (r < l_in) {
+                g[r] = (uint32_t)__ldg(gids + k * l_in + r);
+                st[r] = set_of(g[r], S, M);
+                if (k > 0) {
+                    pg[r] = (uint32_t)__ldg(gids + (k - 1) * l_in + r);
+                    ps[r] = set_of(pg[r], S, M);
+                }
+                if (k + 1 < K) {
+                    ng[r] = (uint32_t)__ldg(gids + (k + 1) * l_in + r);
+                    ns[r] = set_of(ng[r], S, M);
+                }
+            }
+        }
+        const int32_t *prow = (pf && k > 0) ? pf + (k - 1) * pf_stride : nullptr;
+        const int32_t *crow = pf ? pf + k * pf_stride : nullptr;
+        uint32_t *out = ev + kk * Ec;
+        // serves (runtime.py:254-264) with the within- and cross-chunk hit rules
+#pragma unroll
+        for (int r = 0; r < LM; r++) {
+            if (r >= l_in) continue;
+            bool found = false, dup = false;
+#pragma unroll
+            for (int q = LM - 1; q >= 0; q--)
+                if (q < r && !found && st[q] == st[r]) { found = true; dup = g[q] == g[r]; }
+            bool coll = dup;
+            if (!found && k > 0) {
+                bool f2 = false;
+                uint32_t last = 0;
+#pragma unroll
+                for (int q = LM - 1; q >= 0; q--)
+                    if (!f2 && ps[q] == st[r]) { f2 = true; last = pg[q]; }
+                coll = f2 && last == g[r];
+                if (coll && prow)
+                    for (int j = 0; j < pf_stride && prow[j] >= 0; j++)
+                        if (set_of((uint32_t)prow[j], S, M) == st[r] && (uint32_t)prow[j] != g[r]) {
+                            coll = false;
+                            break;
+                        }
+            }
+            if (coll) {
+                collapsed++;
+                if (access_class) access_class[k * l_in + r] = 0;
+            }
+            out[r] = ev_make(EV_SERVE, coll ? kGidMask : g[r]);
+        }
+        // keep-bit updates (runtime.py:126-130): the last of an id in the
+        // chunk, unless dead (overwritten before any eviction in its set)
+#pragma unroll
+        for (int j = 0; j < LM; j++) {
+            if (j >= l_in) continue;
+            bool later = false;
+#pragma unroll
+            for (int q = 0; q < LM; q++) later |= (q > j && q < l_in && g[q] == g[j]);
+            bool dead = later;
+            if (!dead) {
+                bool decided = false;
+                if (crow)
+                    for (int q = 0; q < pf_stride && crow[q] >= 0; q++)
+                        if (set_of((uint32_t)crow[q], S, M) == st[j]) {
+                            decided = true;
+                            dead = (uint32_t)crow[q] == g[j];
+                            break;
+                        }
+                if (!decided && k + 1 < K) {
+                    bool touched = false, only = true;
+#pragma unroll
+                    for (int q = 0; q < LM; q++)
+                        if (ns[q] == st[j]) { touched = true; only = only && ng[q] == g[j]; }
+                    dead = touched && only;
+                }
+            }
+            const uint32_t b = bits ? (uint32_t)bits[k * l_in + j] : 0u;
+            out[l_in + j] = dead ? ev_make(EV_UPD0, kGidMask) : ev_make(b ? EV_UPD1 : EV_UPD0, g[j]);
+        }
+        // prefetches (runtime.py:131-137); -1 ends a row
+        bool pad = false;
+        for (int j = 0; j < pf_stride; j++) {
+            const int32_t x = crow[j];
+            pad |= x < 0;
+            out[2 * l_in + j] = ev_make(EV_PREFETCH, pad ? kGidMask : (uint32_t)x);
+        }
+        if (vals)
+            for (int64_t i = 0; i < Ec; i++) vals[kk * Ec + i] = (uint32_t)(k * Ec + i);
+    }
+    collapsed = __reduce_add_sync(0xFFFFFFFFu, collapsed);
+    if ((threadIdx.x & 31) == 0 && collapsed)
+        atomicAdd((unsigned long long *)&ctr->cache_hits, (unsigned long long)collapsed);
+}
+
+template __global__ void build_chunk_events_kernel<16>(const int32_t *, int32_t, const uint8_t *,
+                                                       const int32_t *, int32_t, int64_t, int64_t,
+                                                       int64_t, uint32_t, uint32_t, uint32_t *,
+                                                       uint32_t *, recmg_counters *, uint8_t *);
 
 // event position -> access index (only meaningful for serve events)
 __device__ __forceinline__ int64_t access_of_event(int64_t pos, int64_t Ec, int64_t K,
@@ -349,7 +527,20 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
     extern __shared__ __align__(16) uint8_t dsm[];
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t set = (int64_t)blockIdx.x * warps_per_cta + warp;
+    int64_t set = (int64_t)blockIdx.x * warps_per_cta + warp;
+    if (a.heavy) {
+        // CTAs [0, kHeavySets) replay the listed heavy sets, the rest every
+        // other set in order (one warp per CTA when heavy sets are listed)
+        const int nh = min(__ldg(a.heavy), kHeavySets);
+        if (blockIdx.x < kHeavySets) {
+            if ((int)blockIdx.x >= nh) return;
+            set = __ldg(a.heavy + 1 + blockIdx.x);
+        } else {
+            set = (int64_t)blockIdx.x - kHeavySets;
+            const bool listed = lane < nh && __ldg(a.heavy + 1 + lane) == (int32_t)set;
+            if (__any_sync(0xFFFFFFFFu, listed)) return;
+        }
+    }
     if (set >= a.S) return;
     const int W = (int)a.W;
     const int64_t sbase = set * a.W;
@@ -1179,7 +1370,7 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         // CTAs co-reside with other kernels' CTAs (pipelined with the forwards)
         const int wpc = 1;
         const size_t smem = (size_t)wpc * bytes;
-        const unsigned grid = (unsigned)((nsets + wpc - 1) / wpc);
+        const unsigned grid = (unsigned)((nsets + wpc - 1) / wpc + (a.heavy ? kHeavySets : 0));
 #define RECMG_SMEM_LAUNCH(P, C)                                                            \
     do {                                                                                    \
         RECMG_CUDA_TRY(cudaFuncSetAttribute(replay_smem_kernel<P, C>,                       \

@@ -11,9 +11,23 @@ __global__ void build_events_kernel(const int32_t *__restrict__ gids, int64_t n,
                                     const uint8_t *__restrict__ bits,
                                     const int32_t *__restrict__ pf, int32_t pf_stride, int64_t K,
                                     int64_t k0, int64_t nk, int with_tail, uint32_t S,
+                                    uint32_t M, int64_t i_begin,
                                     uint32_t *__restrict__ ev, uint32_t *__restrict__ vals,
                                     recmg_counters *__restrict__ ctr,
                                     uint8_t *__restrict__ access_class);
+template <int LM>
+__global__ void build_chunk_events_kernel(const int32_t *__restrict__ gids, int32_t l_in,
+                                          const uint8_t *__restrict__ bits,
+                                          const int32_t *__restrict__ pf, int32_t pf_stride,
+                                          int64_t K, int64_t k0, int64_t nk, uint32_t S,
+                                          uint32_t M, uint32_t *__restrict__ ev,
+                                          uint32_t *__restrict__ vals,
+                                          recmg_counters *__restrict__ ctr,
+                                          uint8_t *__restrict__ access_class);
+// M = ceil(2^32 / S) for set_of (0 for S = 1)
+inline uint32_t set_magic(uint32_t S) {
+    return S <= 1 ? 0u : (uint32_t)((((uint64_t)1 << 32) + S - 1) / S);
+}
 __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t k0, int64_t nk,
                                       int32_t l_in, int32_t l_win, const int32_t *__restrict__ pf,
                                       int32_t pf_stride, uint16_t *__restrict__ cov_num,
@@ -33,6 +47,7 @@ struct ReplayArgs {
     const uint32_t *ev;
     const uint32_t *vals;
     const uint32_t *seg_start, *seg_end;
+    const int32_t *heavy;      // [1 + kHeavySets] or null: sets started first
     int64_t E;
     int64_t S, W;
     int32_t es;
