@@ -668,7 +668,11 @@ def main():
                     "cache_hits": c[0], "prefetch_hits": c[1], "prefetch_issued": c[3],
                     "prefetch_useful": c[4], "evictions": c[5], "prefetch_inserts": c[6],
                     "coverage_rank0": rep.coverage, "capacity_rank0": C32, "unique_rank0": U,
-                    "comparators_rank0": comp},
+                    "comparators_rank0": comp,
+                    "note": "random-init models (training is out of the hot path's scope): "
+                            "their decisions carry no information, so on-demand fetches exceed "
+                            "the 32-way LRU's misses; the counts measure the replay of these "
+                            "decisions, bit-exact vs the oracle (parity), not RecMG's quality"},
         "stages_ms": mean,
         "gpu_launches": int(launches // args.steps),
         "roofline": roof,
