@@ -367,21 +367,38 @@ def measure_rows(args, hp, n, torch):
             "note": "K5/K6 run after the timed replay; not part of `value`"}
 
 
-def build_state_config3(args, idx, torch, device=True):
-    """Config 3: stream the whole trace, assign tables by access count,
-    keep shard `idx`'s order-preserving sub-trace, draw its local models."""
+def _stream_config3(args, sizes):
     import paper_2511_08568_b200 as rb
-    from paper_2511_08568_b200 import shard as shd
-    from paper_2511_08568_b200.trace import Trace, TraceStream
-    t0 = time.time()
-    sizes = [args.rows] * args.tables
+    from paper_2511_08568_b200.trace import TraceStream
     ts = TraceStream(rb.TraceGenConfig(sizes, args.accesses, 1.05, 0.4, 32, 3))
     g = np.empty(args.accesses, dtype=np.int32)
-    counts = np.zeros(args.tables, dtype=np.int64)
     for b in ts.blocks(1 << 24):
         g[ts.pos - len(b):ts.pos] = b
-        counts += np.bincount(b // args.rows, minlength=args.tables)
-    del ts
+    return g
+
+
+def build_state_config3(args, idx, torch, device=True, dist=None):
+    """Config 3: stream the whole trace, assign tables by access count,
+    keep shard `idx`'s order-preserving sub-trace, draw its local models.
+    Under several ranks the trace is streamed once per node (local rank 0,
+    into /dev/shm) and mapped by the others."""
+    from paper_2511_08568_b200 import shard as shd
+    from paper_2511_08568_b200.trace import Trace
+    t0 = time.time()
+    sizes = [args.rows] * args.tables
+    shm = None
+    if dist is not None and os.path.isdir("/dev/shm"):
+        shm = f"/dev/shm/recmg_c3_{args.tables}x{args.rows}_{args.accesses}_{os.getppid()}.npy"
+        if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+            np.save(shm + ".tmp.npy", _stream_config3(args, sizes))
+            os.replace(shm + ".tmp.npy", shm)
+        dist.barrier()
+        g = np.load(shm, mmap_mode="r")
+    else:
+        g = _stream_config3(args, sizes)
+    counts = np.zeros(args.tables, dtype=np.int64)
+    for i in range(0, len(g), 1 << 24):
+        counts += np.bincount(np.asarray(g[i:i + (1 << 24)]) // args.rows, minlength=args.tables)
     assign = shd.assign_tables(counts, args.shards_eff)
     mine = assign == idx
     parts = []
@@ -391,6 +408,10 @@ def build_state_config3(args, idx, torch, device=True):
     del g
     sub = np.concatenate(parts)
     del parts
+    if shm is not None:
+        dist.barrier()        # every rank has its sub-trace: drop the shared copy
+        if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+            os.unlink(shm)
     t = Trace(sub, sizes)
     t._unique = int(np.count_nonzero(np.bincount(sub, minlength=sum(sizes))))
     U = t.unique_count
@@ -404,11 +425,12 @@ def build_state_config3(args, idx, torch, device=True):
     return t, U, C, C32, cp, emb_c, pp, emb_p, time.time() - t0, sh
 
 
-def build_state(args, rank, torch):
+def build_state(args, rank, torch, dist=None):
     import paper_2511_08568_b200 as rb
     from paper_2511_08568_b200.model import DeviceModel, init_params_device
     if args.config == 3:
-        return build_state_config3(args, rank if args.world > 1 else args.shard_index, torch)
+        return build_state_config3(args, rank if args.world > 1 else args.shard_index, torch,
+                                   dist=dist)
     t0 = time.time()
     t = rb.generate_trace(rb.TraceGenConfig([args.rows] * args.tables, args.accesses, 1.05, 0.4,
                                             32, 2 + rank))
@@ -463,7 +485,7 @@ def main():
     from paper_2511_08568_b200.model import DeviceModel
     from paper_2511_08568_b200.pipeline import HotPath
 
-    t, U, C, C32, cp, emb_c, pp, emb_p, setup_s, sh = build_state(args, rank, torch)
+    t, U, C, C32, cp, emb_c, pp, emb_p, setup_s, sh = build_state(args, rank, torch, dist)
     n = len(t)
     dec = sh.total_ids if sh is not None else 0
     hp = HotPath(DeviceModel(cp, emb_c, decode_ids=dec), DeviceModel(pp, emb_p, decode_ids=dec),

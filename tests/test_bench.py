@@ -68,3 +68,47 @@ def test_oracle_row_draws_equal_init_params():
         for k, v in full.items():
             if k != "embed_id":
                 assert np.array_equal(got[k], v), k
+
+
+def _c3_rank(rank, world, port, out):
+    import torch  # noqa: F401
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class A:
+        accesses, tables, rows, dim, init_scale = 200_000, 16, 1000, 8, 0.4
+        shards_eff, world, shard_index = 2, 2, 0
+    st = bench.build_state_config3(A, rank, None, device=False, dist=dist)
+    out[rank] = (st[0].gid_array.copy(), st[-1].tables)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_config3_trace_streamed_once_per_node_and_shared():
+    """Under several ranks the config-3 trace is streamed by local rank 0 into
+    /dev/shm and mapped by the others; the shards partition the trace and the
+    shared copy is removed."""
+    import glob
+    import multiprocessing as mp
+    import socket
+    from paper_2511_08568_b200 import TraceGenConfig, generate_trace
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    ps = [mp.Process(target=_c3_rank, args=(r, 2, port, out)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+    assert all(p.exitcode == 0 for p in ps)
+    full = generate_trace(TraceGenConfig([1000] * 16, 200_000, 1.05, 0.4, 32, 3)).gid_array
+    (g0, t0), (g1, t1) = out[0], out[1]
+    assert sorted(set(t0) | set(t1)) == list(range(16)) and not set(t0) & set(t1)
+    assert len(g0) + len(g1) == len(full)
+    assert np.array_equal(g0, full[np.isin(full // 1000, t0)])
+    assert not glob.glob("/dev/shm/recmg_c3_16x1000_200000_*")
