@@ -307,7 +307,6 @@ __global__ void lru_events_kernel(const int32_t *in, uint32_t *keys, uint32_t *v
         if (vals) vals[i] = (uint32_t)i;
         if (dup) {
             collapsed++;
-            if (per_access_hit) per_access_hit[i] = 1;
         }
     }
     collapsed = __reduce_add_sync(0xFFFFFFFFu, collapsed);
@@ -330,6 +329,9 @@ int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *g
     if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
     const unsigned grid = (unsigned)imin64((n + 255) / 256, 16 * kSmCount);
     uint8_t *hit = per_access_hit ? per_access_hit : p.hit;
+    // every access a hit until a kernel writes its miss: hit runs (most of a
+    // skewed trace) then cost no scattered byte stores
+    if (hit) RECMG_CUDA_TRY(cudaMemsetAsync(hit, 1, (size_t)n, s));
     if (cfg->policy == RECMG_POLICY_OPTGEN) {
         // next use of every access: stable sort by id, neighbours (cache_sim.py:80-89)
         iota_copy_kernel<<<grid, 256, 0, s>>>(gids, p.ids, p.pos, n);

@@ -668,8 +668,6 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 else v.meta[way] = clk;
                 lhits += __popc(peers);
             }
-            if (a.per_access_hit && lane < n_run)
-                a.per_access_hit[a.vals ? a.vals[base + lane] : base + lane] = 1;
         }
         __syncwarp();
     };
@@ -771,13 +769,6 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                         else if (OPT) v.meta[way] = a.next_use[a.vals ? a.vals[pos + last] : pos + last];
                         else v.meta[way] = clk;
                         lhits += nf;
-                    }
-                    if (a.per_access_hit) {
-#pragma unroll
-                        for (int j = 0; j < kFast / 32; j++) {
-                            const int i = j * 32 + lane;
-                            if (i < nf) a.per_access_hit[a.vals ? a.vals[pos + i] : pos + i] = 1;
-                        }
                     }
                 }
                 __syncwarp();
@@ -1092,7 +1083,6 @@ replay_wide_kernel(ReplayArgs a) {
                         else meta[slot] = clk;
                         lhits += __popc(peers);
                     }
-                    if (a.per_access_hit && lane < cut) a.per_access_hit[access_at(pos + lane)] = 1;
                 }
                 __syncwarp();
                 if (cut == nb) {

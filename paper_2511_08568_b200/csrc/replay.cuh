@@ -58,7 +58,7 @@ struct ReplayArgs {
     recmg_counters *ctr;
     uint8_t *access_class;
     int64_t *hits_misses;
-    uint8_t *per_access_hit;
+    uint8_t *per_access_hit;   // pre-filled with 1 by the caller: kernels write the misses
     const int32_t *next_use;   // OPTGEN: next reference of each access (n if none)
 };
 
