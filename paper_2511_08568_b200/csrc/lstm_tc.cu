@@ -108,7 +108,7 @@ struct TcArgs {
     float *logits;
     uint8_t *bits;
     int32_t *pf_gid;
-    float *scratch;        // [gridDim.x][2][L][16][128] float4
+    float *scratch;        // [gridDim.x][2][L][8][128] 32-byte pairs (scratch_at)
     int *tile_counter;     // dynamic tile scheduler (zeroed before the launch)
     long long *prof;       // PROF builds: per-CTA cycles per phase [grid][16]
 };
@@ -199,18 +199,21 @@ __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, u
                                      int N, bool acc) {
     const uint32_t idesc = umma::idesc_f16(128, N);
     const uint32_t lo_off = (uint32_t)N * 128u;  // hi image N*64*2 bytes, lo follows
+    // one descriptor built per B image; the k-steps and the lo image only move
+    // its 16 B-granular start field (+16 per 256 B k-step), so each MMA costs
+    // one independent add instead of a dependent shift/mask chain
+    const uint64_t dh = umma::make_desc(b_saddr, 128, 1024);
+    const uint64_t dl = dh + (uint64_t)(lo_off >> 4);
 #pragma unroll
     for (int ks = 0; ks < 4; ks++)
-        umma::mma_ts(d, a_hi + 8 * ks, umma::make_desc(b_saddr + 256 * ks, 128, 1024), idesc,
-                     (acc || ks > 0) ? 1u : 0u);
+        umma::mma_ts(d, a_hi + 8 * ks, dh + (uint64_t)(16 * ks), idesc, (acc || ks > 0) ? 1u : 0u);
     if (SINGLE) return;
 #pragma unroll
     for (int ks = 0; ks < 4; ks++)
-        umma::mma_ts(d, a_hi + 8 * ks, umma::make_desc(b_saddr + lo_off + 256 * ks, 128, 1024),
-                     idesc, 1u);
+        umma::mma_ts(d, a_hi + 8 * ks, dl + (uint64_t)(16 * ks), idesc, 1u);
 #pragma unroll
     for (int ks = 0; ks < 4; ks++)
-        umma::mma_ts(d, a_lo + 8 * ks, umma::make_desc(b_saddr + 256 * ks, 128, 1024), idesc, 1u);
+        umma::mma_ts(d, a_lo + 8 * ks, dh + (uint64_t)(16 * ks), idesc, 1u);
 }
 
 // sync point after threads wrote TMEM operands / before the MMA issue
@@ -264,13 +267,38 @@ __device__ __forceinline__ void zero_operand(const Ctx<PARTS> &c, uint32_t col_h
 // re-reads stays L2-resident (measured: caching -2.2%, prefetch -1.6% vs plain
 // __ldg; an L2 evict_last policy on the scratch instead, or L1::no_allocate
 // scratch loads, were slower -- DESIGN.md)
+#ifndef RECMG_ROW_L1
+#define RECMG_ROW_L1 0
+#endif
+#if RECMG_ROW_L1 == 0
+#define RECMG_ROW_L1_Q "L1::evict_last"
+#elif RECMG_ROW_L1 == 1
+#define RECMG_ROW_L1_Q "L1::evict_normal"
+#elif RECMG_ROW_L1 == 2
+#define RECMG_ROW_L1_Q "L1::evict_first"
+#else
+#define RECMG_ROW_L1_Q "L1::no_allocate"
+#endif
 __device__ __forceinline__ float4 row_ld(const float4 *p) {
     float4 v;
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.nc." RECMG_ROW_L1_Q ".L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
     return v;
+}
+#ifndef RECMG_ROW_V8
+#define RECMG_ROW_V8 1
+#endif
+// the same as one 256-bit load (LDG.256, sm_100): a full 32 B sector per lane,
+// half the load instructions and L1 tag lookups of two LDG.128
+__device__ __forceinline__ void row_ld8(const float4 *p, float4 &a, float4 &b) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.nc." RECMG_ROW_L1_Q ".L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                   "=f"(b.w)
+                 : "l"(p), "l"(pol));
 }
 
 // Folded-table row of the NEXT step, gathered while the current step's MMA
@@ -284,17 +312,30 @@ struct RowStage {
     const float4 *src;
     __device__ __forceinline__ void prefetch(const Ctx<PARTS> &c, const float *pid, int32_t g) {
         src = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + 4 * Ctx<PARTS>::U * c.part);
+        if constexpr (RECMG_ROW_V8 && NPRE % 2 == 0) {
 #pragma unroll
-        for (int q = 0; q < NPRE; q++) x[q] = row_ld(src + q);
+            for (int q = 0; q < NPRE; q += 2) row_ld8(src + q, x[q], x[q + 1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < NPRE; q++) x[q] = row_ld(src + q);
+        }
     }
     __device__ __forceinline__ void commit(const Ctx<PARTS> &c) {
 #pragma unroll
         for (int blk = 0; blk < NF4 / 4; blk++) {
             uint32_t r[16];
+            float4 late[4];
+            if constexpr (RECMG_ROW_V8) {
+                if (blk * 4 >= NPRE) {
+                    row_ld8(src + blk * 4, late[0], late[1]);
+                    row_ld8(src + blk * 4 + 2, late[2], late[3]);
+                }
+            }
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int i = blk * 4 + q;
-                const float4 u = i < NPRE ? x[i < NPRE ? i : 0] : row_ld(src + i);
+                const float4 u = i < NPRE ? x[i < NPRE ? i : 0]
+                                 : (RECMG_ROW_V8 ? late[q] : row_ld(src + i));
                 r[4 * q + 0] = __float_as_uint(u.x);
                 r[4 * q + 1] = __float_as_uint(u.y);
                 r[4 * q + 2] = __float_as_uint(u.z);
@@ -379,20 +420,39 @@ __device__ __forceinline__ void readU(const Ctx<PARTS> &c, uint32_t col,
     umma::tmem_ld_wait();
 }
 
-// scratch position j of this thread: NQ float4 at [(j*16 + NQ*part + u)*128 + row];
-// consecutive rows of a warp are consecutive float4 -> fully coalesced
+// scratch position j of this thread: NQ float4 as NQ/2 32-byte pairs at
+// pair index ((j*8 + NQ/2*part + u/2)*128 + row); consecutive rows of a warp
+// are consecutive 32 B -> one LDG.256 / STG.256 per pair, fully coalesced
 template <int PARTS>
 __device__ __forceinline__ float4 *scratch_at(float *base, const Ctx<PARTS> &c, int j, int u) {
     return reinterpret_cast<float4 *>(base) +
-           ((int64_t)(j * 16 + Ctx<PARTS>::NQ * c.part + u) * 128 + c.row);
+           ((int64_t)(j * 8 + Ctx<PARTS>::NQ / 2 * c.part + u / 2) * 128 + c.row) * 2 + (u & 1);
+}
+
+// all NQ float4 of scratch position j (256-bit loads)
+template <int PARTS>
+__device__ __forceinline__ void scr_ld_pos(float *base, const Ctx<PARTS> &c, int j,
+                                           float4 (&x)[Ctx<PARTS>::NQ]) {
+#pragma unroll
+    for (int u = 0; u < Ctx<PARTS>::NQ; u += 2) {
+        const float4 *p = scratch_at(base, c, j, u);
+        asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(x[u].x), "=f"(x[u].y), "=f"(x[u].z), "=f"(x[u].w), "=f"(x[u + 1].x),
+                       "=f"(x[u + 1].y), "=f"(x[u + 1].z), "=f"(x[u + 1].w)
+                     : "l"(p));
+    }
 }
 
 template <int PARTS>
 __device__ __forceinline__ void storeU(float *base, const Ctx<PARTS> &c, int j,
                                        const float (&v)[Ctx<PARTS>::U]) {
 #pragma unroll
-    for (int u = 0; u < Ctx<PARTS>::NQ; u++)
-        *scratch_at(base, c, j, u) = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+    for (int u = 0; u < Ctx<PARTS>::NQ; u += 2)
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                     ::"l"(scratch_at(base, c, j, u)), "f"(v[4 * u]), "f"(v[4 * u + 1]),
+                       "f"(v[4 * u + 2]), "f"(v[4 * u + 3]), "f"(v[4 * u + 4]), "f"(v[4 * u + 5]),
+                       "f"(v[4 * u + 6]), "f"(v[4 * u + 7])
+                     : "memory");
 }
 
 // encoder: position j of the attention keys, stored as X = e^(2e) (bit j of
@@ -480,15 +540,13 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
     int j = 0;
     for (; j + 2 <= npos; j += 2) {
         float4 e0[NQ], e1[NQ];
-#pragma unroll
-        for (int u = 0; u < NQ; u++) { e0[u] = *scratch_at(Es, c, j, u); e1[u] = *scratch_at(Es, c, j + 1, u); }
+        scr_ld_pos(Es, c, j, e0); scr_ld_pos(Es, c, j + 1, e1);
         s_part[(c.part * L + j) * 128 + c.row] = score(e0, j);
         s_part[(c.part * L + j + 1) * 128 + c.row] = score(e1, j + 1);
     }
     if (j < npos) {
         float4 e0[NQ];
-#pragma unroll
-        for (int u = 0; u < NQ; u++) e0[u] = *scratch_at(Es, c, j, u);
+        scr_ld_pos(Es, c, j, e0);
         s_part[(c.part * L + j) * 128 + c.row] = score(e0, j);
     }
 }
@@ -535,8 +593,7 @@ __device__ __forceinline__ void attn_context(const Ctx<PARTS> &c, float *Hs, int
     int j = 0;
     for (; j + 2 <= npos; j += 2) {
         float4 h0[NQ], h1[NQ];
-#pragma unroll
-        for (int u = 0; u < NQ; u++) { h0[u] = *scratch_at(Hs, c, j, u); h1[u] = *scratch_at(Hs, c, j + 1, u); }
+        scr_ld_pos(Hs, c, j, h0); scr_ld_pos(Hs, c, j + 1, h1);
         const float e0 = __expf(full_score<PARTS>(s_part, L, j, c.row) - mx);
         const float e1 = __expf(full_score<PARTS>(s_part, L, j + 1, c.row) - mx);
         sum += e0 + e1;
@@ -545,8 +602,7 @@ __device__ __forceinline__ void attn_context(const Ctx<PARTS> &c, float *Hs, int
     }
     if (j < npos) {
         float4 h0[NQ];
-#pragma unroll
-        for (int u = 0; u < NQ; u++) h0[u] = *scratch_at(Hs, c, j, u);
+        scr_ld_pos(Hs, c, j, h0);
         const float e0 = __expf(full_score<PARTS>(s_part, L, j, c.row) - mx);
         sum += e0;
         acc_ctx<NQ>(ctx, e0, h0);

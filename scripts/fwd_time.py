@@ -16,6 +16,11 @@ precision = sys.argv[3] if len(sys.argv) > 3 else "auto"
 t = rb.generate_trace(rb.TraceGenConfig([50000] * 256, n, 1.05, 0.4, 32, 2))
 K = rb.num_chunks(len(t))
 g = torch.from_numpy(t.gid_array[:K * 15].astype(np.int32).reshape(K, 15)).cuda()
+import os
+if os.environ.get("FWD_IDS") == "const":      # every token the same id: rows always L1 hits
+    g.fill_(12345)
+elif os.environ.get("FWD_IDS") == "few":      # 64 distinct ids
+    g.remainder_(64)
 for kind, seed in (("caching", 0), ("prefetch", 1)):
     p, emb = init_params_device(kind, t.table_sizes, dim=64, seed=seed, init_scale=0.4)
     dm = DeviceModel(p, emb, precision=precision)

@@ -107,21 +107,28 @@ __global__ void rate_kernel(int mode, int N, int per, int rounds, long long *out
     if (tid < 32) umma::tmem_free<512>(tb);
 }
 
-int main() {
+int main(int argc, char **argv) {
     long long *d;
     cudaMalloc(&d, 148 * sizeof(long long));
     cudaFuncSetAttribute(rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    for (int nt : {128, 256, 512})
-        for (int wm = 0; wm < 2; wm++) {
-            const int rounds = 2000;
-            rate_kernel<<<148, nt, 100 * 1024>>>(4, 256, 0, rounds, d, 1, wm);
-            cudaError_t e = cudaDeviceSynchronize();
-            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
-            std::vector<long long> h(148);
-            cudaMemcpy(h.data(), d, 148 * sizeof(long long), cudaMemcpyDeviceToHost);
-            double m = 0;
-            for (auto v : h) m += v;
-            printf("mma3 Z256+Q64 threads=%d waitmode=%d: %8.1f cyc/round\n", nt, wm, m / 148 / rounds);
-        }
+    auto run = [&](int mode, int N, int per, int nt, int wm, const char *name) {
+        const int rounds = 2000;
+        rate_kernel<<<148, nt, 100 * 1024>>>(mode, N, per, rounds, d, 1, wm);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); exit(1); }
+        std::vector<long long> h(148);
+        cudaMemcpy(h.data(), d, 148 * sizeof(long long), cudaMemcpyDeviceToHost);
+        double m = 0;
+        for (auto v : h) m += v;
+        m /= 148.0 * rounds;
+        printf("%-16s N=%3d per=%2d threads=%d: %8.1f cyc/round %7.1f cyc/MMA (peak-rate MMA %5.1f cyc)\n",
+               name, N, per, nt, m, per ? m / per : 0.0, 128.0 * N * 16 / 4096.0);
+    };
+    const char *names[] = {"ts/no-swizzle", "ss/no-swizzle", "ss/sw128", "ts/sw128"};
+    for (int mode = 0; mode < 4; mode++)
+        for (int N : {64, 128, 256})
+            for (int per : {1, 12, 48}) run(mode, N, per, 128, 0, names[mode]);
+    for (int nt : {128, 512})
+        for (int wm = 0; wm < 2; wm++) run(4, 256, 0, nt, wm, "mma3 Z256+Q64");
     return 0;
 }
