@@ -307,7 +307,13 @@ __device__ __forceinline__ void row_ld8(const float4 *p, float4 &a, float4 &b) {
 template <int PARTS>
 struct RowStage {
     static constexpr int NF4 = Ctx<PARTS>::U;            // 4U floats = U float4
-    static constexpr int NPRE = PARTS == 4 ? 4 : 16;   // measured: more early loads clog the LSU
+#ifndef RECMG_NPRE
+#define RECMG_NPRE 8
+#endif
+    // measured (LDG.256 rows): 8 early float4 beat 4 by 1.2% (caching) / 1.5% (prefetch)
+    // despite ~100 B of spills; 12 spills more
+    static constexpr int NPRE = PARTS == 4 ? RECMG_NPRE : 16;
+    static_assert(NPRE % 4 == 0, "late loads are whole 64-byte blocks");
     float4 x[NPRE];
     const float4 *src;
     __device__ __forceinline__ void prefetch(const Ctx<PARTS> &c, const float *pid, int32_t g) {
