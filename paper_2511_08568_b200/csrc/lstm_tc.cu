@@ -148,13 +148,25 @@ struct PhaseClock {
 };
 
 // ---- per-thread helpers ------------------------------------------------------
+// Unit ownership: the gate product Z is issued as two N = 128 halves (units
+// 0-31, then 32-63) with their own commits, and every thread owns HU units of
+// EACH half -- part p holds units [HU p, HU p + HU) and [32 + HU p, 32 + HU p + HU)
+// -- so all warps start their cell on the first half while the tensor pipe
+// still runs the second.  Local unit k < HU is in half 0, k >= HU in half 1.
 template <int PARTS>
 struct Ctx {
     static constexpr int U = 64 / PARTS;       // hidden units per thread
+    static constexpr int HU = U / 2;           // units per Z half
     static constexpr int NQ = U / 4;           // float4 per scratch position
     static constexpr int NT = 128 * PARTS;     // threads
     int tid, warp, lane, quad, part, row;
     uint32_t tbase, lane_addr;  // tmem base, + lane quadrant
+    // global hidden unit of local unit k
+    __device__ __forceinline__ int unit(int k) const {
+        return (k < HU ? 0 : 32 - HU) + HU * part + k;
+    }
+    // Z column (gate-interleaved, 4 per unit) of the first gate of local unit k
+    __device__ __forceinline__ uint32_t zcol(int k) const { return 4u * (uint32_t)unit(k); }
 };
 
 // all threads: copy a phase's B images (bytes [off, off+len) of the blob) to smem
@@ -195,10 +207,9 @@ __device__ __forceinline__ void tma_piece(uint8_t *dst, const uint8_t *blob, int
 // the three split products for one B matrix: d (+)= a * b, K = 64 (4 k-steps)
 // SINGLE: the reduced-precision variant (RECMG_PREC_TC16) keeps only xh * wh
 template <bool SINGLE>
-__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_saddr,
-                                     int N, bool acc) {
+__device__ __forceinline__ void mma3x(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_saddr,
+                                      uint32_t lo_off, int N, bool acc) {
     const uint32_t idesc = umma::idesc_f16(128, N);
-    const uint32_t lo_off = (uint32_t)N * 128u;  // hi image N*64*2 bytes, lo follows
     // one descriptor built per B image; the k-steps and the lo image only move
     // its 16 B-granular start field (+16 per 256 B k-step), so each MMA costs
     // one independent add instead of a dependent shift/mask chain
@@ -214,6 +225,39 @@ __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, u
 #pragma unroll
     for (int ks = 0; ks < 4; ks++)
         umma::mma_ts(d, a_lo + 8 * ks, dh + (uint64_t)(16 * ks), idesc, 1u);
+}
+template <bool SINGLE>
+__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_saddr,
+                                     int N, bool acc) {
+    mma3x<SINGLE>(d, a_hi, a_lo, b_saddr, (uint32_t)N * 128u, N, acc);  // lo image follows hi
+}
+// half h of an N = 256 gate product into Z: B rows [128h, 128h + 128) start
+// 16 KB into the hi (and lo) image of the N = 256 B matrix, D = Z columns [128h, +128)
+template <bool SINGLE>
+__device__ __forceinline__ void mma3_zhalf(uint32_t tbase, uint32_t a_hi, uint32_t a_lo,
+                                           uint32_t b_saddr, bool acc, int h) {
+    mma3x<SINGLE>(tbase + COL_Z + 128u * h, a_hi, a_lo, b_saddr + 16384u * h, 32768u, 128, acc);
+}
+
+// Z (+)= a * b for an N = 256 gate product; SPLIT: as two N = 128 halves
+// committed to bar_a / bar_b (the cell starts on the first half), else one
+// product committed to bar_a only (measured per model and phase: the split
+// pays where the products are long -- the prefetch model's two-operand layers --
+// and costs where one N = 256 product is short)
+template <bool SINGLE, bool SPLIT>
+__device__ __forceinline__ void zproduct(uint32_t tbase, uint32_t a_hi, uint32_t a_lo,
+                                         uint32_t b_saddr, bool acc, uint64_t *bar_a,
+                                         uint64_t *bar_b) {
+    if constexpr (SPLIT) {
+        mma3_zhalf<SINGLE>(tbase, a_hi, a_lo, b_saddr, acc, 0);
+        umma::commit(bar_a);
+        mma3_zhalf<SINGLE>(tbase, a_hi, a_lo, b_saddr, acc, 1);
+        umma::commit(bar_b);
+    } else {
+        mma3<SINGLE>(tbase + COL_Z, a_hi, a_lo, b_saddr, 256, acc);
+        umma::commit(bar_a);
+        (void)bar_b;
+    }
 }
 
 // sync point after threads wrote TMEM operands / before the MMA issue
@@ -232,10 +276,24 @@ __device__ __forceinline__ void wait_mma(uint64_t *mbar, uint32_t &phase) {
 template <int N>
 __device__ __forceinline__ void st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
     if constexpr (N == 16) umma::tmem_st16(taddr, r);
-    else umma::tmem_st8(taddr, r);
+    else if constexpr (N == 8) umma::tmem_st8(taddr, r);
+    else umma::tmem_st4(taddr, r);
 }
 
-// this thread's U units as fp16 hi|lo into an A operand region (U/2 columns each)
+// the two half-sized column runs of an operand region (fp16 pairs: unit u at
+// column u / 2) that hold this thread's units
+template <int PARTS>
+__device__ __forceinline__ void st_op_halves(const Ctx<PARTS> &c, uint32_t col,
+                                             const uint32_t (&r)[Ctx<PARTS>::U / 2]) {
+    constexpr int Q = Ctx<PARTS>::HU / 2;
+    uint32_t r0[Q], r1[Q];
+#pragma unroll
+    for (int m = 0; m < Q; m++) { r0[m] = r[m]; r1[m] = r[Q + m]; }
+    st_cols<Q>(c.lane_addr + col + (uint32_t)c.unit(0) / 2, r0);
+    st_cols<Q>(c.lane_addr + col + (uint32_t)c.unit(Ctx<PARTS>::HU) / 2, r1);
+}
+
+// this thread's U units as fp16 hi|lo into an A operand region (32 columns each)
 template <bool SINGLE, int PARTS>
 __device__ __forceinline__ void store_operand(const Ctx<PARTS> &c, uint32_t col_hi,
                                               uint32_t col_lo, const float (&v)[Ctx<PARTS>::U]) {
@@ -248,8 +306,8 @@ __device__ __forceinline__ void store_operand(const Ctx<PARTS> &c, uint32_t col_
         hi[m] = *reinterpret_cast<const uint32_t *>(&h);
         lo[m] = umma::pack_half2(v[2 * m] - hf.x, v[2 * m + 1] - hf.y);
     }
-    st_cols<H>(c.lane_addr + col_hi + H * c.part, hi);
-    if (!SINGLE) st_cols<H>(c.lane_addr + col_lo + H * c.part, lo);
+    st_op_halves(c, col_hi, hi);
+    if (!SINGLE) st_op_halves(c, col_lo, lo);
 }
 
 template <int PARTS>
@@ -258,8 +316,8 @@ __device__ __forceinline__ void zero_operand(const Ctx<PARTS> &c, uint32_t col_h
     uint32_t z[H];
 #pragma unroll
     for (int m = 0; m < H; m++) z[m] = 0u;
-    st_cols<H>(c.lane_addr + col_hi + H * c.part, z);
-    st_cols<H>(c.lane_addr + col_lo + H * c.part, z);
+    st_op_halves(c, col_hi, z);
+    st_op_halves(c, col_lo, z);
 }
 
 // folded-table row loads: kept in L1 (hot ids repeat within a tile) but
@@ -306,48 +364,54 @@ __device__ __forceinline__ void row_ld8(const float4 *p, float4 &a, float4 &b) {
 // the rest when the row is committed into Z (after the cell has read Z).
 template <int PARTS>
 struct RowStage {
-    static constexpr int NF4 = Ctx<PARTS>::U;            // 4U floats = U float4
+    using C = Ctx<PARTS>;
+    static constexpr int NF4 = C::U;            // 4U floats = U float4
+    static constexpr int NH = C::HU;            // float4 per Z half (4 HU floats)
 #ifndef RECMG_NPRE
 #define RECMG_NPRE 8
 #endif
     // measured (LDG.256 rows): 8 early float4 beat 4 by 1.2% (caching) / 1.5% (prefetch)
     // despite ~100 B of spills; 12 spills more
     static constexpr int NPRE = PARTS == 4 ? RECMG_NPRE : 16;
-    static_assert(NPRE % 4 == 0, "late loads are whole 64-byte blocks");
+    static_assert(NPRE % 4 == 0 && NH % 4 == 0, "loads and commits are whole 64-byte blocks");
     float4 x[NPRE];
-    const float4 *src;
-    __device__ __forceinline__ void prefetch(const Ctx<PARTS> &c, const float *pid, int32_t g) {
-        src = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + 4 * Ctx<PARTS>::U * c.part);
-        if constexpr (RECMG_ROW_V8 && NPRE % 2 == 0) {
+    const float4 *src;   // this thread's first-half run; the second half is +128 floats
+    // float4 i of this thread's row part: half i / NH, float4 i % NH of that half's run
+    __device__ __forceinline__ const float4 *at(int i) const {
+        return src + (i >= NH ? 32 : 0) + (i % NH);
+    }
+    __device__ __forceinline__ void prefetch(const C &c, const float *pid, int32_t g) {
+        src = reinterpret_cast<const float4 *>(pid + (int64_t)g * 256 + c.zcol(0));
+        if constexpr (RECMG_ROW_V8) {
 #pragma unroll
-            for (int q = 0; q < NPRE; q += 2) row_ld8(src + q, x[q], x[q + 1]);
+            for (int q = 0; q < NPRE; q += 2) row_ld8(at(q), x[q], x[q + 1]);
         } else {
 #pragma unroll
-            for (int q = 0; q < NPRE; q++) x[q] = row_ld(src + q);
+            for (int q = 0; q < NPRE; q++) x[q] = row_ld(at(q));
         }
     }
-    __device__ __forceinline__ void commit(const Ctx<PARTS> &c) {
+    __device__ __forceinline__ void commit(const C &c) {
 #pragma unroll
         for (int blk = 0; blk < NF4 / 4; blk++) {
             uint32_t r[16];
             float4 late[4];
             if constexpr (RECMG_ROW_V8) {
                 if (blk * 4 >= NPRE) {
-                    row_ld8(src + blk * 4, late[0], late[1]);
-                    row_ld8(src + blk * 4 + 2, late[2], late[3]);
+                    row_ld8(at(blk * 4), late[0], late[1]);
+                    row_ld8(at(blk * 4 + 2), late[2], late[3]);
                 }
             }
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int i = blk * 4 + q;
                 const float4 u = i < NPRE ? x[i < NPRE ? i : 0]
-                                 : (RECMG_ROW_V8 ? late[q] : row_ld(src + i));
+                                 : (RECMG_ROW_V8 ? late[q] : row_ld(at(i)));
                 r[4 * q + 0] = __float_as_uint(u.x);
                 r[4 * q + 1] = __float_as_uint(u.y);
                 r[4 * q + 2] = __float_as_uint(u.z);
                 r[4 * q + 3] = __float_as_uint(u.w);
             }
-            umma::tmem_st16(c.lane_addr + COL_Z + 4 * Ctx<PARTS>::U * c.part + 16 * blk, r);
+            umma::tmem_st16(c.lane_addr + COL_Z + c.zcol(4 * blk), r);
         }
     }
 };
@@ -356,33 +420,41 @@ struct RowStage {
 template <int PARTS>
 __device__ __forceinline__ void init_z_from_row(const Ctx<PARTS> &c, const float *rowp) {
     constexpr int NC = 4 * Ctx<PARTS>::U;
-    const float4 *a = reinterpret_cast<const float4 *>(rowp + NC * c.part);
 #pragma unroll
     for (int blk = 0; blk < NC / 16; blk++) {
+        const float4 *a = reinterpret_cast<const float4 *>(rowp + c.zcol(4 * blk));
         uint32_t r[16];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-            const float4 x = __ldg(a + blk * 4 + q);
+            const float4 x = __ldg(a + q);
             r[4 * q + 0] = __float_as_uint(x.x);
             r[4 * q + 1] = __float_as_uint(x.y);
             r[4 * q + 2] = __float_as_uint(x.z);
             r[4 * q + 3] = __float_as_uint(x.w);
         }
-        umma::tmem_st16(c.lane_addr + COL_Z + NC * c.part + 16 * blk, r);
+        umma::tmem_st16(c.lane_addr + COL_Z + c.zcol(4 * blk), r);
     }
 }
 
+struct NoMid {
+    __device__ __forceinline__ void operator()() const {}
+};
+
 // LSTM cell on this thread's U hidden units (model.py:103-112)
-template <bool BIAS, int PARTS>
+// mid() runs between the two Z halves (the wait for the second half's commit)
+template <bool BIAS, int PARTS, class Mid = NoMid>
 __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
-                                     float (&cs)[Ctx<PARTS>::U], float (&h)[Ctx<PARTS>::U]) {
+                                     float (&cs)[Ctx<PARTS>::U], float (&h)[Ctx<PARTS>::U],
+                                     Mid mid = Mid()) {
     constexpr int U = Ctx<PARTS>::U;
-    const float4 *b4 = reinterpret_cast<const float4 *>(bias) + U * c.part;
+    static_assert(Ctx<PARTS>::HU == 8, "one loop iteration per Z half");
+    const float4 *b4 = reinterpret_cast<const float4 *>(bias);   // gate-interleaved per unit
 #pragma unroll
     for (int blk = 0; blk < U / 4; blk += 2) {
+        if (blk == 2) mid();
         float z0[16], z1[16];
-        umma::tmem_ld16(c.lane_addr + COL_Z + 4 * U * c.part + 16 * blk, z0);
-        umma::tmem_ld16(c.lane_addr + COL_Z + 4 * U * c.part + 16 * (blk + 1), z1);
+        umma::tmem_ld16(c.lane_addr + COL_Z + c.zcol(4 * blk), z0);
+        umma::tmem_ld16(c.lane_addr + COL_Z + c.zcol(4 * blk + 4), z1);
         umma::tmem_ld_wait();
 #pragma unroll
         for (int g4 = 0; g4 < 2; g4++) {
@@ -393,7 +465,7 @@ __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
                 const float *z = g4 == 0 ? &z0[4 * u] : &z1[4 * u];
                 float zi = z[0], zf = z[1], zg = z[2], zo = z[3];
                 if (BIAS) {
-                    const float4 bb = __ldg(b4 + j);
+                    const float4 bb = __ldg(b4 + c.unit(j));
                     zi += bb.x; zf += bb.y; zg += bb.z; zo += bb.w;
                 }
                 float ig = ex2_den(zi), fg = ex2_den(zf), gd = ex2_den(zg), o = ex2_den(zo);
@@ -411,19 +483,17 @@ __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
     }
 }
 
-// U columns [col + U*part, +U) of this thread's lane
+// this thread's U unit columns (col + unit) of a per-unit TMEM region
 template <int PARTS>
 __device__ __forceinline__ void readU(const Ctx<PARTS> &c, uint32_t col,
                                       float (&v)[Ctx<PARTS>::U]) {
-    constexpr int U = Ctx<PARTS>::U;
-#pragma unroll
-    for (int k = 0; k < U / 16; k++) {
-        float t[16];
-        umma::tmem_ld16(c.lane_addr + col + U * c.part + 16 * k, t);
-#pragma unroll
-        for (int i = 0; i < 16; i++) v[16 * k + i] = t[i];
-    }
+    static_assert(Ctx<PARTS>::HU == 8, "two 8-column runs");
+    float t0[8], t1[8];
+    umma::tmem_ld8(c.lane_addr + col + c.unit(0), t0);
+    umma::tmem_ld8(c.lane_addr + col + c.unit(8), t1);
     umma::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; i++) { v[i] = t0[i]; v[8 + i] = t1[i]; }
 }
 
 // scratch position j of this thread: NQ float4 as NQ/2 32-byte pairs at
@@ -504,11 +574,11 @@ __device__ __forceinline__ float score_fast(const float4 (&x)[NQ], const float (
 // direct form: raw keys (raw) or keys stored as X = e^(2e) recovered by log
 template <int NQ>
 __device__ __forceinline__ float score_slow(const float4 (&x)[NQ], const float (&q)[4 * NQ],
-                                            const float4 *v4, bool raw) {
+                                            const float4 (&vr)[NQ], bool raw) {
     float s = 0.0f;
 #pragma unroll
     for (int u = 0; u < NQ; u++) {
-        const float4 v = __ldg(v4 + u);
+        const float4 v = vr[u];
         const float4 e = raw ? x[u] : make_float4(0.5f * __logf(x[u].x), 0.5f * __logf(x[u].y),
                                                   0.5f * __logf(x[u].z), 0.5f * __logf(x[u].w));
         s += v.x * ftanh(e.x + q[4 * u + 0]);
@@ -527,7 +597,7 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
                                             float vsum, uint32_t rawmask, float *s_part, int L) {
     constexpr int NQ = Ctx<PARTS>::NQ;
     constexpr int U = Ctx<PARTS>::U;
-    const float4 *v4 = reinterpret_cast<const float4 *>(vp) + NQ * c.part;
+    const float4 *v4 = reinterpret_cast<const float4 *>(vp);   // float4 u of mine: unit(4u) / 4
     float qx[U];
     bool qok = true;
 #pragma unroll
@@ -538,9 +608,9 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
     const uint32_t slow = qok ? rawmask : 0xFFFFFFFFu;
     float4 vr[NQ];   // this thread's att_v units, loaded once per step
 #pragma unroll
-    for (int u = 0; u < NQ; u++) vr[u] = __ldg(v4 + u);
+    for (int u = 0; u < NQ; u++) vr[u] = __ldg(v4 + c.unit(4 * u) / 4);
     auto score = [&](const float4 (&x)[NQ], int j) {
-        return ((slow >> j) & 1u) ? score_slow<NQ>(x, q, v4, (rawmask >> j) & 1u)
+        return ((slow >> j) & 1u) ? score_slow<NQ>(x, q, vr, (rawmask >> j) & 1u)
                                   : vsum + score_fast<NQ>(x, qx, vr);
     };
     int j = 0;
@@ -626,11 +696,11 @@ __device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
     float v[U];
     readU(c, col, v);
     float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    const float4 *cb4 = reinterpret_cast<const float4 *>(comb_b + U * c.part);
-    const float4 *hw4 = reinterpret_cast<const float4 *>(head_w + U * c.part);
+    const float4 *cb4 = reinterpret_cast<const float4 *>(comb_b);
+    const float4 *hw4 = reinterpret_cast<const float4 *>(head_w);
 #pragma unroll
     for (int k = 0; k < U; k += 4) {
-        const float4 cb = __ldg(cb4 + k / 4), hw = __ldg(hw4 + k / 4);
+        const float4 cb = __ldg(cb4 + c.unit(k) / 4), hw = __ldg(hw4 + c.unit(k) / 4);
         float d[4] = {ex2_den(v[k] + cb.x), ex2_den(v[k + 1] + cb.y), ex2_den(v[k + 2] + cb.z),
                       ex2_den(v[k + 3] + cb.w)};
         rcp4(d[0], d[1], d[2], d[3]);
@@ -664,6 +734,15 @@ __device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T
 // 4 dec MMA1 wait, 5 dec head+scores+sync, 6 dec softmax/ctx+sync, 7 dec MMA2 wait,
 // 8 dec cell, 9 weight loads, 10 prefetch layer-1 MMA wait, 11 prefetch layer-1 cell
 // MODE bit 0: phase-cycle instrumentation; bit 1: single-product GEMMs (TC16)
+#ifndef RECMG_ZSPLIT_CENC
+#define RECMG_ZSPLIT_CENC 0
+#endif
+#ifndef RECMG_ZSPLIT_CDEC
+#define RECMG_ZSPLIT_CDEC 0
+#endif
+constexpr bool kSplitCEnc = RECMG_ZSPLIT_CENC != 0;   // caching encoder Z += h Wh
+constexpr bool kSplitCDec = RECMG_ZSPLIT_CDEC != 0;   // caching decoder Z += ctx Wc
+
 template <int KIND, int MODE>
 __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(TcArgs a) {
     constexpr bool PROF = (MODE & 1) != 0;
@@ -676,6 +755,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     constexpr int NT = C::NT;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar, mbar2;   // caching: mbar2 tracks the MMAs split off
+    __shared__ uint64_t mbar3;         // second N = 128 half of a gate product
     __shared__ uint64_t tma_bar;       // async weight loads / swaps
     __shared__ uint64_t tma_bar2;      // prefetch decoder: reload of the weights s_part overlays
     __shared__ uint32_t tmem_base_s;
@@ -696,6 +776,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     if (c.tid == 0) {
         umma::mbar_init(&mbar, 1);
         umma::mbar_init(&mbar2, 1);
+        umma::mbar_init(&mbar3, 1);
         umma::mbar_init(&tma_bar, 1);
         umma::mbar_init(&tma_bar2, 1);
     }
@@ -705,7 +786,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     umma::fence_after();
     c.tbase = tmem_base_s;
     c.lane_addr = c.tbase + ((uint32_t)(32 * c.quad) << 16);
-    uint32_t phase = 0, phase2 = 0, tphase = 0, tphase2 = 0;
+    uint32_t phase = 0, phase2 = 0, phase3 = 0, tphase = 0, tphase2 = 0;
     const uint32_t sbase = umma::smem_u32(smem);
     const TcLayout &tl = a.tl;
     const PackedLayout &pl = a.pl;
@@ -718,7 +799,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     const float *head_w = a.dense + pl.head_w;
     const float head_b = __ldg(a.dense + pl.head_b);
     float vsum = 0.0f;   // sum of this thread's att_v units (score_fast)
-    for (int k = 0; k < U; k++) vsum += __ldg(att_v + U * c.part + k);
+    for (int k = 0; k < U; k++) vsum += __ldg(att_v + c.unit(k));
     float vabs = 0.0f;   // sum over all d units of |att_v| (attn_context's shift)
     for (int k = 0; k < 64; k++) vabs += fabsf(__ldg(att_v + k));
     const int64_t n_tiles = (a.batch + 127) / 128;
@@ -778,11 +859,9 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     mma3<SINGLE>(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
                          sbase + tl.b_off[1], 64, false);                  // Q = h att_enc
                     umma::commit(&mbar);
-                    if (!last) {
-                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase + tl.b_off[0], 256, true);             // Z += h Wh
-                        umma::commit(&mbar2);
-                    }
+                    if (!last)                                    // Z += h Wh
+                        zproduct<SINGLE, kSplitCEnc>(c.tbase, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                                                     sbase + tl.b_off[0], true, &mbar2, &mbar3);
                 }
                 pc.mark(12);
                 if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
@@ -796,7 +875,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 if (!last) {
                     wait_mma(&mbar2, phase2);
-                    cell<false>(c, nullptr, cs0, h);
+                    if constexpr (kSplitCEnc)
+                        cell<false>(c, nullptr, cs0, h, [&] { wait_mma(&mbar3, phase3); });
+                    else
+                        cell<false>(c, nullptr, cs0, h);
                     store_operand<SINGLE>(c, A_H_HI, A_H_LO, h);
                     storeU(Hs, c, t, h);
                     if (t + 1 < L) stage.commit(c);
@@ -809,10 +891,13 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last) {
-                        // layer 0: Z = Pid + Ptab + h0 Wh0 (slot)
-                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                             sbase + tl.eslot, 256, true);
+                        // layer 0: Z = Pid + Ptab + h0 Wh0 (slot), two halves
+                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                           sbase + tl.eslot, true, 0);
                         umma::commit(&mbar);
+                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                           sbase + tl.eslot, true, 1);
+                        umma::commit(&mbar3);
                     }
                     if (t >= 1) {
                         mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
@@ -823,12 +908,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     wait_mma(&mbar, phase);
                     pc.mark(2);
-                    if (c.tid == 0) {   // Wh0 done: Wx1 into the slot under the layer-0 cell
-                        umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
-                        tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[1],
-                                  tl.img256, &tma_bar);
-                    }
-                    cell<false>(c, nullptr, cs0, h);
+                    cell<false>(c, nullptr, cs0, h, [&] {
+                        wait_mma(&mbar3, phase3);
+                        if (c.tid == 0) {   // Wh0 done: Wx1 into the slot under the layer-0 cell
+                            umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                            tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[1],
+                                      tl.img256, &tma_bar);
+                        }
+                    });
                     store_operand<SINGLE>(c, P_H0_HI, P_H0_LO, h);
                     pc.mark(15);
                     wait_mma(&tma_bar, tphase);                    // Wx1 in the slot
@@ -838,11 +925,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell)
                     if (c.tid == 0) {
                         umma::fence_after();
-                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                             sbase + tl.eslot, 256, false);        // Wx1 (slot)
-                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase, 256, true);                    // Wh1
-                        umma::commit(&mbar);
+#pragma unroll
+                        for (int hf = 0; hf < 2; hf++) {
+                            mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                               sbase + tl.eslot, false, hf);   // Wx1 (slot)
+                            mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                                               sbase, true, hf);               // Wh1
+                            umma::commit(hf == 0 ? &mbar : &mbar3);
+                        }
                     }
                 }
                 if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
@@ -857,12 +947,14 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     wait_mma(&mbar, phase);
                     pc.mark(11);
-                    if (t + 1 < L && c.tid == 0) {   // Wx1 done: Wh0 back for the next step
-                        umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
-                        tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[0],
-                                  tl.img256, &tma_bar);
-                    }
-                    cell<true>(c, a.dense + pl.enc_b[1], cs1, h);
+                    cell<true>(c, a.dense + pl.enc_b[1], cs1, h, [&] {
+                        wait_mma(&mbar3, phase3);
+                        if (t + 1 < L && c.tid == 0) {   // Wx1 done: Wh0 back for the next step
+                            umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                            tma_piece(smem + tl.eslot, a.blob, tl.phase_off[0] + tl.b_off[0],
+                                      tl.img256, &tma_bar);
+                        }
+                    });
                     store_operand<SINGLE>(c, P_H1_HI, P_H1_LO, h);
                     storeU(Hs, c, t, h);
                     if (t + 1 < L) stage.commit(c);
@@ -972,24 +1064,31 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 // C = ctx Wcomb_c (barrier 2, read by the next step's head)
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_X_HI, c.tbase + A_X_LO,
-                         sbase + tl.dslot, 256, true);                   // Wc_d (slot)
-                    umma::commit(&mbar);
+                    zproduct<SINGLE, kSplitCDec>(c.tbase, c.tbase + A_X_HI, c.tbase + A_X_LO,
+                                                 sbase + tl.dslot, true, &mbar, &mbar3);  // Wc_d
+
                     mma3<SINGLE>(c.tbase + COL_C, c.tbase + A_X_HI, c.tbase + A_X_LO,
                          sbase + 2 * tl.img64, 64, false);               // Wcomb_c
                     umma::commit(&mbar2);
                 }
                 if (t + 1 < T) dstage.prefetch(c, pid_dec, __ldg(gid + t + 1));
                 wait_mma(&mbar, phase);
+                pc.mark(8);
                 // Wc_d done (and so every earlier MMA): swap Wh_d back under the cell
                 // (the last step's GEMM1 has no Z product, so it is not needed then)
-                if (t + 1 < T && c.tid == 0) {
-                    umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
-                    tma_piece(smem + tl.dslot, a.blob, tl.phase_off[1] + tl.b_off[2], tl.img256,
-                              &tma_bar);
+                auto swap_whd = [&] {
+                    if (t + 1 < T && c.tid == 0) {
+                        umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
+                        tma_piece(smem + tl.dslot, a.blob, tl.phase_off[1] + tl.b_off[2],
+                                  tl.img256, &tma_bar);
+                    }
+                };
+                if constexpr (kSplitCDec) {
+                    cell<false>(c, nullptr, cs0, h, [&] { wait_mma(&mbar3, phase3); swap_whd(); });
+                } else {
+                    swap_whd();
+                    cell<false>(c, nullptr, cs0, h);
                 }
-                pc.mark(8);
-                cell<false>(c, nullptr, cs0, h);
                 store_operand<SINGLE>(c, A_H_HI, A_H_LO, h);
                 if (t + 1 < T) dstage.commit(c);
             }
@@ -1055,20 +1154,25 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(7);
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
-                         sbase, 256, true);                              // Wctx0
-                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                         sbase + tl.img256, 256, true);                  // Wh0
-                    umma::commit(&mbar);
+#pragma unroll
+                    for (int hf = 0; hf < 2; hf++) {
+                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
+                                           sbase, true, hf);                  // Wctx0
+                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                           sbase + tl.img256, true, hf);      // Wh0
+                        umma::commit(hf == 0 ? &mbar : &mbar3);
+                    }
                 }
                 wait_mma(&mbar, phase);
-                // GEMM2 done: DEC-B (Wx1 | Wh1) into the region under the layer-0 cell
-                if (c.tid == 0) {
-                    umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.phase_len[2]);
-                    tma_piece(smem, a.blob, tl.phase_off[2], tl.phase_len[2], &tma_bar);
-                }
                 pc.mark(8);
-                cell<false>(c, nullptr, cs0, h);
+                cell<false>(c, nullptr, cs0, h, [&] {
+                    wait_mma(&mbar3, phase3);
+                    // GEMM2 done: DEC-B (Wx1 | Wh1) into the region under the layer-0 cell
+                    if (c.tid == 0) {
+                        umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.phase_len[2]);
+                        tma_piece(smem, a.blob, tl.phase_off[2], tl.phase_len[2], &tma_bar);
+                    }
+                });
                 store_operand<SINGLE>(c, P_H0_HI, P_H0_LO, h);
                 // layer 1 (DEC-B weights): Z = h0 Wx1 + h1 Wh1 (+ b1)
                 pc.mark(9);
@@ -1076,21 +1180,26 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 tmem_writes_done();
                 if (c.tid == 0) {
                     umma::fence_after();
-                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                         sbase + tl.b_off[9], 256, false);
-                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                         sbase + tl.b_off[10], 256, true);
-                    umma::commit(&mbar);
+#pragma unroll
+                    for (int hf = 0; hf < 2; hf++) {
+                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                           sbase + tl.b_off[9], false, hf);
+                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                                           sbase + tl.b_off[10], true, hf);
+                        umma::commit(hf == 0 ? &mbar : &mbar3);
+                    }
                 }
                 pc.mark(10);
                 wait_mma(&mbar, phase);
-                // layer 1 done: att_dec | Wcomb back for the next step's GEMM1
-                if (c.tid == 0) {
-                    umma::mbar_expect_tx(&tma_bar2, (uint32_t)(3 * tl.img64));
-                    tma_piece(smem, a.blob, dec_a + tl.b_off[4], 3 * tl.img64, &tma_bar2);
-                }
                 pc.mark(11);
-                cell<true>(c, a.dense + pl.dec_b[1], cs1, h);
+                cell<true>(c, a.dense + pl.dec_b[1], cs1, h, [&] {
+                    wait_mma(&mbar3, phase3);
+                    // layer 1 done: att_dec | Wcomb back for the next step's GEMM1
+                    if (c.tid == 0) {
+                        umma::mbar_expect_tx(&tma_bar2, (uint32_t)(3 * tl.img64));
+                        tma_piece(smem, a.blob, dec_a + tl.b_off[4], 3 * tl.img64, &tma_bar2);
+                    }
+                });
                 store_operand<SINGLE>(c, P_H1_HI, P_H1_LO, h);
             }
         }
