@@ -310,6 +310,15 @@ __device__ __forceinline__ void store_operand(const Ctx<PARTS> &c, uint32_t col_
     if (!SINGLE) st_op_halves(c, col_lo, lo);
 }
 
+// zero this thread's unit columns of a per-unit fp32 region (Q)
+template <int PARTS>
+__device__ __forceinline__ void zero_units(const Ctx<PARTS> &c, uint32_t col) {
+    static_assert(Ctx<PARTS>::HU == 8, "two 8-column runs");
+    const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    umma::tmem_st8(c.lane_addr + col + c.unit(0), z);
+    umma::tmem_st8(c.lane_addr + col + c.unit(8), z);
+}
+
 template <int PARTS>
 __device__ __forceinline__ void zero_operand(const Ctx<PARTS> &c, uint32_t col_hi, uint32_t col_lo) {
     constexpr int H = Ctx<PARTS>::U / 2;
@@ -992,6 +1001,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         if (caching) {
             zero_operand(c, A_H_HI, A_H_LO);
             zero_operand(c, A_X_HI, A_X_LO);
+            zero_units(c, COL_Q);
             RowStage<PARTS> dstage;
             dstage.prefetch(c, pid_dec, __ldg(gid));
             dstage.commit(c);
@@ -1005,17 +1015,15 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 }
                 tmem_writes_done();
                 pc.mark(4);
-                // GEMM1 on h_{t-1}: Z += h Wh_d ; Q = h att_dec ; C += h Wcomb_h
-                // Q and C first (barrier 1), Z += h Wh_d after (barrier 2): the
-                // head and the attention run while the N=256 product finishes
+                // GEMM1 on h_{t-1}: Z += h Wh_d ; [Q | C] += h [att_dec | Wcomb_h]
+                // (one N = 128 product: Q was zeroed after the previous step's
+                // scores, C holds ctx_{t-1} Wcomb_c) first (barrier 1), Z += h Wh_d
+                // after (barrier 2): the head and the attention run while the N=256
+                // product finishes
                 if (c.tid == 0) {
                     umma::fence_after();
-                    if (!last)
-                        mma3<SINGLE>(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase, 64, false);                          // att_dec
-                    if (t >= 1)
-                        mma3<SINGLE>(c.tbase + COL_C, c.tbase + A_H_HI, c.tbase + A_H_LO,
-                             sbase + tl.img64, 64, true);                // Wcomb_h
+                    mma3<SINGLE>(c.tbase + COL_Q, c.tbase + A_H_HI, c.tbase + A_H_LO,
+                         sbase, 128, true);                              // att_dec | Wcomb_h
                     umma::commit(&mbar);
                     if (!last) {
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + A_H_HI, c.tbase + A_H_LO,
@@ -1029,6 +1037,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     float q[U];
                     readU(c, COL_Q, q);
+                    zero_units(c, COL_Q);   // Q accumulates from zero in the next GEMM1
                     attn_scores(c, Es, t + 1, q, att_v, vsum, rawmask, s_part, L);   // causal: j <= t
                 }
                 __syncthreads();
@@ -1226,6 +1235,8 @@ struct BSpec {
                       // 0: identity; 2: identity, scaled by 2 log2(e) (W_comb: the head's
                       // tanh denominators then need no FMUL)
     int64_t dst;      // byte offset of the hi image in the TC blob
+    int row0 = 0;     // first B row written (several matrices stacked along N in one image)
+    int img_n = 0;    // N of the whole image (lo image at dst + img_n * 128); 0 = N
 };
 
 __global__ void bimage_kernel(const float *raw, uint8_t *out, BSpec s, int d) {
@@ -1238,9 +1249,10 @@ __global__ void bimage_kernel(const float *raw, uint8_t *out, BSpec s, int d) {
                         (s.gates == 1 ? gate_scale(n & 3) : s.gates == 2 ? 2.0f * kLog2e : 1.0f);
         const __half hi = __float2half_rn(w);
         const __half lo = __float2half_rn(w - __half2float(hi));
-        const uint32_t off = umma::kmajor_offset(n, k, 64);
+        const uint32_t off = umma::kmajor_offset(n + s.row0, k, 64);
+        const int64_t img_n = s.img_n ? s.img_n : s.N;
         *reinterpret_cast<__half *>(out + s.dst + off) = hi;
-        *reinterpret_cast<__half *>(out + s.dst + (int64_t)s.N * 128 + off) = lo;
+        *reinterpret_cast<__half *>(out + s.dst + img_n * 128 + off) = lo;
     }
 }
 
@@ -1420,8 +1432,12 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
         spec(0, 0, r.enc_wh[0], 4 * d, 256, 1);
         spec(0, 1, r.att_enc, d, 64, 0);
         spec(1, 2, r.dec_wh[0], 4 * d, 256, 1);
+        // att_dec | Wcomb_h (rows 0..d-1: the h part) stacked as one N = 128 image
         spec(1, 3, r.att_dec, d, 64, 0);
-        spec(1, 4, r.comb_w, d, 64, 2);                       // rows 0..d-1: h part
+        specs.back().img_n = 128;
+        spec(1, 3, r.comb_w, d, 64, 2);
+        specs.back().row0 = 64;
+        specs.back().img_n = 128;
         spec(1, 5, r.dec_wx[0] + 2 * d * 4 * d, 4 * d, 256, 1); // rows 2d..3d-1: ctx part
         spec(1, 6, r.comb_w + d * d, d, 64, 2);               // rows d..2d-1: ctx part
     } else {
