@@ -600,24 +600,57 @@ __device__ __forceinline__ float score_slow(const float4 (&x)[NQ], const float (
 
 // partial attention scores over this thread's units (model.py:118-119),
 // two positions per iteration so 2*NQ loads are in flight
+#ifndef RECMG_SCORE_POS
+#define RECMG_SCORE_POS 4
+#endif
+// partial attention scores over this thread's units (model.py:118-119) from
+// the query in TMEM column col_q.  Warps whose positions and query are all in
+// the fast (exponential-product) range -- the common case -- run a loop that
+// keeps no raw query in registers and has RECMG_SCORE_POS positions' loads in
+// flight; otherwise the two-position loop with the direct-form fallback runs.
 template <int PARTS>
 __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int npos,
-                                            const float (&q)[Ctx<PARTS>::U], const float *vp,
+                                            uint32_t col_q, const float *vp,
                                             float vsum, uint32_t rawmask, float *s_part, int L) {
     constexpr int NQ = Ctx<PARTS>::NQ;
     constexpr int U = Ctx<PARTS>::U;
     const float4 *v4 = reinterpret_cast<const float4 *>(vp);   // float4 u of mine: unit(4u) / 4
     float qx[U];
     bool qok = true;
+    {
+        float q[U];
+        readU(c, col_q, q);
 #pragma unroll
-    for (int k = 0; k < U; k++) {
-        qok = qok && fabsf(q[k]) <= 0.5f * kExpLim;
-        qx[k] = ex2f(q[k] * (2.0f * kLog2e));
+        for (int k = 0; k < U; k++) {
+            qok = qok && fabsf(q[k]) <= 0.5f * kExpLim;
+            qx[k] = ex2f(q[k] * (2.0f * kLog2e));
+        }
     }
-    const uint32_t slow = qok ? rawmask : 0xFFFFFFFFu;
+    const uint32_t npmask = npos >= 32 ? 0xFFFFFFFFu : ((1u << npos) - 1u);
+    const uint32_t slow = (qok ? rawmask : 0xFFFFFFFFu) & npmask;
     float4 vr[NQ];   // this thread's att_v units, loaded once per step
 #pragma unroll
     for (int u = 0; u < NQ; u++) vr[u] = __ldg(v4 + c.unit(4 * u) / 4);
+    float *sp = s_part + (c.part * L) * 128 + c.row;
+    if (!__any_sync(0xFFFFFFFFu, slow != 0u)) {
+        constexpr int P = RECMG_SCORE_POS;
+        int j = 0;
+        for (; j + P <= npos; j += P) {
+            float4 e[P][NQ];
+#pragma unroll
+            for (int i = 0; i < P; i++) scr_ld_pos(Es, c, j + i, e[i]);
+#pragma unroll
+            for (int i = 0; i < P; i++) sp[(j + i) * 128] = vsum + score_fast<NQ>(e[i], qx, vr);
+        }
+        for (; j < npos; j++) {
+            float4 e0[NQ];
+            scr_ld_pos(Es, c, j, e0);
+            sp[j * 128] = vsum + score_fast<NQ>(e0, qx, vr);
+        }
+        return;
+    }
+    float q[U];   // warp-uniform reload for the direct form
+    readU(c, col_q, q);
     auto score = [&](const float4 (&x)[NQ], int j) {
         return ((slow >> j) & 1u) ? score_slow<NQ>(x, q, vr, (rawmask >> j) & 1u)
                                   : vsum + score_fast<NQ>(x, qx, vr);
@@ -626,13 +659,13 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
     for (; j + 2 <= npos; j += 2) {
         float4 e0[NQ], e1[NQ];
         scr_ld_pos(Es, c, j, e0); scr_ld_pos(Es, c, j + 1, e1);
-        s_part[(c.part * L + j) * 128 + c.row] = score(e0, j);
-        s_part[(c.part * L + j + 1) * 128 + c.row] = score(e1, j + 1);
+        sp[j * 128] = score(e0, j);
+        sp[(j + 1) * 128] = score(e1, j + 1);
     }
     if (j < npos) {
         float4 e0[NQ];
         scr_ld_pos(Es, c, j, e0);
-        s_part[(c.part * L + j) * 128 + c.row] = score(e0, j);
+        sp[j * 128] = score(e0, j);
     }
 }
 
@@ -1035,10 +1068,8 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(5);
                 if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_C, comb_b, head_w);
                 if (!last) {
-                    float q[U];
-                    readU(c, COL_Q, q);
+                    attn_scores(c, Es, t + 1, COL_Q, att_v, vsum, rawmask, s_part, L);  // causal: j <= t
                     zero_units(c, COL_Q);   // Q accumulates from zero in the next GEMM1
-                    attn_scores(c, Es, t + 1, q, att_v, vsum, rawmask, s_part, L);   // causal: j <= t
                 }
                 __syncthreads();
                 if (t >= 1 && c.part == 0) {
@@ -1140,9 +1171,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(5);
                 if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_Z, comb_b, head_w);
                 if (!last) {
-                    float q[U];
-                    readU(c, COL_Q, q);
-                    attn_scores(c, Es, L, q, att_v, vsum, rawmask, s_part, L);      // non-causal
+                    attn_scores(c, Es, L, COL_Q, att_v, vsum, rawmask, s_part, L);  // non-causal
                 }
                 __syncthreads();
                 if (t >= 1 && c.part == 0) {
