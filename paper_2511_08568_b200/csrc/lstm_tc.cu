@@ -688,6 +688,9 @@ __device__ __forceinline__ void acc_ctx(float (&ctx)[4 * NQ], float e, const flo
     }
 }
 
+#ifndef RECMG_CTX_POS
+#define RECMG_CTX_POS 3
+#endif
 constexpr float kShiftMax = 40.0f;   // e^(-2 * 40) = 1.8e-35 > FLT_MIN
 
 // softmax over positions + context on this thread's units (model.py:120-123)
@@ -709,6 +712,18 @@ __device__ __forceinline__ void attn_context(const Ctx<PARTS> &c, float *Hs, int
     for (int k = 0; k < 4 * NQ; k++) ctx[k] = 0.0f;
     float sum = 0.0f;
     int j = 0;
+    constexpr int P = RECMG_CTX_POS;   // positions' loads in flight
+    for (; j + P <= npos; j += P) {
+        float4 hv[P][NQ];
+#pragma unroll
+        for (int i = 0; i < P; i++) scr_ld_pos(Hs, c, j + i, hv[i]);
+#pragma unroll
+        for (int i = 0; i < P; i++) {
+            const float e = __expf(full_score<PARTS>(s_part, L, j + i, c.row) - mx);
+            sum += e;
+            acc_ctx<NQ>(ctx, e, hv[i]);
+        }
+    }
     for (; j + 2 <= npos; j += 2) {
         float4 h0[NQ], h1[NQ];
         scr_ld_pos(Hs, c, j, h0); scr_ld_pos(Hs, c, j + 1, h1);
