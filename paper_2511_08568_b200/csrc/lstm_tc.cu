@@ -244,7 +244,7 @@ __device__ __forceinline__ void mma3_zhalf(uint32_t tbase, uint32_t a_hi, uint32
 // product committed to bar_a only (measured per model and phase: the split
 // pays where the products are long -- the prefetch model's two-operand layers --
 // and costs where one N = 256 product is short)
-template <bool SINGLE, bool SPLIT>
+template <bool SINGLE, bool SPLIT, bool BOTH = false>
 __device__ __forceinline__ void zproduct(uint32_t tbase, uint32_t a_hi, uint32_t a_lo,
                                          uint32_t b_saddr, bool acc, uint64_t *bar_a,
                                          uint64_t *bar_b) {
@@ -256,7 +256,27 @@ __device__ __forceinline__ void zproduct(uint32_t tbase, uint32_t a_hi, uint32_t
     } else {
         mma3<SINGLE>(tbase + COL_Z, a_hi, a_lo, b_saddr, 256, acc);
         umma::commit(bar_a);
-        (void)bar_b;
+        if constexpr (BOTH) umma::commit(bar_b);   // the caller's cell waits on both
+    }
+}
+// Z (+)= a1 * b1 + a2 * b2 (two operands, e.g. h0 Wx1 + h1 Wh1), split as above;
+// unsplit it commits both barriers
+template <bool SINGLE, bool SPLIT>
+__device__ __forceinline__ void zproduct2(uint32_t tbase, uint32_t a1_hi, uint32_t a1_lo,
+                                          uint32_t b1, bool acc1, uint32_t a2_hi, uint32_t a2_lo,
+                                          uint32_t b2, uint64_t *bar_a, uint64_t *bar_b) {
+    if constexpr (SPLIT) {
+#pragma unroll
+        for (int hf = 0; hf < 2; hf++) {
+            mma3_zhalf<SINGLE>(tbase, a1_hi, a1_lo, b1, acc1, hf);
+            mma3_zhalf<SINGLE>(tbase, a2_hi, a2_lo, b2, true, hf);
+            umma::commit(hf == 0 ? bar_a : bar_b);
+        }
+    } else {
+        mma3<SINGLE>(tbase + COL_Z, a1_hi, a1_lo, b1, 256, acc1);
+        mma3<SINGLE>(tbase + COL_Z, a2_hi, a2_lo, b2, 256, true);
+        umma::commit(bar_a);
+        umma::commit(bar_b);
     }
 }
 
@@ -799,6 +819,13 @@ __device__ __forceinline__ void emit_logit(const TcArgs &a, int64_t chunk, int T
 #endif
 constexpr bool kSplitCEnc = RECMG_ZSPLIT_CENC != 0;   // caching encoder Z += h Wh
 constexpr bool kSplitCDec = RECMG_ZSPLIT_CDEC != 0;   // caching decoder Z += ctx Wc
+#ifndef RECMG_ZSPLIT_P
+#define RECMG_ZSPLIT_P 15
+#endif
+constexpr bool kSplitPL0 = (RECMG_ZSPLIT_P & 1) != 0;  // prefetch encoder layer 0
+constexpr bool kSplitPL1 = (RECMG_ZSPLIT_P & 2) != 0;  // prefetch encoder layer 1
+constexpr bool kSplitPD0 = (RECMG_ZSPLIT_P & 4) != 0;  // prefetch decoder layer 0
+constexpr bool kSplitPD1 = (RECMG_ZSPLIT_P & 8) != 0;  // prefetch decoder layer 1
 
 template <int KIND, int MODE>
 __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(TcArgs a) {
@@ -948,13 +975,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (c.tid == 0) {
                     umma::fence_after();
                     if (!last) {
-                        // layer 0: Z = Pid + Ptab + h0 Wh0 (slot), two halves
-                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                                           sbase + tl.eslot, true, 0);
-                        umma::commit(&mbar);
-                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                                           sbase + tl.eslot, true, 1);
-                        umma::commit(&mbar3);
+                        // layer 0: Z = Pid + Ptab + h0 Wh0 (slot)
+                        zproduct<SINGLE, kSplitPL0, true>(c.tbase, c.tbase + P_H0_HI,
+                                                          c.tbase + P_H0_LO, sbase + tl.eslot,
+                                                          true, &mbar, &mbar3);
                     }
                     if (t >= 1) {
                         mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
@@ -982,14 +1006,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     // layer 1: Z = h0 Wx1 + h1 Wh1 (+b1 in the cell)
                     if (c.tid == 0) {
                         umma::fence_after();
-#pragma unroll
-                        for (int hf = 0; hf < 2; hf++) {
-                            mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                                               sbase + tl.eslot, false, hf);   // Wx1 (slot)
-                            mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                                               sbase, true, hf);               // Wh1
-                            umma::commit(hf == 0 ? &mbar : &mbar3);
-                        }
+                        zproduct2<SINGLE, kSplitPL1>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                                     sbase + tl.eslot, false,      // Wx1 (slot)
+                                                     c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                                                     sbase, &mbar, &mbar3);        // Wh1
                     }
                 }
                 if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
@@ -1207,14 +1227,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(7);
                 if (c.tid == 0) {
                     umma::fence_after();
-#pragma unroll
-                    for (int hf = 0; hf < 2; hf++) {
-                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
-                                           sbase, true, hf);                  // Wctx0
-                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                                           sbase + tl.img256, true, hf);      // Wh0
-                        umma::commit(hf == 0 ? &mbar : &mbar3);
-                    }
+                    zproduct2<SINGLE, kSplitPD0>(c.tbase, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
+                                                 sbase, true,                       // Wctx0
+                                                 c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                                 sbase + tl.img256, &mbar, &mbar3);  // Wh0
                 }
                 wait_mma(&mbar, phase);
                 pc.mark(8);
@@ -1233,14 +1249,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 tmem_writes_done();
                 if (c.tid == 0) {
                     umma::fence_after();
-#pragma unroll
-                    for (int hf = 0; hf < 2; hf++) {
-                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
-                                           sbase + tl.b_off[9], false, hf);
-                        mma3_zhalf<SINGLE>(c.tbase, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                                           sbase + tl.b_off[10], true, hf);
-                        umma::commit(hf == 0 ? &mbar : &mbar3);
-                    }
+                    zproduct2<SINGLE, kSplitPD1>(c.tbase, c.tbase + P_H0_HI, c.tbase + P_H0_LO,
+                                                 sbase + tl.b_off[9], false,
+                                                 c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                                                 sbase + tl.b_off[10], &mbar, &mbar3);
                 }
                 pc.mark(10);
                 wait_mma(&mbar, phase);
