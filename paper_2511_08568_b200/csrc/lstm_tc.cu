@@ -455,7 +455,7 @@ __device__ __forceinline__ void init_z_from_row(const Ctx<PARTS> &c, const float
         uint32_t r[16];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-            const float4 x = __ldg(a + q);
+            const float4 x = a[q];
             r[4 * q + 0] = __float_as_uint(x.x);
             r[4 * q + 1] = __float_as_uint(x.y);
             r[4 * q + 2] = __float_as_uint(x.z);
@@ -494,7 +494,7 @@ __device__ __forceinline__ void cell(const Ctx<PARTS> &c, const float *bias,
                 const float *z = g4 == 0 ? &z0[4 * u] : &z1[4 * u];
                 float zi = z[0], zf = z[1], zg = z[2], zo = z[3];
                 if (BIAS) {
-                    const float4 bb = __ldg(b4 + c.unit(j));
+                    const float4 bb = b4[c.unit(j)];
                     zi += bb.x; zf += bb.y; zg += bb.z; zo += bb.w;
                 }
                 float ig = ex2_den(zi), fg = ex2_den(zf), gd = ex2_den(zg), o = ex2_den(zo);
@@ -650,7 +650,7 @@ __device__ __forceinline__ void attn_scores(const Ctx<PARTS> &c, float *Es, int 
     const uint32_t slow = (qok ? rawmask : 0xFFFFFFFFu) & npmask;
     float4 vr[NQ];   // this thread's att_v units, loaded once per step
 #pragma unroll
-    for (int u = 0; u < NQ; u++) vr[u] = __ldg(v4 + c.unit(4 * u) / 4);
+    for (int u = 0; u < NQ; u++) vr[u] = v4[c.unit(4 * u) / 4];
     float *sp = s_part + (c.part * L) * 128 + c.row;
     if (!__any_sync(0xFFFFFFFFu, slow != 0u)) {
         constexpr int P = RECMG_SCORE_POS;
@@ -777,7 +777,7 @@ __device__ __forceinline__ float head_partial(const Ctx<PARTS> &c, uint32_t col,
     const float4 *hw4 = reinterpret_cast<const float4 *>(head_w);
 #pragma unroll
     for (int k = 0; k < U; k += 4) {
-        const float4 cb = __ldg(cb4 + c.unit(k) / 4), hw = __ldg(hw4 + c.unit(k) / 4);
+        const float4 cb = cb4[c.unit(k) / 4], hw = hw4[c.unit(k) / 4];
         float d[4] = {ex2_den(v[k] + cb.x), ex2_den(v[k + 1] + cb.y), ex2_den(v[k + 2] + cb.z),
                       ex2_den(v[k + 3] + cb.w)};
         rcp4(d[0], d[1], d[2], d[3]);
@@ -878,14 +878,39 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     const float *pid_dec = reinterpret_cast<const float *>(a.blob + tl.pid[1]);
     float *Hs = a.scratch + (int64_t)blockIdx.x * 2 * L * 128 * 64;
     float *Es = Hs + (int64_t)L * 128 * 64;
-    const float *att_v = a.dense + pl.att_v;
-    const float *comb_b = a.dense + pl.comb_b;
-    const float *head_w = a.dense + pl.head_w;
+    // the per-unit constants every step reads (layer-1 biases, att_v, comb bias,
+    // head weights, prefetch slot projections) live in shared memory: broadcast
+    // LDS instead of LDG, the L1 tag stage is kept for the row gathers
+    float *cst = reinterpret_cast<float *>(smem + tl.const_off);
+    {
+        const int nslot = caching ? 0 : a.m.l_out * 256;
+        for (int i = c.tid; i < 704 + nslot; i += NT) {
+            float v = 0.0f;
+            if (i < 512) {
+                if (!caching) v = __ldg(a.dense + (i < 256 ? pl.enc_b[1] + i : pl.dec_b[1] + i - 256));
+            } else if (i < 576) {
+                v = __ldg(a.dense + pl.att_v + i - 512);
+            } else if (i < 640) {
+                v = __ldg(a.dense + pl.comb_b + i - 576);
+            } else if (i < 704) {
+                v = __ldg(a.dense + pl.head_w + i - 640);
+            } else {
+                v = __ldg(a.dense + pl.slot_proj + i - 704);
+            }
+            cst[i] = v;
+        }
+        __syncthreads();
+    }
+    const float *enc_b1 = cst, *dec_b1 = cst + 256;
+    const float *att_v = cst + 512;
+    const float *comb_b = cst + 576;
+    const float *head_w = cst + 640;
+    const float *slot_proj = cst + 704;
     const float head_b = __ldg(a.dense + pl.head_b);
     float vsum = 0.0f;   // sum of this thread's att_v units (score_fast)
-    for (int k = 0; k < U; k++) vsum += __ldg(att_v + c.unit(k));
+    for (int k = 0; k < U; k++) vsum += att_v[c.unit(k)];
     float vabs = 0.0f;   // sum over all d units of |att_v| (attn_context's shift)
-    for (int k = 0; k < 64; k++) vabs += fabsf(__ldg(att_v + k));
+    for (int k = 0; k < 64; k++) vabs += fabsf(att_v[k]);
     const int64_t n_tiles = (a.batch + 127) / 128;
 
     // dynamic tile scheduler: a CTA that starts late (its SM busy with a
@@ -1024,7 +1049,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     wait_mma(&mbar, phase);
                     pc.mark(11);
-                    cell<true>(c, a.dense + pl.enc_b[1], cs1, h, [&] {
+                    cell<true>(c, enc_b1, cs1, h, [&] {
                         wait_mma(&mbar3, phase3);
                         if (t + 1 < L && c.tid == 0) {   // Wx1 done: Wh0 back for the next step
                             umma::mbar_expect_tx(&tma_bar, (uint32_t)tl.img256);
@@ -1221,7 +1246,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 attn_context(c, Hs, L, s_part, L, vabs, ctx);
                 store_operand<SINGLE>(c, P_CTX_HI, P_CTX_LO, ctx);
                 // layer 0: Z = slot_proj[t] + ctx Wctx0 + h0 Wh0   (model.py:208-209)
-                init_z_from_row(c, a.dense + pl.slot_proj + (int64_t)t * 256);
+                init_z_from_row(c, slot_proj + t * 256);
                 wait_mma(&tma_bar, tphase);                      // Wctx0 | Wh0 in the region
                 tmem_writes_done();
                 pc.mark(7);
@@ -1257,7 +1282,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(10);
                 wait_mma(&mbar, phase);
                 pc.mark(11);
-                cell<true>(c, a.dense + pl.dec_b[1], cs1, h, [&] {
+                cell<true>(c, dec_b1, cs1, h, [&] {
                     wait_mma(&mbar3, phase3);
                     // layer 1 done: att_dec | Wcomb back for the next step's GEMM1
                     if (c.tid == 0) {
@@ -1437,6 +1462,9 @@ TcLayout tc_layout(const recmg_model_shape *m) {
                                                                      : (size_t)t.phase_len[0];
     if (m->kind == RECMG_MODEL_PREFETCH) wmax = (size_t)(t.eslot + t.img256);   // encoder 144 KB
     t.smem_bytes = wmax > t.spart_off + spart ? wmax : t.spart_off + spart;
+    // per-unit constants (lstm_tc_kernel: biases, att_v, comb_b, head_w, slot_proj)
+    t.const_off = (t.smem_bytes + 15) / 16 * 16;
+    t.smem_bytes = t.const_off + (size_t)(704 + (m->kind == RECMG_MODEL_CACHING ? 0 : m->l_out * 256)) * 4;
     t.total = o;
     return t;
 }

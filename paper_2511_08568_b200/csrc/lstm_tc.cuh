@@ -10,6 +10,7 @@ struct TcLayout {              // byte offsets into the TC blob
     int nb;
     int64_t pid[2];                      // folded token tables (enc, dec) [ids][256] fp32
     size_t spart_off, smem_bytes;
+    size_t const_off;                    // per-unit constants in shared memory
     int64_t img64, img256, dslot;        // B image bytes (N = 64 / 256); caching decoder slot
     int64_t eslot;                       // prefetch encoder slot (Wh0 <-> Wx1)
     int64_t swap_off;                    // prefetch: DEC-B swap region (bytes in smem)
