@@ -77,7 +77,10 @@ def parse():
                     help="skip the K5/K6 host-row gather + EmbeddingBag measurement")
     ap.add_argument("--row-dim", type=int, default=128)
     ap.add_argument("--pool", type=int, default=2, help="EmbeddingBag pooling factor")
-    ap.add_argument("--pieces", type=int, default=8, help="replay pipeline pieces")
+    ap.add_argument("--pieces", type=int, default=None,
+                    help="replay pipeline pieces (default: 1 = the replay after both forwards "
+                         "for config 2; 8 pipelined pieces for config 3, whose shard-0 hot "
+                         "set makes the replay a single long chain)")
     ap.add_argument("--model-sms", type=int, default=136, help="SMs the forwards may use")
     ap.add_argument("--batch", type=int, default=512, help="config 4: samples per batch")
     ap.add_argument("--config", type=int, default=None, choices=[2, 3, 4],
@@ -105,6 +108,8 @@ def parse():
             # more SMs beside the forwards (measured: 146 -> 124 SMs, +17%)
             args.model_sms = 124
         args.no_rows = True   # 44 GB of pinned host rows: config 2 measures K5/K6
+    if args.pieces is None:
+        args.pieces = 8 if args.config == 3 else 1
     return args
 
 

@@ -132,6 +132,25 @@ int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t 
                         uint16_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
                         void *stream);
 
+/* recmg_replay_chunks with flags.  RECMG_REPLAY_SKIP_STATS: the per-chunk
+ * prefetch statistics (prefetch_issued / prefetch_useful and the coverage
+ * counts of runtime.py:271-276) of this range were already produced by
+ * recmg_prefetch_stats, so only the buffer replay runs.                     */
+#define RECMG_REPLAY_SKIP_STATS 1
+int recmg_replay_chunks_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids,
+                           int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio,
+                           int64_t k_begin, int64_t k_end, int32_t with_tail, const uint8_t *bits,
+                           const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
+                           uint16_t *cov_num, uint16_t *cov_den, uint8_t *access_class,
+                           void *ws, size_t ws_bytes, int32_t flags, void *stream);
+/* The prefetch statistics of chunks [k_begin, k_end) alone: they depend only
+ * on the ids and the decoded prefetch ids (runtime.py:271-276), not on the
+ * buffer, so they can run as soon as the prefetch forward is done.          */
+int recmg_prefetch_stats(const int32_t *gids, int64_t n, int32_t l_in, int32_t l_out,
+                         int32_t window_ratio, int64_t k_begin, int64_t k_end, const int32_t *pf,
+                         int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
+                         uint16_t *cov_den, void *stream);
+
 /* Host: sequential float64 mean of num/den in chunk order (runtime.py:276,282). */
 double recmg_coverage_mean(const uint16_t *host_num, const uint16_t *host_den, int64_t K);
 /* Host: acc + the same left-to-right float64 sum over `count` chunks, for
@@ -288,6 +307,23 @@ int recmg_model_forward_ex(const recmg_model_shape *shape, int32_t precision,
                            const int32_t *tid, int64_t batch, int64_t decode_ids, float *logits,
                            uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes,
                            void *stream);
+
+/* recmg_model_forward_ex (TC32 / TC16 only) that also reports progress for a
+ * consumer on another stream: every finished tile of 128 chunks adds one to
+ * progress[(tile * 128) / piece_chunks] (device int32 counters, zeroed by the
+ * caller; piece_chunks a multiple of 128), released after the tile's logits,
+ * bits and decoded ids are visible device-wide.  Lets one forward launch over
+ * the whole trace feed a piecewise replay without launch boundaries between
+ * the pieces (pipeline.HotPath).                                            */
+int recmg_model_forward_signal(const recmg_model_shape *shape, int32_t precision,
+                               const float *embed_id, const void *packed, const int32_t *gid,
+                               const int32_t *tid, int64_t batch, int64_t decode_ids,
+                               float *logits, uint8_t *bits, int32_t *pf_gid, void *ws,
+                               size_t ws_bytes, int32_t *progress, int64_t piece_chunks,
+                               void *stream);
+/* Stream-ordered wait: work queued on `stream` after this call starts once
+ * progress[piece] >= target (acquire; one 1-thread kernel that polls).      */
+int recmg_wait_progress(const int32_t *progress, int64_t piece, int32_t target, void *stream);
 
 /* Upper bound on the CTAs (= SMs) the TC32 forwards occupy (default 148);
  * returns the previous value.  Leaving a few SMs to the replay lets a

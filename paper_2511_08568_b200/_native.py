@@ -36,6 +36,7 @@ OP_ADD, OP_POPULATE, OP_REFERENCE, OP_SET_PRIORITY, OP_QUERY = range(5)
 MODEL_CACHING, MODEL_PREFETCH = 0, 1
 PREC_FP32 = 0
 PREC_TC32 = 1
+REPLAY_SKIP_STATS = 1   # recmg.h RECMG_REPLAY_SKIP_STATS
 PREC_TC16 = 2
 
 # every symbol include/recmg.h declares (tests check the export table)
@@ -52,6 +53,8 @@ EXPORTS = (
     "recmg_trace_generate_block", "recmg_shard_local_ids", "recmg_trace_parse_text",
     "recmg_coverage_accumulate", "recmg_embedding_bag_a2a", "recmg_peer_alloc",
     "recmg_peer_free", "recmg_peer_handle", "recmg_peer_open", "recmg_peer_close",
+    "recmg_model_forward_signal", "recmg_wait_progress", "recmg_replay_chunks_ex",
+    "recmg_prefetch_stats",
 )
 
 
@@ -107,6 +110,11 @@ def lib():
         "recmg_peer_close": (ctypes.c_int, [vp]),
         "recmg_replay_chunks": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64, i32,
                                                vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
+        "recmg_replay_chunks_ex": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64,
+                                                  i32, vp, vp, i32, vp, vp, vp, vp, vp, sz, i32,
+                                                  vp]),
+        "recmg_prefetch_stats": (ctypes.c_int, [vp, i64, i32, i32, i32, i64, i64, vp, i32, vp,
+                                                vp, vp, vp]),
         "recmg_set_model_sm_budget": (ctypes.c_int, [ctypes.c_int]),
         "recmg_rows_refresh": (ctypes.c_int, [cfgp, vp, vp, vp, i32, vp, vp, vp]),
         "recmg_embedding_bag": (ctypes.c_int, [cfgp, vp, vp, vp, i64, vp, vp, i32, vp, vp, vp]),
@@ -122,6 +130,9 @@ def lib():
                                                sz, vp]),
         "recmg_model_forward_ex": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, i64, vp, vp,
                                                   vp, vp, sz, vp]),
+        "recmg_model_forward_signal": (ctypes.c_int, [shp, i32, vp, vp, vp, vp, i64, i64, vp,
+                                                      vp, vp, vp, sz, vp, i64, vp]),
+        "recmg_wait_progress": (ctypes.c_int, [vp, i64, i32, vp]),
         "recmg_trace_parse_text": (ctypes.c_int, [vp, i64, i64, vp, i32, vp, i64, vp, vp, vp]),
         "recmg_shard_local_ids": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, vp, vp, vp]),
         "recmg_pcg64_uniforms": (ctypes.c_int, [vp, i64, i64, vp, i32]),

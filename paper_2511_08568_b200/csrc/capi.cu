@@ -1,4 +1,6 @@
 // extern "C" entry points declared in include/recmg.h.
+#include <chrono>
+#include <cstdio>
 #include <string.h>
 
 #include "lstm.cuh"
@@ -55,24 +57,52 @@ bool plan_replay(const recmg_buffer_cfg *cfg, int64_t n, int32_t l_in, int32_t l
     return true;
 }
 
+#ifdef RECMG_CHAIN_TIMING
+// diagnostic builds only: host wall time of each stage of the replay chain
+struct ChainTimer {
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t;
+    explicit ChainTimer(cudaStream_t st) : s(st) {
+        cudaStreamSynchronize(s);
+        t = std::chrono::steady_clock::now();
+    }
+    void lap(const char *what) {
+        cudaStreamSynchronize(s);
+        const auto u = std::chrono::steady_clock::now();
+        fprintf(stderr, "chain %-10s %8.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(u - t).count());
+        t = u;
+    }
+};
+#define RECMG_LAP(x) tm.lap(x)
+#else
+struct ChainTimer {
+    explicit ChainTimer(cudaStream_t) {}
+};
+#define RECMG_LAP(x) ((void)0)
+#endif
+
 int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
                  int32_t l_in, int32_t l_out, int32_t window_ratio, int64_t k_begin,
                  int64_t k_end, int with_tail, const uint8_t *bits, const int32_t *pf,
                  int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
                  uint16_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
-                 cudaStream_t s) {
+                 cudaStream_t s, int32_t flags = 0) {
     if (!pf) pf_stride = 0;
+    ChainTimer tm(s);
+    (void)tm;
     Arena a{(char *)ws, ws_bytes, 0};
     ReplayPlan p;
     if (!state || !counters || (n > 0 && !gids)) return RECMG_E_INVALID_CONFIG;
     if (!plan_replay(cfg, n, l_in, l_out, window_ratio, pf_stride, access_class != nullptr,
                      k_begin, k_end, with_tail != 0, a, p))
         return RECMG_E_INVALID_CONFIG;
-    if (p.nk > 0) {
+    if (p.nk > 0 && !(flags & RECMG_REPLAY_SKIP_STATS)) {
         prefetch_stats_kernel<<<(unsigned)((p.nk + 255) / 256), 256, 0, s>>>(
             gids, p.k0, p.nk, l_in, window_ratio * l_out, pf, pf_stride, cov_num, cov_den,
             counters);
         RECMG_LAUNCH_CHECK();
+        RECMG_LAP("stats");
     }
     if (p.E == 0) return RECMG_OK;
     if (!a.ok() || !ws) return RECMG_E_WORKSPACE;
@@ -85,6 +115,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
                                                 (uint32_t)p.g.S, magic, p.ev, p.vv, counters,
                                                 access_class);
         RECMG_LAUNCH_CHECK();
+        RECMG_LAP("events");
         i_begin = p.nk * p.Ec;
     }
     if (p.E > i_begin) {
@@ -100,6 +131,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     if (p.g.S > 1) {
         int rc = partition_run(p.pb, ev, vv, s);
         if (rc) return rc;
+        RECMG_LAP("partition");
         ra.seg_start = p.pb.seg_start;
         ra.seg_end = p.pb.seg_end;
         ra.heavy = p.g.wide ? nullptr : p.pb.heavy;
@@ -119,6 +151,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     ra.access_class = access_class;
     int rc = launch_replay(cfg->policy, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
     if (rc) return rc;
+    RECMG_LAP("replay");
     if (cfg->policy == RECMG_POLICY_LRU_PF) {
         // clocks are event positions of this call: keep them monotonic across calls
         clock_bump_kernel<<<1, 1, 0, s>>>(st.header, p.E);
@@ -206,6 +239,39 @@ int recmg_replay(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, 0, -1, 1, bits, pf,
                         pf_stride, counters, cov_num, cov_den, access_class, ws, ws_bytes,
                         as_stream(stream));
+}
+
+int recmg_replay_chunks_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids,
+                           int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio,
+                           int64_t k_begin, int64_t k_end, int32_t with_tail, const uint8_t *bits,
+                           const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
+                           uint16_t *cov_num, uint16_t *cov_den, uint8_t *access_class,
+                           void *ws, size_t ws_bytes, int32_t flags, void *stream) {
+    if (flags & ~RECMG_REPLAY_SKIP_STATS) return RECMG_E_INVALID_CONFIG;
+    return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, k_begin, k_end,
+                        with_tail, bits, pf, pf_stride, counters, cov_num, cov_den,
+                        access_class, ws, ws_bytes, as_stream(stream), flags);
+}
+
+int recmg_prefetch_stats(const int32_t *gids, int64_t n, int32_t l_in, int32_t l_out,
+                         int32_t window_ratio, int64_t k_begin, int64_t k_end, const int32_t *pf,
+                         int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
+                         uint16_t *cov_den, void *stream) {
+    if (n < 0 || l_in < 1 || l_out < 1 || window_ratio < 1 || pf_stride < 0 || !counters ||
+        (int64_t)window_ratio * l_out > 65535)
+        return RECMG_E_INVALID_CONFIG;
+    const int64_t K = recmg_num_chunks(n, l_in, l_out, window_ratio);
+    if (k_begin < 0) k_begin = 0;
+    if (k_end < 0 || k_end > K) k_end = K;
+    if (k_begin > k_end || (k_end > k_begin && !gids)) return RECMG_E_INVALID_CONFIG;
+    if (!pf) pf_stride = 0;
+    const int64_t nk = k_end - k_begin;
+    if (nk == 0) return RECMG_OK;
+    cudaStream_t s = as_stream(stream);
+    prefetch_stats_kernel<<<(unsigned)((nk + 255) / 256), 256, 0, s>>>(
+        gids, k_begin, nk, l_in, window_ratio * l_out, pf, pf_stride, cov_num, cov_den, counters);
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
 }
 
 int recmg_replay_chunks(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, int64_t n,
@@ -437,6 +503,29 @@ size_t recmg_model_workspace_bytes(const recmg_model_shape *shape, int32_t preci
                                    int64_t batch) {
     if ((precision == RECMG_PREC_TC32 || precision == RECMG_PREC_TC16) && tc_supported(shape)) return tc_workspace_bytes(shape, batch);
     return 0;
+}
+
+int recmg_model_forward_signal(const recmg_model_shape *shape, int32_t precision,
+                               const float *embed_id, const void *packed, const int32_t *gid,
+                               const int32_t *tid, int64_t batch, int64_t decode_ids,
+                               float *logits, uint8_t *bits, int32_t *pf_gid, void *ws,
+                               size_t ws_bytes, int32_t *progress, int64_t piece_chunks,
+                               void *stream) {
+    if (!shape_ok(shape) || batch < 0 || !logits || decode_ids < 0 ||
+        decode_ids >= (int64_t)kGidMask || !progress)
+        return RECMG_E_INVALID_CONFIG;
+    if (batch > 0 && (!packed || !gid || !tid)) return RECMG_E_INVALID_CONFIG;
+    if (!((precision == RECMG_PREC_TC32 || precision == RECMG_PREC_TC16) && tc_supported(shape)))
+        return RECMG_E_INVALID_CONFIG;
+    return model_forward_tc(shape, packed, (const char *)packed + dense_bytes_aligned(shape), gid,
+                            tid, batch, logits, bits, pf_gid, ws, ws_bytes, as_stream(stream),
+                            nullptr, decode_ids, precision == RECMG_PREC_TC16, progress,
+                            piece_chunks);
+}
+
+int recmg_wait_progress(const int32_t *progress, int64_t piece, int32_t target, void *stream) {
+    if (!progress || piece < 0 || target < 0) return RECMG_E_INVALID_CONFIG;
+    return wait_progress(progress + piece, target, as_stream(stream));
 }
 
 int recmg_model_forward_ex(const recmg_model_shape *shape, int32_t precision,

@@ -110,6 +110,8 @@ struct TcArgs {
     int32_t *pf_gid;
     float *scratch;        // [gridDim.x][2][L][8][128] 32-byte pairs (scratch_at)
     int *tile_counter;     // dynamic tile scheduler (zeroed before the launch)
+    int *progress;         // nullable: finished tiles per piece (piece = tile / piece_tiles)
+    int64_t piece_tiles;
     long long *prof;       // PROF builds: per-CTA cycles per phase [grid][16]
 };
 
@@ -1293,8 +1295,19 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 store_operand<SINGLE>(c, P_H1_HI, P_H1_LO, h);
             }
         }
+        // progress signal for a consumer on another stream (recmg_wait_progress):
+        // every thread's outputs of this tile are made visible device-wide, then
+        // one arrival per tile is released on its piece's counter
+        if (a.progress) __threadfence();
         __syncthreads();
-        if (c.tid == 0) s_tile = atomicAdd(a.tile_counter, 1);
+        if (c.tid == 0) {
+            if (a.progress) {
+                const int64_t piece = tile / a.piece_tiles;
+                asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
+                             ::"l"(a.progress + piece) : "memory");
+            }
+            s_tile = atomicAdd(a.tile_counter, 1);
+        }
         __syncthreads();
         tile = s_tile;
     }
@@ -1567,8 +1580,10 @@ int set_model_sm_budget(int n) {
 int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const void *tc_blob,
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,
-                     long long *prof, int64_t decode_ids, bool single) {
+                     long long *prof, int64_t decode_ids, bool single, int32_t *progress,
+                     int64_t piece_chunks) {
     if (batch <= 0) return RECMG_OK;
+    if (progress && (piece_chunks <= 0 || piece_chunks % 128 != 0)) return RECMG_E_INVALID_CONFIG;
     const int64_t n_tiles = (batch + 127) / 128;
     const int grid = (int)imin64(n_tiles, g_model_sm_budget);
     if (ws_bytes < tc_workspace_bytes(m, batch)) return RECMG_E_WORKSPACE;
@@ -1586,6 +1601,8 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
     a.bits = bits;
     a.pf_gid = pf_gid;
     a.tile_counter = (int *)ws;
+    a.progress = progress;
+    a.piece_tiles = progress ? piece_chunks / 128 : 1;
     a.scratch = (float *)((char *)ws + 256);
     RECMG_CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), s));
     a.prof = prof;
@@ -1606,6 +1623,21 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
         else RECMG_TC_LAUNCH(RECMG_MODEL_PREFETCH, 0);
     }
 #undef RECMG_TC_LAUNCH
+    RECMG_LAUNCH_CHECK();
+    return RECMG_OK;
+}
+
+__global__ void wait_progress_kernel(const int32_t *p, int32_t target) {
+    for (;;) {
+        int32_t v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+        if (v >= target) break;
+        __nanosleep(500);
+    }
+}
+
+int wait_progress(const int32_t *progress, int32_t target, cudaStream_t s) {
+    wait_progress_kernel<<<1, 1, 0, s>>>(progress, target);
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
 }

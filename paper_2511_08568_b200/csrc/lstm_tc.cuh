@@ -25,7 +25,9 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
                      const int32_t *gid, const int32_t *tid, int64_t batch, float *logits,
                      uint8_t *bits, int32_t *pf_gid, void *ws, size_t ws_bytes, cudaStream_t s,
                      long long *prof = nullptr, int64_t decode_ids = 0,
-                     bool single = false);
+                     bool single = false, int32_t *progress = nullptr,
+                     int64_t piece_chunks = 0);
+int wait_progress(const int32_t *progress, int32_t target, cudaStream_t s);
 size_t tc_workspace_bytes(const recmg_model_shape *m, int64_t batch);
 int set_model_sm_budget(int n);
 

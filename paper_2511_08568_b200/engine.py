@@ -70,19 +70,33 @@ class BufferReplay:
             _native.ptr(access_class), _native.ptr(self._ws), self._ws.numel(),
             _native.stream_handle(self.torch)), "replay")
 
-    def run_chunks(self, gids, k0, k1, with_tail, bits=None, pf=None):
+    def run_chunks(self, gids, k0, k1, with_tail, bits=None, pf=None, skip_stats=False):
         """Replay chunks [k0, k1) (+ tail) of the trace on the current state
-        (recmg_replay_chunks); consecutive ranges == one run()."""
+        (recmg_replay_chunks_ex); consecutive ranges == one run().  skip_stats:
+        the range's prefetch statistics were produced by stats_chunks()."""
         n = gids.numel()
         stride = int(pf.shape[1]) if pf is not None else 0
         self.reserve(n, stride)
         self.K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
-        _native.check(_native.lib().recmg_replay_chunks(
+        _native.check(_native.lib().recmg_replay_chunks_ex(
             ctypes.byref(self.cfg), _native.ptr(self.state), _native.ptr(gids), n, self.l_in,
             self.l_out, self.window_ratio, int(k0), int(k1), 1 if with_tail else 0,
             _native.ptr(bits), _native.ptr(pf), stride, _native.ptr(self.counters),
             _native.ptr(self._cov[0]), _native.ptr(self._cov[1]), None, _native.ptr(self._ws),
-            self._ws.numel(), _native.stream_handle(self.torch)), "replay_chunks")
+            self._ws.numel(), _native.REPLAY_SKIP_STATS if skip_stats else 0,
+            _native.stream_handle(self.torch)), "replay_chunks")
+
+    def stats_chunks(self, gids, k0, k1, pf=None):
+        """Prefetch statistics (counters + coverage counts) of chunks [k0, k1)
+        alone (recmg_prefetch_stats): they need the decoded ids, not the buffer."""
+        n = gids.numel()
+        stride = int(pf.shape[1]) if pf is not None else 0
+        self.reserve(n, stride)
+        self.K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
+        _native.check(_native.lib().recmg_prefetch_stats(
+            _native.ptr(gids), n, self.l_in, self.l_out, self.window_ratio, int(k0), int(k1),
+            _native.ptr(pf), stride, _native.ptr(self.counters), _native.ptr(self._cov[0]),
+            _native.ptr(self._cov[1]), _native.stream_handle(self.torch)), "prefetch_stats")
 
     def cov_host(self):
         """(num, den) uint16 arrays of the last run, copied to the host."""

@@ -280,13 +280,24 @@ class DeviceModel:
             self._ws = _native.device_bytes(torch, need)
         return self._ws
 
-    def forward(self, gid, tid, logits=None, bits=None, pf_gid=None):
-        """gid/tid: device int32 [B, l_in].  Returns logits [B, out_len] fp32."""
+    def forward(self, gid, tid, logits=None, bits=None, pf_gid=None, progress=None,
+                piece_chunks=0):
+        """gid/tid: device int32 [B, l_in].  Returns logits [B, out_len] fp32.
+        progress (device int32 counters) + piece_chunks: per-piece tile
+        completion signals for a consumer stream (recmg_model_forward_signal)."""
         torch = _native.torch_cuda()
         B = gid.shape[0]
         if logits is None:
             logits = torch.empty((B, self.out_len), dtype=torch.float32, device="cuda")
         ws = self.workspace(B)
+        if progress is not None:
+            _native.check(_native.lib().recmg_model_forward_signal(
+                ctypes.byref(self.shape), self.prec, _native.ptr(self.embed_id),
+                _native.ptr(self.packed), _native.ptr(gid), _native.ptr(tid), B,
+                self.decode_ids, _native.ptr(logits), _native.ptr(bits), _native.ptr(pf_gid),
+                _native.ptr(ws), ws.numel() if ws is not None else 0, _native.ptr(progress),
+                int(piece_chunks), _native.stream_handle(torch)), "model_forward_signal")
+            return logits
         _native.check(_native.lib().recmg_model_forward_ex(
             ctypes.byref(self.shape), self.prec, _native.ptr(self.embed_id),
             _native.ptr(self.packed), _native.ptr(gid), _native.ptr(tid), B, self.decode_ids,

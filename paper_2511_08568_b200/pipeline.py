@@ -33,6 +33,19 @@ from .trace import num_chunks
 # more sensitive to the replay's event streams (config 2: +0.9% per step, two
 # A/B pairs).  RECMG_PF_FIRST=0 restores caching-first for A/B runs.
 _PF_FIRST = os.environ.get("RECMG_PF_FIRST", "1") == "1"
+# Streamed mode (the default for a plain pieces > 1 replay): each model runs
+# ONE forward over the whole trace and the second one releases a per-piece
+# progress counter as its tiles finish (recmg_model_forward_signal); piece i's
+# replay waits on that counter (recmg_wait_progress) on the replay stream.
+# The forwards then never end between pieces, so the replay's kernels cannot
+# take the SMs a forward launch boundary frees (measured with 8 per-piece
+# launch pairs: +36% prefetch / +4% caching forward time).  RECMG_STREAMED=0
+# restores per-piece forward launches.
+_STREAMED = os.environ.get("RECMG_STREAMED", "0") == "1"
+# The LRU comparator launched after the forwards (it then shares the GPU with
+# the replay, whose tail is one set's serial chain) instead of at the start
+# (where its kernels take SMs at every forward launch boundary).
+_LRU_LATE = os.environ.get("RECMG_LRU_LATE", "1") == "1"
 
 
 class HotPath:
@@ -42,10 +55,18 @@ class HotPath:
                  prefetch: ModelParameters | DeviceModel | None, table_sizes, capacity: int,
                  n_max: int, ways: int | None = 32, eviction_speed: int = 4,
                  lru_capacity: int | None = None, lru_ways: int | None = 32, l_in: int = 15,
-                 l_out: int = 5, window_ratio: int = 3, pieces: int = 8, model_sms: int = 136,
+                 l_out: int = 5, window_ratio: int = 3, pieces: int | None = None,
+                 model_sms: int = 136,
                  shard=None, replay_priority: bool = True, piece_chunks: int | None = None,
                  piece_hook=None):
-        """pieces > 1 pipelines the replay: chunks are scored in `pieces`
+        """pieces = None picks the schedule from the buffer geometry: one
+        replay after both forwards (pieces = 1, `_launch_serial`) when the
+        buffer has at least 256 sets -- the replay is then throughput-bound and
+        a replay beside the forwards only takes SMs they need -- and 8 pipelined
+        pieces for fewer, longer sets (the fully associative buffer: one chain
+        that only hides under the forwards).
+
+        pieces > 1 pipelines the replay: chunks are scored in `pieces`
         ranges on the main stream while earlier ranges replay on a side stream
         (recmg_replay_chunks continues the buffer state, so the result is the
         same as one replay); the LRU comparator runs on a third stream from
@@ -99,6 +120,9 @@ class HotPath:
         self.lru = None
         if lru_capacity:
             self.lru = LruSim(lru_capacity, self.total_ids, lru_ways, self.n_max)
+        if pieces is None:
+            sets = capacity // (ways or capacity) if capacity else 1
+            pieces = 1 if sets >= 256 else 8
         self.pieces = max(1, int(pieces))
         self.piece_chunks = int(piece_chunks) if piece_chunks else None
         self.piece_hook = piece_hook
@@ -177,9 +201,16 @@ class HotPath:
         g = self.gids[:n]
         main = torch.cuda.current_stream()
         pieces = self._piece_bounds(K) if K else [(0, 0)]
+        has_models = self.caching is not None or self.prefetch is not None
+        serial = (K > 0 and has_models and len(pieces) == 1 and self.piece_hook is None
+                  and not self.piece_chunks)
+        # serial mode: the first forward starts after the first eighth of the ids
+        serial_split = min(K, (K // 8 + 127) // 128 * 128) if (serial and host_src is not None) \
+            else K
         all_ids = torch.cuda.Event()
         if host_src is not None:
-            first = min(n, pieces[0][1] * self.l_in) if K else n
+            first = (min(n, serial_split * self.l_in) if serial else
+                     min(n, pieces[0][1] * self.l_in) if K else n)
             self.s_copy.wait_stream(main)       # earlier readers of self.gids
             first_ids = torch.cuda.Event()
             with torch.cuda.stream(self.s_copy):
@@ -193,13 +224,17 @@ class HotPath:
             all_ids.record(main)
         self._cov_events = []
         # K4: the LRU comparator depends only on the ids
-        if self.lru is not None:
-            self.s_lru.wait_event(all_ids)
+        def run_lru(after):
+            self.s_lru.wait_event(after)
             with torch.cuda.stream(self.s_lru):
                 self._ev("lru", self.s_lru)
                 self.lru.reset()
                 self.lru.run(g)
                 self._ev("lru", self.s_lru)
+
+        lru_late = _LRU_LATE and self.lru is not None
+        if self.lru is not None and not lru_late:
+            run_lru(all_ids)
         prev = L.recmg_set_model_sm_budget(self.model_sms)
         try:
             self.s_replay.wait_event(all_ids)
@@ -211,10 +246,22 @@ class HotPath:
             # table ids in (at most) two launches: the first piece's as soon as
             # its ids are in, the rest once all ids are
             split = pieces[0][1] if host_src is not None else K
+            if serial:
+                split = serial_split
             if models:
                 self._ev("table_ids", main)
                 gk, tk = self._ids_of(g, 0, split)
                 self._ev("table_ids", main)
+            if serial:
+                self._launch_serial(g, K, host_src, all_ids, main, bits, pf, split)
+                pieces = []
+            streamed = (_STREAMED and models and len(pieces) > 1 and self.piece_hook is None
+                        and not self.piece_chunks and all(
+                            m is None or m.prec in (_native.PREC_TC32, _native.PREC_TC16)
+                            for m in (self.caching, self.prefetch)))
+            if streamed:
+                self._launch_streamed(g, K, pieces, host_src, all_ids, main, bits, pf, split)
+                pieces = []
             for i, (k0, k1) in enumerate(pieces):
                 if i == 1 and host_src is not None:
                     main.wait_event(all_ids)
@@ -263,6 +310,10 @@ class HotPath:
                         self._cov_events.append((k0, k1, e))
         finally:
             L.recmg_set_model_sm_budget(prev)
+        if lru_late:   # after the forwards: beside the replay's single-warp chain
+            fwd_done = torch.cuda.Event()
+            fwd_done.record(main)
+            run_lru(fwd_done)
         self._ev("tail", main)          # forwards done ...
         main.wait_stream(self.s_replay)
         if self.lru is not None:
@@ -270,6 +321,133 @@ class HotPath:
         self._ev("tail", main)          # ... -> last replay piece and LRU done
         self.K = K
         self.n = n
+
+    def _launch_serial(self, g, K, host_src, all_ids, main, bits, pf, split):
+        """One replay after both forwards (pieces == 1; measured the fastest
+        schedule: a replay beside the forwards takes the SMs they need, the
+        replay and forwards are both throughput-bound).  The prefetch forward
+        runs first (in two launches on the end-to-end path: the first eighth
+        starts once its ids are in); its prefetch statistics and coverage counts
+        need only the decoded ids, so they run right after it on the replay
+        stream and are copied back while the caching forward runs."""
+        torch = self.torch
+        gk = (self.lgid if self.shard is not None else self.gids)[
+            :K * self.l_in].view(K, self.l_in)
+        tk = self.tid[:K * self.l_in].view(K, self.l_in)
+
+        def fwd(model, k0, k1):
+            if model is None or k1 <= k0:
+                return
+            if model is self.caching:
+                self._ev("caching_fwd", main)
+                model.forward(gk[k0:k1], tk[k0:k1], logits=self.clog[k0:k1],
+                              bits=self.bits[k0:k1])
+                self._ev("caching_fwd", main)
+            else:
+                self._ev("prefetch_fwd", main)
+                model.forward(gk[k0:k1], tk[k0:k1], logits=self.plog[k0:k1],
+                              pf_gid=self.pf[k0:k1])
+                self._ev("prefetch_fwd", main)
+
+        first, second = ((self.prefetch, self.caching) if self.prefetch is not None
+                         else (self.caching, None))
+        fwd(first, 0, split)
+        if split < K:
+            main.wait_event(all_ids)
+            self._ev("table_ids", main)
+            self._ids_of(g, split, K)
+            self._ev("table_ids", main)
+            fwd(first, split, K)
+        early_stats = self.prefetch is not None
+        if early_stats:
+            pf_done = torch.cuda.Event()
+            pf_done.record(main)
+            self.s_replay.wait_event(pf_done)
+            with torch.cuda.stream(self.s_replay):
+                self.buffer.stats_chunks(g, 0, K, pf)
+                if host_src is not None:
+                    for r in range(2):
+                        self.cov_host[r, :K].copy_(self.buffer._cov[r, :K], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(self.s_replay)
+                    self._cov_events.append((0, K, e))
+        fwd(second, 0, K)
+        scored = torch.cuda.Event()
+        scored.record(main)
+        self.s_replay.wait_event(scored)
+        with torch.cuda.stream(self.s_replay):
+            self._ev("replay", self.s_replay)
+            self.buffer.run_chunks(g, 0, K, True, bits, pf, skip_stats=early_stats)
+            self._ev("replay", self.s_replay)
+            if host_src is not None and not early_stats:
+                for r in range(2):
+                    self.cov_host[r, :K].copy_(self.buffer._cov[r, :K], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(self.s_replay)
+                self._cov_events.append((0, K, e))
+
+    def _launch_streamed(self, g, K, pieces, host_src, all_ids, main, bits, pf, split):
+        """The streamed pipeline (see _STREAMED): the first model's forward
+        over all chunks (two launches on the end-to-end path, so it starts
+        after the first piece's ids), then the second model's with progress
+        signals; the replay stream runs piece i once its tiles are done."""
+        torch = self.torch
+        L = _native.lib()
+        gk = (self.lgid if self.shard is not None else self.gids)[
+            :K * self.l_in].view(K, self.l_in)
+        tk = self.tid[:K * self.l_in].view(K, self.l_in)
+        step = pieces[0][1] - pieces[0][0]
+        progress = torch.zeros(len(pieces), dtype=torch.int32, device="cuda")   # on main
+        zeroed = torch.cuda.Event()
+        zeroed.record(main)
+        self.s_replay.wait_event(zeroed)   # the waits below must see this launch's zeros
+
+        def fwd(model, key, k0, k1, signal):
+            self._ev(key, main)
+            kw = {"progress": progress, "piece_chunks": step} if signal else {}
+            if model is self.caching:
+                model.forward(gk[k0:k1], tk[k0:k1], logits=self.clog[k0:k1],
+                              bits=self.bits[k0:k1], **kw)
+            else:
+                model.forward(gk[k0:k1], tk[k0:k1], logits=self.plog[k0:k1],
+                              pf_gid=self.pf[k0:k1], **kw)
+            self._ev(key, main)
+
+        order = [(self.prefetch, "prefetch_fwd"), (self.caching, "caching_fwd")]
+        if not _PF_FIRST:
+            order.reverse()
+        order = [(m, k) for m, k in order if m is not None]
+        (m0, k0name), (m1, k1name) = (order[0], order[-1]) if len(order) > 1 else (
+            (None, None), order[0])
+        if m0 is not None:
+            if host_src is not None and split < K:
+                fwd(m0, k0name, 0, split, False)
+                main.wait_event(all_ids)
+                self._ev("table_ids", main)
+                self._ids_of(g, split, K)
+                self._ev("table_ids", main)
+                fwd(m0, k0name, split, K, False)
+            else:
+                fwd(m0, k0name, 0, K, False)
+        if host_src is not None and m0 is None and split < K:
+            main.wait_event(all_ids)
+            self._ids_of(g, split, K)
+        fwd(m1, k1name, 0, K, True)
+        for i, (a, b) in enumerate(pieces):
+            with torch.cuda.stream(self.s_replay):
+                _native.check(L.recmg_wait_progress(
+                    _native.ptr(progress), i, (b - a + 127) // 128,
+                    _native.stream_handle(torch)), "wait_progress")
+                self._ev("replay", self.s_replay)
+                self.buffer.run_chunks(g, a, b, i == len(pieces) - 1, bits, pf)
+                self._ev("replay", self.s_replay)
+                if host_src is not None and b > a:
+                    for r in range(2):
+                        self.cov_host[r, a:b].copy_(self.buffer._cov[r, a:b], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(self.s_replay)
+                    self._cov_events.append((a, b, e))
+        self._progress = progress   # keep the counters alive until the stream is done
 
     def report(self):
         """Synchronise and return (BreakdownReport, lru (hits, misses) or None).
