@@ -385,7 +385,10 @@ __device__ __forceinline__ void flush_counters(recmg_counters *ctr, unsigned lon
 // round trip per 32-event batch (the replay of the hottest set is a single
 // dependency chain).
 constexpr int kRingBlk = 256;
-constexpr int kRingSlots = 8;                      // power of two
+#ifndef RECMG_RING_SLOTS
+#define RECMG_RING_SLOTS 4
+#endif
+constexpr int kRingSlots = RECMG_RING_SLOTS;       // power of two
 constexpr int kRingMask = kRingBlk * kRingSlots - 1;
 constexpr int kL2Ahead = 32;   // blocks prefetched into L2 beyond the ring (long segments)
 
@@ -521,8 +524,11 @@ __device__ __forceinline__ void ht_erase(const SetView &v, uint32_t g) {
     v.ht[i] = kHtEmpty;
 }
 
+#ifndef RECMG_REPLAY_MINB
+#define RECMG_REPLAY_MINB 24
+#endif
 template <int POLICY, bool CLASS>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32, RECMG_REPLAY_MINB)
 replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes_per_warp) {
     extern __shared__ __align__(16) uint8_t dsm[];
     const unsigned FULL = 0xFFFFFFFFu;
@@ -532,6 +538,9 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
         // CTAs [0, kHeavySets) replay the listed heavy sets, the rest every
         // other set in order (one warp per CTA when heavy sets are listed)
         const int nh = min(__ldg(a.heavy), kHeavySets);
+#if defined(RECMG_DIAG_SETS)   // diagnostic builds: 1 = heavy sets only, 2 = the others only
+        if ((RECMG_DIAG_SETS == 1) != (blockIdx.x < kHeavySets)) return;
+#endif
         if (blockIdx.x < kHeavySets) {
             if ((int)blockIdx.x >= nh) return;
             set = __ldg(a.heavy + 1 + blockIdx.x);

@@ -42,9 +42,9 @@ _PF_FIRST = os.environ.get("RECMG_PF_FIRST", "1") == "1"
 # launch pairs: +36% prefetch / +4% caching forward time).  RECMG_STREAMED=0
 # restores per-piece forward launches.
 _STREAMED = os.environ.get("RECMG_STREAMED", "0") == "1"
-# The LRU comparator launched after the forwards (it then shares the GPU with
-# the replay, whose tail is one set's serial chain) instead of at the start
-# (where its kernels take SMs at every forward launch boundary).
+# In the serial schedule the LRU comparator is launched after the forwards (it
+# then shares the GPU with the replay) instead of at the start, where its
+# kernels take SMs at the forward launch boundary (config 2: +1.8%).
 _LRU_LATE = os.environ.get("RECMG_LRU_LATE", "1") == "1"
 
 
@@ -232,7 +232,9 @@ class HotPath:
                 self.lru.run(g)
                 self._ev("lru", self.s_lru)
 
-        lru_late = _LRU_LATE and self.lru is not None
+        # late only in the serial schedule: pipelined runs (few-set buffers, config
+        # 3's one-hot-set shards) have chain-bound LRUs that must hide under the forwards
+        lru_late = _LRU_LATE and self.lru is not None and serial
         if self.lru is not None and not lru_late:
             run_lru(all_ids)
         prev = L.recmg_set_model_sm_budget(self.model_sms)
