@@ -18,6 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CUDA = "/usr/local/cuda/bin"
 rep, fn = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+unit = sys.argv[4] if len(sys.argv) > 4 else "lstm_tc"   # the .cu whose cubin holds fn
 
 csv_text = subprocess.run([f"{CUDA}/ncu", "-i", rep, "--page", "source", "--csv",
                            "--print-source", "sass"], capture_output=True, text=True).stdout
@@ -31,7 +32,7 @@ with tempfile.TemporaryDirectory() as d:
     subprocess.run([f"{CUDA}/cuobjdump", "-xelf", "all",
                     os.path.join(ROOT, "paper_2511_08568_b200", "librecmg.so")],
                    cwd=d, capture_output=True)
-    cubin = os.path.join(d, "lstm_tc.sm_100a.cubin")
+    cubin = os.path.join(d, f"{unit}.sm_100a.cubin")
     sass = subprocess.run([f"{CUDA}/nvdisasm", "-g", "-c", cubin], capture_output=True,
                           text=True).stdout.split("\n")
 start = next(i for i, l in enumerate(sass) if l.startswith(".text.") and fn in l)
@@ -64,7 +65,7 @@ for r in data:
         reasons[loc][h] += float(r[idx[h]] or 0)
 
 src = {}
-for f in ("lstm_tc.cu", "umma.cuh"):
+for f in ("lstm_tc.cu", "umma.cuh", "replay.cu", "partition.cu", "capi.cu"):
     src[f] = open(os.path.join(ROOT, "paper_2511_08568_b200", "csrc", f)).read().split("\n")
 print(f"{os.path.basename(rep)} {fn}: {int(total)} warp-stall samples")
 for loc, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:

@@ -64,3 +64,33 @@ def test_replay_host_edge_sizes_and_reuse():
         assert rep.total == n and h + m == n, n
         assert m == rb.simulate(sub, rb.CacheConfig(C32, rb.Policy.LRU, 32),
                                 per_access=False).misses, n
+
+
+@pytest.mark.parametrize("pf_first", [True, False])
+def test_streamed_schedule_matches_oracle(monkeypatch, pf_first):
+    """The streamed schedule (one forward launch per model, the second one
+    releasing per-piece progress counters that the replay stream waits on:
+    recmg_model_forward_signal / recmg_wait_progress) gives the oracle's counts."""
+    import torch
+    from paper_2511_08568_b200 import pipeline
+    monkeypatch.setattr(pipeline, "_STREAMED", True)
+    monkeypatch.setattr(pipeline, "_PF_FIRST", pf_first)
+    t = rb.generate_trace(rb.TraceGenConfig([3000] * 16, 200_000, 1.05, 0.4, 32, 17))
+    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=0.4)
+    n = len(t)
+    C = int(0.2 * t.unique_count)
+    C32 = C - C % 32
+    hp = HotPath(cp, pp, t.table_sizes, C32, n, ways=32, pieces=8)
+    host = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
+    for _ in range(2):   # the second pass reuses the progress counters' memory
+        rep, _ = hp.replay_host(host)
+    K = hp.K
+    bits = hp.bits[:K].cpu().numpy()
+    pf = hp.pf[:K].cpu().numpy()
+    ref, cov = oracle.replay(t.gid_array, t.total_ids, C32, 32, 4, bits=bits, pf=pf)
+    assert [rep.cache_hits, rep.prefetch_hits, rep.on_demand, rep.prefetch_issued,
+            rep.prefetch_useful, rep.evictions, rep.prefetch_inserts] == \
+        [ref[k] for k in ("cache_hits", "prefetch_hits", "on_demand", "prefetch_issued",
+                          "prefetch_useful", "evictions", "prefetch_inserts")]
+    assert rep.coverage == cov
