@@ -608,9 +608,9 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
 
     // Apply the hit-run part held by one 32-event half (events base+lane,
     // lane < n_run): group by way, the group leader updates its way.
-    auto apply_run = [&](int64_t base, uint32_t e, int way, int n_run) {
+    auto apply_run = [&](int64_t base, uint32_t e, int way, int r0, int n_run) {
         const uint32_t ty = ev_type(e);
-        const bool inrun = way >= 0 && lane < n_run;
+        const bool inrun = way >= 0 && lane >= r0 && lane < n_run;
         const unsigned peers = __match_any_sync(FULL, inrun ? (unsigned)way : (0x80000000u | lane));
         const int leader = 31 - __clz(peers);
         if (PRIO) {
@@ -787,7 +787,13 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             try_fast = false;
         }
         // 64 events per step (two per lane): membership of both halves against
-        // the same tag set, one cut, the run applied half by half
+        // the same tag set, cut at the first residency-changing miss, the run
+        // before it applied half by half, the miss resolved -- and then the
+        // rest of the SAME window continues from the miss: a miss changes the
+        // membership of at most two gids (the inserted one, now at `target`,
+        // and the evicted one), so the window's ways are patched instead of
+        // re-read and re-probed (miss-dense sets resolved several misses per
+        // 64 probes instead of one)
         const int nb = (int)imin64(64, hi - pos);
         ring.ensure(pos - lo, nb);
         const bool v0 = lane < nb, v1 = lane + 32 < nb;
@@ -799,136 +805,150 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             real0 = real0 && (ev_type(e0) == EV_SERVE || ev_type(e0) == EV_PREFETCH);
             real1 = real1 && (ev_type(e1) == EV_SERVE || ev_type(e1) == EV_PREFETCH);
         }
-        const int way0 = real0 ? ht_find(v, g0) : -1;
-        const int way1 = real1 ? ht_find(v, g1) : -1;
-        unsigned miss0, miss1;
+        int way0 = real0 ? ht_find(v, g0) : -1;
+        int way1 = real1 ? ht_find(v, g1) : -1;
+        bool cand0, cand1;   // events that miss when not resident
         if (PRIO || LRUPF) {
             const uint32_t t0 = ev_type(e0), t1 = ev_type(e1);
-            miss0 = __ballot_sync(FULL, real0 && way0 < 0 && (t0 == EV_SERVE || t0 == EV_PREFETCH));
-            miss1 = __ballot_sync(FULL, real1 && way1 < 0 && (t1 == EV_SERVE || t1 == EV_PREFETCH));
+            cand0 = real0 && (t0 == EV_SERVE || t0 == EV_PREFETCH);
+            cand1 = real1 && (t1 == EV_SERVE || t1 == EV_PREFETCH);
         } else {
-            miss0 = __ballot_sync(FULL, real0 && way0 < 0);
-            miss1 = __ballot_sync(FULL, real1 && way1 < 0);
+            cand0 = real0;
+            cand1 = real1;
         }
-        const int cut = miss0 ? (__ffs(miss0) - 1) : (miss1 ? 32 + __ffs(miss1) - 1 : nb);
-        {
-            // a whole 64-window of hits on one gid: the next window may be a long run
-            const uint32_t gref = __shfl_sync(FULL, g0, 0);
-            const bool same = (!real0 || g0 == gref) && (!real1 || g1 == gref);
-            try_fast = cut == nb && nb == 64 && __all_sync(FULL, same);
+        int start = 0;
+        for (;;) {
+            const unsigned miss0 = __ballot_sync(FULL, cand0 && way0 < 0 && lane >= start);
+            const unsigned miss1 = __ballot_sync(FULL, cand1 && way1 < 0 && lane + 32 >= start);
+            const int cut = miss0 ? (__ffs(miss0) - 1) : (miss1 ? 32 + __ffs(miss1) - 1 : nb);
+            if (start == 0) {
+                // a whole 64-window of hits on one gid: the next window may be a long run
+                const uint32_t gref = __shfl_sync(FULL, g0, 0);
+                const bool same = (!real0 || g0 == gref) && (!real1 || g1 == gref);
+                try_fast = cut == nb && nb == 64 && __all_sync(FULL, same);
 #ifdef RECMG_NO_FASTRUN
-            try_fast = false;
+                try_fast = false;
 #endif
-        }
-        apply_run(pos, e0, way0, cut < 32 ? cut : 32);
-        if (cut > 32) apply_run(pos + 32, e1, way1, cut - 32);
-        const uint32_t e = cut < 32 ? e0 : e1;
-
-        if (cut < nb) {
-            const uint32_t ec = __shfl_sync(FULL, e, cut & 31);
-            const uint32_t gc = ev_gid(ec);
-            const uint32_t tc = ev_type(ec);
-            if (PRIO || LRUPF) {
-                if (tc == EV_SERVE) {
-                    od++;
-                    if (CLASS && lane == 0) write_class(a, pos + cut, 2);
-                } else {
-                    ins++;
-                }
-            } else {
-                od++;
-                if (a.per_access_hit && lane == 0)
-                    a.per_access_hit[a.vals ? a.vals[pos + cut] : pos + cut] = 0;
             }
-            int target;
-            if (count >= W) {
-                // populate(): victim = argmin (priority, gid) [LRU: min clock]
-                unsigned long long best = ~0ull;
-                int bslot = -1;
-                for (int w = lane; w < W; w += 32) {
-                    const int32_t t = v.tags[w];
-                    if (t < 0) continue;
-                    const int64_t m = v.meta[w];
-                    unsigned long long key;
-                    if (PRIO) key = ((unsigned long long)(uint32_t)m << 32) | (uint32_t)t;
-                    else if (OPT) key = ((unsigned long long)((int64_t(1) << 31) - m) << 32) | (uint32_t)t;
-                    else if (SRRIP) key = (unsigned long long)w;   // chosen below
-                    else if (LFU) key = (unsigned long long)m;
-                    else key = (unsigned long long)(m & kClockMask);
-                    if (key < best) { best = key; bslot = w; }
-                }
-                if (SRRIP) {
-                    // age until some way reaches max (cache_sim.py:158-165), then
-                    // take the first such way in slot order
-                    int64_t mx = 0;
-                    for (int w = lane; w < W; w += 32)
-                        if (v.tags[w] >= 0) mx = v.meta[w] > mx ? v.meta[w] : mx;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const int64_t om = __shfl_xor_sync(FULL, mx, o);
-                        mx = om > mx ? om : mx;
+            if (start < 32) apply_run(pos, e0, way0, start, cut < 32 ? cut : 32);
+            if (cut > 32) apply_run(pos + 32, e1, way1, start > 32 ? start - 32 : 0, cut - 32);
+            if (cut >= nb) break;
+            const uint32_t e = cut < 32 ? e0 : e1;
+            int32_t evicted = -1;
+                const uint32_t ec = __shfl_sync(FULL, e, cut & 31);
+                const uint32_t gc = ev_gid(ec);
+                const uint32_t tc = ev_type(ec);
+                if (PRIO || LRUPF) {
+                    if (tc == EV_SERVE) {
+                        od++;
+                        if (CLASS && lane == 0) write_class(a, pos + cut, 2);
+                    } else {
+                        ins++;
                     }
-                    const int64_t dlt = (int64_t)a.es - mx;
-                    best = ~0ull;
-                    bslot = -1;
-                    for (int w = lane; w < W; w += 32) {
-                        if (v.tags[w] < 0) continue;
-                        const int64_t r = v.meta[w] + (dlt > 0 ? dlt : 0);
-                        if (dlt > 0) v.meta[w] = r;
-                        if (r >= a.es && (unsigned long long)w < best) { best = (unsigned long long)w; bslot = w; }
-                    }
+                } else {
+                    od++;
+                    if (a.per_access_hit && lane == 0)
+                        a.per_access_hit[a.vals ? a.vals[pos + cut] : pos + cut] = 0;
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
-                    const int os = __shfl_xor_sync(FULL, bslot, o);
-                    if (ob < best) { best = ob; bslot = os; }
-                }
-                if (PRIO) {
+                int target;
+                if (count >= W) {
+                    // populate(): victim = argmin (priority, gid) [LRU: min clock]
+                    unsigned long long best = ~0ull;
+                    int bslot = -1;
                     for (int w = lane; w < W; w += 32) {
-                        if (v.tags[w] < 0) continue;
+                        const int32_t t = v.tags[w];
+                        if (t < 0) continue;
                         const int64_t m = v.meta[w];
-                        if ((int32_t)(m & 0xFFFFFFFF) > 0) v.meta[w] = m - 1;
+                        unsigned long long key;
+                        if (PRIO) key = ((unsigned long long)(uint32_t)m << 32) | (uint32_t)t;
+                        else if (OPT) key = ((unsigned long long)((int64_t(1) << 31) - m) << 32) | (uint32_t)t;
+                        else if (SRRIP) key = (unsigned long long)w;   // chosen below
+                        else if (LFU) key = (unsigned long long)m;
+                        else key = (unsigned long long)(m & kClockMask);
+                        if (key < best) { best = key; bslot = w; }
                     }
+                    if (SRRIP) {
+                        // age until some way reaches max (cache_sim.py:158-165), then
+                        // take the first such way in slot order
+                        int64_t mx = 0;
+                        for (int w = lane; w < W; w += 32)
+                            if (v.tags[w] >= 0) mx = v.meta[w] > mx ? v.meta[w] : mx;
+    #pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const int64_t om = __shfl_xor_sync(FULL, mx, o);
+                            mx = om > mx ? om : mx;
+                        }
+                        const int64_t dlt = (int64_t)a.es - mx;
+                        best = ~0ull;
+                        bslot = -1;
+                        for (int w = lane; w < W; w += 32) {
+                            if (v.tags[w] < 0) continue;
+                            const int64_t r = v.meta[w] + (dlt > 0 ? dlt : 0);
+                            if (dlt > 0) v.meta[w] = r;
+                            if (r >= a.es && (unsigned long long)w < best) { best = (unsigned long long)w; bslot = w; }
+                        }
+                    }
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+                        const int os = __shfl_xor_sync(FULL, bslot, o);
+                        if (ob < best) { best = ob; bslot = os; }
+                    }
+                    if (PRIO) {
+                        for (int w = lane; w < W; w += 32) {
+                            if (v.tags[w] < 0) continue;
+                            const int64_t m = v.meta[w];
+                            if ((int32_t)(m & 0xFFFFFFFF) > 0) v.meta[w] = m - 1;
+                        }
+                    }
+                    __syncwarp();
+                    evicted = v.tags[bslot];
+                    __syncwarp();
+                    if (lane == 0) {
+                        ht_erase(v, (uint32_t)evicted);
+                        v.tags[bslot] = -1;
+                    }
+                    count--;
+                    nev++;
+                    target = bslot;
+                } else {
+                    // first free way at or after the hint (ways below it are occupied:
+                    // inside a launch a way is only freed by an eviction, refilled at once)
+                    int found = -1;
+                    for (int64_t b = free_hint; b < Wp && found < 0; b += 32) {
+                        const int w = (int)b + lane;
+                        const unsigned fm = __ballot_sync(FULL, w < W && v.tags[w] == -1);
+                        if (fm) found = (int)b + __ffs(fm) - 1;
+                    }
+                    target = found;
+                    free_hint = found + 1;
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    ht_erase(v, (uint32_t)v.tags[bslot]);
-                    v.tags[bslot] = -1;
+                    v.tags[target] = (int32_t)gc;
+                    int64_t m;
+                    if (PRIO) m = (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
+                    else if (LFU) m = lfu_meta(0, 1, clock_base + pos + cut);
+                    else if (SRRIP) m = a.es > 1 ? a.es - 1 : 0;
+                    else if (OPT) m = a.next_use[a.vals ? a.vals[pos + cut] : pos + cut];
+                    else m = (clock_base + pos + cut) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0);
+                    v.meta[target] = m;
+                    ht_insert(v, gc, (uint32_t)target);
                 }
-                count--;
-                nev++;
-                target = bslot;
-            } else {
-                // first free way at or after the hint (ways below it are occupied:
-                // inside a launch a way is only freed by an eviction, refilled at once)
-                int found = -1;
-                for (int64_t b = free_hint; b < Wp && found < 0; b += 32) {
-                    const int w = (int)b + lane;
-                    const unsigned fm = __ballot_sync(FULL, w < W && v.tags[w] == -1);
-                    if (fm) found = (int)b + __ffs(fm) - 1;
-                }
-                target = found;
-                free_hint = found + 1;
+                count++;
+                __syncwarp();
+            // patch the window's membership: the inserted gid now lives at
+            // `target`, the evicted one nowhere
+            if (evicted >= 0) {
+                if (g0 == (uint32_t)evicted) way0 = -1;
+                if (g1 == (uint32_t)evicted) way1 = -1;
             }
-            __syncwarp();
-            if (lane == 0) {
-                v.tags[target] = (int32_t)gc;
-                int64_t m;
-                if (PRIO) m = (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
-                else if (LFU) m = lfu_meta(0, 1, clock_base + pos + cut);
-                else if (SRRIP) m = a.es > 1 ? a.es - 1 : 0;
-                else if (OPT) m = a.next_use[a.vals ? a.vals[pos + cut] : pos + cut];
-                else m = (clock_base + pos + cut) | (LRUPF ? ((int64_t)(tc == EV_PREFETCH) << 62) : 0);
-                v.meta[target] = m;
-                ht_insert(v, gc, (uint32_t)target);
-            }
-            count++;
-            __syncwarp();
-            pos += cut + 1;
-        } else {
-            pos += nb;
+            if (real0 && g0 == gc) way0 = target;
+            if (real1 && g1 == gc) way1 = target;
+            start = cut + 1;
+            if (start >= nb) break;
         }
+        pos += nb;
     }
 
     // write back the set
