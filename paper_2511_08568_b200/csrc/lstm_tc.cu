@@ -1206,22 +1206,19 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             const int64_t dec_a = tl.phase_off[1];
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);
-                // GEMM1: Q = h1 att_dec ; Z[0:64) = h1 Wcomb_h + ctx Wcomb_c
+                // GEMM1: [comb | Q] = h1 [Wcomb_h | att_dec] into Z[0:128) (one
+                // N = 128 product over the stacked image), then comb += ctx Wcomb_c
                 pc.mark(3);
                 if (t >= 1) wait_mma(&tma_bar2, tphase2);   // att_dec | Wcomb back in the region
                 tmem_writes_done();
                 pc.mark(4);
                 if (c.tid == 0) {
                     umma::fence_after();
-                    if (!last)
-                        mma3<SINGLE>(c.tbase + COL_Q, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase, 64, false);                          // att_dec
-                    if (t >= 1) {
-                        mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
-                             sbase + tl.img64, 64, false);               // Wcomb_h
+                    mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_H1_HI, c.tbase + P_H1_LO,
+                         sbase, 128, false);                             // Wcomb_h | att_dec
+                    if (t >= 1)
                         mma3<SINGLE>(c.tbase + COL_Z, c.tbase + P_CTX_HI, c.tbase + P_CTX_LO,
                              sbase + 2 * tl.img64, 64, true);            // Wcomb_c
-                    }
                     umma::commit(&mbar);
                 }
                 wait_mma(&mbar, phase);
@@ -1233,7 +1230,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 pc.mark(5);
                 if (t >= 1) lpart[c.part][c.row] = head_partial(c, COL_Z, comb_b, head_w);
                 if (!last) {
-                    attn_scores(c, Es, L, COL_Q, att_v, vsum, rawmask, s_part, L);  // non-causal
+                    attn_scores(c, Es, L, COL_Z + 64, att_v, vsum, rawmask, s_part, L);  // non-causal
                 }
                 __syncthreads();
                 if (t >= 1 && c.part == 0) {
@@ -1542,8 +1539,12 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
         spec(0, 1, r.enc_wx[1], 4 * d, 256, 1);
         spec(0, 2, r.enc_wh[1], 4 * d, 256, 1);
         spec(0, 3, r.att_enc, d, 64, 0);
+        // Wcomb_h (h part) | att_dec stacked as one N = 128 image at b_off[4]
+        spec(1, 4, r.comb_w, d, 64, 2);
+        specs.back().img_n = 128;
         spec(1, 4, r.att_dec, d, 64, 0);
-        spec(1, 5, r.comb_w, d, 64, 2);
+        specs.back().row0 = 64;
+        specs.back().img_n = 128;
         spec(1, 6, r.comb_w + d * d, d, 64, 2);
         spec(1, 7, r.dec_wx[0] + 2 * d * 4 * d, 4 * d, 256, 1);
         spec(1, 8, r.dec_wh[0], 4 * d, 256, 1);
