@@ -589,6 +589,12 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
     const int64_t clock_base = a.st.header[0];
     unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
     const unsigned lt = (1u << lane) - 1u;
+    // PRIORITY: populate()'s decay (every positive priority -1 on each
+    // eviction, runtime.py:100-112) is applied lazily -- priorities are stored
+    // as p + decay (decay = evictions so far in this launch) and read as
+    // max(0, stored - decay), which orders the ways exactly as the eager
+    // decrement does, so an eviction costs no pass over the set's ways
+    int32_t decay = 0;
     int64_t free_hint = 0;
     // LRU_PF (replay_policy_only with a prefetcher, runtime.py:318-339):
     // meta = clock | prefetch tag << 62; keep-bit updates do not exist there
@@ -631,7 +637,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 }
                 if (up) {
                     const int last = 31 - __clz(up);
-                    pr = a.es + (((U1mask >> last) & 1u) ? 1 : 0);
+                    pr = a.es + (((U1mask >> last) & 1u) ? 1 : 0) + decay;
                 }
                 if (sp || up) v.meta[way] = (int64_t)(uint32_t)pr | ((int64_t)f << 32);
             }
@@ -741,7 +747,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                             if (f) { ph += 1; ch += nS - 1; f = false; }
                             else ch += nS;
                         }
-                        if (lU >= 0) pr = a.es + (lUty == EV_UPD1 ? 1 : 0);
+                        if (lU >= 0) pr = a.es + (lUty == EV_UPD1 ? 1 : 0) + decay;
                         if (nS || lU >= 0) v.meta[way] = (int64_t)(uint32_t)pr | ((int64_t)f << 32);
                     }
                     if (CLASS) {
@@ -860,7 +866,10 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                         if (t < 0) continue;
                         const int64_t m = v.meta[w];
                         unsigned long long key;
-                        if (PRIO) key = ((unsigned long long)(uint32_t)m << 32) | (uint32_t)t;
+                        if (PRIO) {
+                            const int32_t pe = (int32_t)(m & 0xFFFFFFFF) - decay;
+                            key = ((unsigned long long)(uint32_t)(pe > 0 ? pe : 0) << 32) | (uint32_t)t;
+                        }
                         else if (OPT) key = ((unsigned long long)((int64_t(1) << 31) - m) << 32) | (uint32_t)t;
                         else if (SRRIP) key = (unsigned long long)w;   // chosen below
                         else if (LFU) key = (unsigned long long)m;
@@ -894,13 +903,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                         const int os = __shfl_xor_sync(FULL, bslot, o);
                         if (ob < best) { best = ob; bslot = os; }
                     }
-                    if (PRIO) {
-                        for (int w = lane; w < W; w += 32) {
-                            if (v.tags[w] < 0) continue;
-                            const int64_t m = v.meta[w];
-                            if ((int32_t)(m & 0xFFFFFFFF) > 0) v.meta[w] = m - 1;
-                        }
-                    }
+                    if (PRIO) decay++;   // the lazy decay (see `decay`)
                     __syncwarp();
                     evicted = v.tags[bslot];
                     __syncwarp();
@@ -927,7 +930,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                 if (lane == 0) {
                     v.tags[target] = (int32_t)gc;
                     int64_t m;
-                    if (PRIO) m = (int64_t)(uint32_t)a.es | ((int64_t)(tc == EV_PREFETCH) << 32);
+                    if (PRIO) m = (int64_t)(uint32_t)(a.es + decay) | ((int64_t)(tc == EV_PREFETCH) << 32);
                     else if (LFU) m = lfu_meta(0, 1, clock_base + pos + cut);
                     else if (SRRIP) m = a.es > 1 ? a.es - 1 : 0;
                     else if (OPT) m = a.next_use[a.vals ? a.vals[pos + cut] : pos + cut];
@@ -951,10 +954,15 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
         pos += nb;
     }
 
-    // write back the set
+    // write back the set (PRIORITY: the effective priorities, decay applied)
     for (int w = lane; w < W; w += 32) {
         a.st.tags[sbase + w] = v.tags[w];
-        a.st.meta[sbase + w] = v.meta[w];
+        int64_t m = v.meta[w];
+        if (PRIO) {
+            const int32_t pe = (int32_t)(m & 0xFFFFFFFF) - decay;
+            m = (m & ~int64_t(0xFFFFFFFF)) | (int64_t)(uint32_t)(pe > 0 ? pe : 0);
+        }
+        a.st.meta[sbase + w] = m;
     }
     if (lane == 0) a.st.count[set] = count;
     if (PRIO || LRUPF) {

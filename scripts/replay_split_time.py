@@ -26,7 +26,7 @@ K = hp.K
 g, bits, pf = hp.gids[:n], hp.bits[:K], hp.pf[:K]
 buf = hp.buffer
 ms = []
-for _ in range(4):
+for _ in range(9):
     buf.reset()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
