@@ -898,10 +898,16 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                         }
                     }
     #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
-                        const int os = __shfl_xor_sync(FULL, bslot, o);
-                        if (ob < best) { best = ob; bslot = os; }
+                    {
+                        // warp min of the 64-bit keys (unique per way) with two
+                        // REDUX.MIN: the high words, then the low words of the
+                        // lanes holding the high minimum; the winner's slot
+                        const unsigned hi = (unsigned)(best >> 32);
+                        const unsigned hmin = __reduce_min_sync(FULL, hi);
+                        const unsigned lmin = __reduce_min_sync(FULL, hi == hmin ? (unsigned)best
+                                                                                 : 0xFFFFFFFFu);
+                        const unsigned win = __ballot_sync(FULL, hi == hmin && (unsigned)best == lmin);
+                        bslot = __shfl_sync(FULL, bslot, __ffs(win) - 1);
                     }
                     if (PRIO) decay++;   // the lazy decay (see `decay`)
                     __syncwarp();
