@@ -42,6 +42,8 @@ _PF_FIRST = os.environ.get("RECMG_PF_FIRST", "1") == "1"
 # launch pairs: +36% prefetch / +4% caching forward time).  RECMG_STREAMED=0
 # restores per-piece forward launches.
 _STREAMED = os.environ.get("RECMG_STREAMED", "0") == "1"
+# replay_host() through a CUDA graph of the step's launches (see there)
+_GRAPHS = os.environ.get("RECMG_GRAPHS", "1") == "1"
 # In the serial schedule the LRU comparator is launched after the forwards (it
 # then shares the GPU with the replay) instead of at the start, where its
 # kernels take SMs at the forward launch boundary (config 2: +1.8%).
@@ -307,7 +309,7 @@ class HotPath:
                         for r in range(2):   # contiguous rows: plain async D2H copies
                             self.cov_host[r, k0:k1].copy_(self.buffer._cov[r, k0:k1],
                                                           non_blocking=True)
-                        e = torch.cuda.Event()
+                        e = torch.cuda.Event(external=True)   # an event node in a graph
                         e.record(self.s_replay)
                         self._cov_events.append((k0, k1, e))
         finally:
@@ -370,7 +372,7 @@ class HotPath:
                 if host_src is not None:
                     for r in range(2):
                         self.cov_host[r, :K].copy_(self.buffer._cov[r, :K], non_blocking=True)
-                    e = torch.cuda.Event()
+                    e = torch.cuda.Event(external=True)   # an event node in a graph
                     e.record(self.s_replay)
                     self._cov_events.append((0, K, e))
         fwd(second, 0, K)
@@ -384,7 +386,7 @@ class HotPath:
             if host_src is not None and not early_stats:
                 for r in range(2):
                     self.cov_host[r, :K].copy_(self.buffer._cov[r, :K], non_blocking=True)
-                e = torch.cuda.Event()
+                e = torch.cuda.Event(external=True)   # an event node in a graph
                 e.record(self.s_replay)
                 self._cov_events.append((0, K, e))
 
@@ -446,7 +448,7 @@ class HotPath:
                 if host_src is not None and b > a:
                     for r in range(2):
                         self.cov_host[r, a:b].copy_(self.buffer._cov[r, a:b], non_blocking=True)
-                    e = torch.cuda.Event()
+                    e = torch.cuda.Event(external=True)   # an event node in a graph
                     e.record(self.s_replay)
                     self._cov_events.append((a, b, e))
         self._progress = progress   # keep the counters alive until the stream is done
@@ -476,12 +478,40 @@ class HotPath:
         return rep, lru
 
     def replay_host(self, host_gids):
-        """End to end: pinned/host int32 gids -> BreakdownReport (+ LRU)."""
+        """End to end: pinned/host int32 gids -> BreakdownReport (+ LRU).
+
+        With a pinned source the step's launches (H2D copies, forwards, stats,
+        replay, LRU, coverage copies-back, on their four streams) are captured
+        once into a CUDA graph per (n, source buffer) and replayed as one graph
+        launch, so a synchronous caller does not pay the host launch sequence
+        every step; report() then waits on the graph's coverage event nodes.
+        RECMG_GRAPHS=0 (or a capture failure) runs the launches eagerly."""
         n = int(host_gids.numel()) if hasattr(host_gids, "numel") else len(host_gids)
         if n > self.n_max:
             raise ValueError("trace longer than the HotPath was sized for")
         src = host_gids if hasattr(host_gids, "numel") else self.torch.from_numpy(
             np.ascontiguousarray(host_gids, dtype=np.int32))
+        if _GRAPHS and self.events is None and src.is_pinned():
+            key = (n, src.data_ptr())
+            if getattr(self, "_graph_key", None) != key:
+                self._graph, self._graph_key = None, key
+                self.launch(n, host_src=src)     # eager once: workspaces settle
+                self.report()
+                torch = self.torch
+                g = torch.cuda.CUDAGraph()
+                try:
+                    with torch.cuda.graph(g):
+                        self.launch(n, host_src=src)
+                    self._graph = g
+                    self._graph_state = (list(self._cov_events), self.K, self.n)
+                except Exception:   # not capturable here: stay eager
+                    self._graph = None
+                    torch.cuda.synchronize()
+            if self._graph is not None:
+                self._cov_events, self.K, self.n = (list(self._graph_state[0]),
+                                                    self._graph_state[1], self._graph_state[2])
+                self._graph.replay()
+                return self.report()
         self.launch(n, host_src=src)
         return self.report()
 

@@ -25,6 +25,11 @@ def test_replay_host_matches_device_and_oracle(pieces):
                  pieces=pieces)
     host = torch.from_numpy(t.gid_array.astype(np.int32)).pin_memory()
     rep_h, lru_h = hp.replay_host(host)
+    from paper_2511_08568_b200 import pipeline
+    if pipeline._GRAPHS:   # the pinned end-to-end call runs as one captured CUDA graph
+        assert hp._graph is not None
+        rep_g, lru_g = hp.replay_host(host)   # a graph replay
+        assert rep_g == rep_h and lru_g == lru_h
     K = hp.K
     bits = hp.bits[:K].cpu().numpy()
     pf = hp.pf[:K].cpu().numpy()
