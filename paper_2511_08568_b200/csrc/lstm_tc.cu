@@ -282,6 +282,19 @@ __device__ __forceinline__ void zproduct2(uint32_t tbase, uint32_t a1_hi, uint32
     }
 }
 
+// the four warps of a TMEM lane quadrant (warps q, q+4, q+8, q+12: the four
+// parts of the quadrant's 32 rows) -- all a row's partial scores and head
+// terms are exchanged within them, so the exchange needs no CTA barrier
+#ifndef RECMG_QUAD_SYNC
+#define RECMG_QUAD_SYNC 1
+#endif
+__device__ __forceinline__ void quad_sync(int quad) {
+    if constexpr (RECMG_QUAD_SYNC)
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + quad) : "memory");
+    else
+        __syncthreads();
+}
+
 // sync point after threads wrote TMEM operands / before the MMA issue
 __device__ __forceinline__ void tmem_writes_done() {
     umma::tmem_st_wait();
@@ -1133,7 +1146,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                     attn_scores(c, Es, t + 1, COL_Q, att_v, vsum, rawmask, s_part, L);  // causal: j <= t
                     zero_units(c, COL_Q);   // Q accumulates from zero in the next GEMM1
                 }
-                __syncthreads();
+                quad_sync(c.quad);   // the rows' partial scores / head terms
                 if (t >= 1 && c.part == 0) {
                     lsum = head_b;
 #pragma unroll
@@ -1232,7 +1245,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                 if (!last) {
                     attn_scores(c, Es, L, COL_Z + 64, att_v, vsum, rawmask, s_part, L);  // non-causal
                 }
-                __syncthreads();
+                quad_sync(c.quad);   // the rows' partial scores / head terms
                 if (t >= 1 && c.part == 0) {
                     lsum = head_b;
 #pragma unroll
