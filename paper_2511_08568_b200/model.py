@@ -334,8 +334,9 @@ def _fingerprint(params):
         a = params.arrays[name]
         arr = np.asarray(a)
         h = hashlib.blake2b(digest_size=16)
-        if name == "embed_id" and arr.ndim == 2 and arr.shape[0] > 4096:
-            h.update(np.ascontiguousarray(arr[:: arr.shape[0] // 4096]).tobytes())
+        if name == "embed_id" and arr.ndim == 2 and arr.shape[0] > 1024:
+            # 1024 sampled rows (a strided gather over GBs: 4096 cost ~10 ms a call)
+            h.update(np.ascontiguousarray(arr[:: arr.shape[0] // 1024]).tobytes())
         else:
             h.update(np.ascontiguousarray(arr).tobytes())
         parts.append((name, id(a), arr.__array_interface__["data"][0], arr.shape, h.digest()))

@@ -21,7 +21,7 @@ from .cache_sim import CacheConfig, Policy, simulate
 from .engine import BufferReplay, LruSim, to_device_gids
 from .errors import InvalidConfigError, VocabularyMismatchError
 from .model import CACHING, PREFETCH, ModelParameters, device_model
-from .trace import chunk, num_chunks
+from .trace import Trace, chunk, num_chunks
 
 EVICTION_SPEED = 4
 
@@ -278,12 +278,30 @@ def _hotpath_replay(trace, buffer_cfg, caching_params, prefetch_params, l_in, l_
                      eviction_speed=buffer_cfg.eviction_speed, lru_capacity=None, l_in=l_in,
                      l_out=l_out, window_ratio=window_ratio)
         _HOTPATH.update(key=key, hp=hp, pinned=None)
-    pin = _HOTPATH["pinned"]
-    if pin is None or pin.numel() < n:
-        pin = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
-        _HOTPATH["pinned"] = pin
-    src = pin[:n]
-    src.copy_(torch.from_numpy(np.ascontiguousarray(gids)))   # int64 -> int32, all cores
+    # the pinned int32 copy of an array-backed Trace's ids is kept on the trace
+    # (a Trace is treated as immutable, as its cached unique_count already is),
+    # so a repeated replay() of the same trace skips the host int64 -> int32 pass
+    own = isinstance(trace, Trace)
+    key = (id(trace.gid_array), gids.ctypes.data, n) if own else None
+    cached = getattr(trace, "_recmg_pinned_i32", None) if own else None
+    if cached is not None and cached[0] == key:
+        src = cached[1]
+    else:
+        src_i64 = torch.from_numpy(np.ascontiguousarray(gids))
+        lo, hi = torch.aminmax(src_i64)                       # one parallel host pass
+        if int(lo) < 0 or int(hi) >= trace.total_ids:
+            raise IndexError("access id outside the vocabulary")
+        if own:
+            src = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)[:n]
+        else:
+            pin = _HOTPATH["pinned"]
+            if pin is None or pin.numel() < n:
+                pin = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
+                _HOTPATH["pinned"] = pin
+            src = pin[:n]
+        src.copy_(src_i64)                                    # int64 -> int32, all cores
+        if own:   # validated and converted once per (immutable) trace
+            trace._recmg_pinned_i32 = (key, src)
     rep, _ = hp.replay_host(src)
     return rep
 
@@ -310,10 +328,6 @@ def replay(trace, buffer_cfg: BufferConfig, caching_params=None, prefetch_params
     if (caching_fn is None and prefetch_fn is None and not return_access_class and K and
             (caching_params is not None or prefetch_params is not None) and
             (prefetch_params is None or prefetch_params.l_out == l_out)):
-        torch = _native.torch_cuda()
-        lo, hi = torch.aminmax(torch.from_numpy(gids))        # one parallel host pass
-        if int(lo) < 0 or int(hi) >= trace.total_ids:
-            raise IndexError("access id outside the vocabulary")
         return _hotpath_replay(trace, buffer_cfg, caching_params, prefetch_params, l_in, l_out,
                                window_ratio)
     samples = chunk(trace, l_in, l_out, window_ratio) if (caching_fn or prefetch_fn) else None
