@@ -882,7 +882,7 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                         int64_t mx = 0;
                         for (int w = lane; w < W; w += 32)
                             if (v.tags[w] >= 0) mx = v.meta[w] > mx ? v.meta[w] : mx;
-    #pragma unroll
+#pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
                             const int64_t om = __shfl_xor_sync(FULL, mx, o);
                             mx = om > mx ? om : mx;
@@ -897,7 +897,6 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
                             if (r >= a.es && (unsigned long long)w < best) { best = (unsigned long long)w; bslot = w; }
                         }
                     }
-    #pragma unroll
                     {
                         // warp min of the 64-bit keys (unique per way) with two
                         // REDUX.MIN: the high words, then the low words of the
