@@ -678,8 +678,11 @@ def main():
                                             prefetch_transcendentals(15, 5, args.dim) * K,
                                             prof.get("prefetch_fwd", {}), args.pieces),
                 "replay": {"ms": mean["replay"], "gbs": (ev_n * 4 + n) / (mean["replay"] / 1e3) / 1e9,
-                           "bound": "hbm (7.33 B/access algorithmic); dependency-chain bound",
-                           "overlapped": True},
+                           "bound": "not HBM (7.33 B/access algorithmic): instruction issue on "
+                                    "the ordinary sets' hit-run / miss path (ncu r02e: 60% issue "
+                                    "active at 24 warps/SM); the hot set's serial chain alone is "
+                                    "about half the kernel (DESIGN.md 'Schedule')",
+                           "overlapped": args.pieces > 1},
                 "lru": {"ms": mean["lru"], "gbs": (n * 5) / (mean["lru"] / 1e3) / 1e9,
                         "overlapped": True}}}
     line = {
