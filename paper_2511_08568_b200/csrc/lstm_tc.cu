@@ -406,17 +406,28 @@ __device__ __forceinline__ void row_ld8(const float4 *p, float4 &a, float4 &b) {
 // Folded-table row of the NEXT step, gathered while the current step's MMA
 // and epilogue run: the first NPRE float4 are loaded early into registers,
 // the rest when the row is committed into Z (after the cell has read Z).
-template <int PARTS>
-struct RowStage {
+template <int PARTS, int NPRE_>
+struct RowStageN;
+// early float4 of the next row per phase: measured per model and phase --
+// the register allocation is the whole story (caching decoder at 8: ~240 B
+// of spills, +11%; caching encoder at 4 with decoder 4: +23%; prefetch
+// encoder at 12: +3%)
+#ifndef RECMG_NPRE_ENC_C
+#define RECMG_NPRE_ENC_C 12
+#endif
+#ifndef RECMG_NPRE_ENC_P
+#define RECMG_NPRE_ENC_P 8
+#endif
+#ifndef RECMG_NPRE_DEC
+#define RECMG_NPRE_DEC 4
+#endif
+
+template <int PARTS, int NPRE_>
+struct RowStageN {
     using C = Ctx<PARTS>;
     static constexpr int NF4 = C::U;            // 4U floats = U float4
     static constexpr int NH = C::HU;            // float4 per Z half (4 HU floats)
-#ifndef RECMG_NPRE
-#define RECMG_NPRE 8
-#endif
-    // measured (LDG.256 rows): 8 early float4 beat 4 by 1.2% (caching) / 1.5% (prefetch)
-    // despite ~100 B of spills; 12 spills more
-    static constexpr int NPRE = PARTS == 4 ? RECMG_NPRE : 16;
+    static constexpr int NPRE = PARTS == 4 ? NPRE_ : 16;
     static_assert(NPRE % 4 == 0 && NH % 4 == 0, "loads and commits are whole 64-byte blocks");
     float4 x[NPRE];
     const float4 *src;   // this thread's first-half run; the second half is +128 floats
@@ -860,7 +871,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
     __shared__ uint32_t tmem_base_s;
     __shared__ float lpart[PARTS][128];
     __shared__ int s_tile;
-    const bool caching = (KIND == RECMG_MODEL_CACHING);
+    constexpr bool caching = (KIND == RECMG_MODEL_CACHING);
     const int L = a.m.l_in;
     const int T = caching ? L : a.m.l_out;
     float *s_part = reinterpret_cast<float *>(smem + a.tl.spart_off);
@@ -967,7 +978,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             zero_operand(c, P_H1_HI, P_H1_LO);
         }
         uint32_t rawmask = 0;   // attention key positions stored raw (store_keys)
-        RowStage<PARTS> stage;
+        RowStageN<PARTS, caching ? RECMG_NPRE_ENC_C : RECMG_NPRE_ENC_P> stage;
         stage.prefetch(c, pid_enc, __ldg(gid));
         // prefetch model: the id of the row gathered at step t (for step t + 1)
         // is loaded one step earlier still, so the gather's address is in a
@@ -1119,7 +1130,7 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             zero_operand(c, A_H_HI, A_H_LO);
             zero_operand(c, A_X_HI, A_X_LO);
             zero_units(c, COL_Q);
-            RowStage<PARTS> dstage;
+            RowStageN<PARTS, RECMG_NPRE_DEC> dstage;
             dstage.prefetch(c, pid_dec, __ldg(gid));
             dstage.commit(c);
             for (int t = 0; t <= T; t++) {
