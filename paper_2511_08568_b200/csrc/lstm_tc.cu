@@ -980,11 +980,13 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
         uint32_t rawmask = 0;   // attention key positions stored raw (store_keys)
         RowStageN<PARTS, caching ? RECMG_NPRE_ENC_C : RECMG_NPRE_ENC_P> stage;
         stage.prefetch(c, pid_enc, __ldg(gid));
-        // prefetch model: the id of the row gathered at step t (for step t + 1)
-        // is loaded one step earlier still, so the gather's address is in a
-        // register when the step reaches it (-0.6%; the caching model measured
-        // +0.3% from the extra register)
-        int32_t g_ahead = (!caching && L > 1) ? __ldg(gid + 1) : 0;
+        // the id of the row gathered at step t (for step t + 1) is loaded one
+        // step earlier still, so the gather's address is in a register when the
+        // step reaches it (prefetch -0.6%, caching encoder -0.7%)
+#ifndef RECMG_GID_AHEAD_C
+#define RECMG_GID_AHEAD_C 1
+#endif
+        int32_t g_ahead = ((!caching || RECMG_GID_AHEAD_C) && L > 1) ? __ldg(gid + 1) : 0;
         stage.commit(c);
         for (int t = 0; t <= L; t++) {
             const bool last = (t == L);   // t == L: only enc_pre of the last state
@@ -1004,7 +1006,15 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                                                      sbase + tl.b_off[0], true, &mbar2, &mbar3);
                 }
                 pc.mark(12);
-                if (t + 1 < L) stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
+                if (t + 1 < L) {
+                    if constexpr (RECMG_GID_AHEAD_C) {
+                        const int32_t g1 = g_ahead;
+                        if (t + 2 < L) g_ahead = __ldg(gid + t + 2);
+                        stage.prefetch(c, pid_enc, g1);
+                    } else {
+                        stage.prefetch(c, pid_enc, __ldg(gid + t + 1));
+                    }
+                }
                 pc.mark(13);
                 wait_mma(&mbar, phase);
                 pc.mark(2);
@@ -1132,6 +1142,10 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
             zero_units(c, COL_Q);
             RowStageN<PARTS, RECMG_NPRE_DEC> dstage;
             dstage.prefetch(c, pid_dec, __ldg(gid));
+#ifndef RECMG_GID_AHEAD_D
+#define RECMG_GID_AHEAD_D 0
+#endif
+            int32_t gd_ahead = (RECMG_GID_AHEAD_D && T > 1) ? __ldg(gid + 1) : 0;
             dstage.commit(c);
             for (int t = 0; t <= T; t++) {
                 const bool last = (t == T);   // t == T: only finish comb_{T-1}
@@ -1206,7 +1220,15 @@ __global__ void __launch_bounds__(128 * PartsOf<KIND>::value, 1) lstm_tc_kernel(
                          sbase + 2 * tl.img64, 64, false);               // Wcomb_c
                     umma::commit(&mbar2);
                 }
-                if (t + 1 < T) dstage.prefetch(c, pid_dec, __ldg(gid + t + 1));
+                if (t + 1 < T) {
+                    if constexpr (RECMG_GID_AHEAD_D) {
+                        const int32_t g1 = gd_ahead;
+                        if (t + 2 < T) gd_ahead = __ldg(gid + t + 2);
+                        dstage.prefetch(c, pid_dec, g1);
+                    } else {
+                        dstage.prefetch(c, pid_dec, __ldg(gid + t + 1));
+                    }
+                }
                 wait_mma(&mbar, phase);
                 pc.mark(8);
                 // Wc_d done (and so every earlier MMA): swap Wh_d back under the cell
