@@ -692,7 +692,8 @@ def main():
         "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (reference generator, bit-exact) + reference init_params weights",
         "config": workload(args, 0),
-        "tuning": {"pipeline_pieces": args.pieces, "model_sms": args.model_sms},
+        "tuning": {"pipeline_pieces": hp.pieces, "model_sms": hp.model_sms,
+                   "schedule": "serial" if hp.pieces == 1 and not hp.piece_chunks else "pipelined"},
         "quality": {"on_demand": c[2], "lru32_misses": c[7],
                     "on_demand_vs_lru32": (c[2] / c[7]) if c[7] else None,
                     "cache_hits": c[0], "prefetch_hits": c[1], "prefetch_issued": c[3],

@@ -35,3 +35,4 @@ for _ in range(9):
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1))
 print(f"whole-trace replay (events + partition + replay): {np.median(ms[1:]):.2f} ms")
+print("counters", buf.result(with_coverage=False))
