@@ -83,6 +83,8 @@ def parse():
                          "set makes the replay a single long chain)")
     ap.add_argument("--model-sms", type=int, default=136, help="SMs the forwards may use")
     ap.add_argument("--batch", type=int, default=512, help="config 4: samples per batch")
+    ap.add_argument("--hook-inline", action="store_true",
+                    help="config 4: K5/K6 in line on the replay stream (no state snapshot)")
     ap.add_argument("--config", type=int, default=None, choices=[2, 3, 4],
                     help="workload: 2 (single-GPU config, the N=1 default) or 3 (856 tables, "
                          "500 M accesses, table-sharded: the N>1 default)")
@@ -786,7 +788,7 @@ def run_config4(args, torch):
     torch.cuda.synchronize()
     st = {}
 
-    def hook(k0, k1, last):
+    def hook(k0, k1, last, state):
         a0, a1 = 15 * k0, (n if last else 15 * k1)
         nb = -(-(a1 - a0) // P)
         off = st["offsets"].get(a1 - a0)
@@ -796,15 +798,21 @@ def run_config4(args, torch):
             st["offsets"][a1 - a0] = off
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         evs[0].record()
-        st["rows"].refresh()
+        st["rows"].refresh(state)
         evs[1].record()
-        st["rows"].pool(st["hp"].gids[a0:a1], off, st["out"][:nb])
+        st["rows"].pool(st["hp"].gids[a0:a1], off, st["out"][:nb], state=state)
         evs[2].record()
         st["ev"].append(evs)
 
+    # one wave of 128-chunk tiles per batch forward: 17,477 chunks are 137
+    # tiles, so the default 136-SM budget would run the last tile as a second
+    # wave (measured: forwards 171 -> 122 ms per step at 137 SMs)
+    sms = args.model_sms
+    if sms == 136:
+        sms = min(148, max(sms, -(-Kb // 128)))
     hp = HotPath(DeviceModel(cp, emb_c), DeviceModel(pp, emb_p), t.table_sizes, C32, n, ways=32,
-                 eviction_speed=4, lru_capacity=C32, lru_ways=32, model_sms=args.model_sms,
-                 piece_chunks=Kb, piece_hook=hook)
+                 eviction_speed=4, lru_capacity=C32, lru_ways=32, model_sms=sms,
+                 piece_chunks=Kb, piece_hook=hook, hook_snapshot=not args.hook_inline)
     del emb_c, emb_p
     rows = RowStore(hp.buffer, host)
     st.update(hp=hp, rows=rows, ev=[], offsets={},
@@ -857,7 +865,8 @@ def run_config4(args, torch):
         "data": "synthetic (reference generator, bit-exact) + reference init_params weights + "
                 "N(0,1) host rows",
         "config": workload(args, 0),
-        "tuning": {"model_sms": args.model_sms, "chunks_per_batch": Kb},
+        "tuning": {"model_sms": hp.model_sms, "chunks_per_batch": Kb,
+                   "hook": "snapshot stream" if hp.hook_snapshot else "in line"},
         "batches_per_step": nbatch, "ms_per_batch": ms / nbatch,
         "quality": {"on_demand": rep.on_demand, "prefetch_inserts": rep.prefetch_inserts,
                     "lru32_misses": lru[1], "cache_hits": rep.cache_hits,

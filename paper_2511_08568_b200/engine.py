@@ -200,19 +200,22 @@ class RowStore:
         self.copied = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.src = torch.zeros(2, dtype=torch.int64, device="cuda")
 
-    def refresh(self):
+    def refresh(self, state=None):
+        """state: a buffer state blob of this replay's geometry (default: the
+        live one), e.g. a HotPath hook snapshot."""
         _native.check(_native.lib().recmg_rows_refresh(
-            ctypes.byref(self.replay.cfg), _native.ptr(self.replay.state),
+            ctypes.byref(self.replay.cfg), _native.ptr(self.replay.state if state is None else state),
             _native.ptr(self.loaded), ctypes.c_void_p(self.host.data_ptr()), self.dim,
             _native.ptr(self.buf), _native.ptr(self.copied),
             _native.stream_handle(self.torch)), "rows_refresh")
 
-    def pool(self, gids, offsets, out=None):
+    def pool(self, gids, offsets, out=None, state=None):
         n_bags = offsets.numel() - 1
         if out is None:
             out = self.torch.empty((n_bags, self.dim), dtype=self.torch.float32, device="cuda")
         _native.check(_native.lib().recmg_embedding_bag(
-            ctypes.byref(self.replay.cfg), _native.ptr(self.replay.state), _native.ptr(gids),
+            ctypes.byref(self.replay.cfg),
+            _native.ptr(self.replay.state if state is None else state), _native.ptr(gids),
             _native.ptr(offsets), n_bags, _native.ptr(self.buf),
             ctypes.c_void_p(self.host.data_ptr()), self.dim, _native.ptr(out),
             _native.ptr(self.src), _native.stream_handle(self.torch)), "embedding_bag")

@@ -60,7 +60,7 @@ class HotPath:
                  l_out: int = 5, window_ratio: int = 3, pieces: int | None = None,
                  model_sms: int = 136,
                  shard=None, replay_priority: bool = True, piece_chunks: int | None = None,
-                 piece_hook=None):
+                 piece_hook=None, hook_snapshot: bool = True):
         """pieces = None picks the schedule from the buffer geometry: one
         replay after both forwards (pieces = 1, `_launch_serial`) when the
         buffer has at least 256 sets -- the replay is then throughput-bound and
@@ -75,9 +75,16 @@ class HotPath:
         the start.  The TC forwards then use `model_sms` SMs, leaving the rest
         to the replay CTAs.  piece_chunks fixes the piece length in chunks (a
         serving batch) instead of dividing the trace into `pieces`;
-        piece_hook(k0, k1, last) runs on the replay stream right after each
-        piece's replay (the DLRM embedding stage: K5 row refresh + K6 pooling
-        of that batch), so it overlaps the next piece's forwards.
+        piece_hook(k0, k1, last, state) runs after each piece's replay (the
+        DLRM embedding stage: K5 row refresh + K6 pooling of that batch) on the
+        buffer state as that replay left it, so it overlaps the next piece's
+        forwards.  With hook_snapshot (the default) the state is a copy taken
+        on the replay stream (double-buffered, 5 MB at config 2) and the hook
+        runs on its own stream, so the next piece's replay overlaps this
+        piece's hook as well (the hook sees exactly the state it would see
+        in line; config 4: the replay stream no longer carries replay + K5 +
+        K6 per batch); without it, the hook runs in line on the replay stream
+        with state = the live buffer state.
 
         shard (shard.TableShard): the models are a table shard's, packed over
         its local vocabulary (shard.init_params_shard, DeviceModel with
@@ -128,6 +135,7 @@ class HotPath:
         self.pieces = max(1, int(pieces))
         self.piece_chunks = int(piece_chunks) if piece_chunks else None
         self.piece_hook = piece_hook
+        self.hook_snapshot = bool(hook_snapshot) and piece_hook is not None
         self.model_sms = int(model_sms) if (self.pieces > 1 or self.piece_chunks) else 148
         # the replay and the LRU run under the forwards on the SMs they leave;
         # high priority makes the block scheduler hand freed SMs to them first
@@ -138,6 +146,9 @@ class HotPath:
         self.cov_host = torch.empty((2, max(self.K_max, 1)), dtype=torch.int16, pin_memory=True)
         self._cov_events = []
         self.s_lru = torch.cuda.Stream(priority=prio)
+        self.s_hook = torch.cuda.Stream(priority=prio) if self.hook_snapshot else None
+        self._snaps = ([torch.empty_like(self.buffer.state) for _ in range(2)]
+                       if self.hook_snapshot else None)
         self.events = None
         self.stage_ms = {}
 
@@ -225,6 +236,7 @@ class HotPath:
         else:
             all_ids.record(main)
         self._cov_events = []
+        hook_done = [None, None]   # per snapshot slot: the hook that last read it
         # K4: the LRU comparator depends only on the ids
         def run_lru(after):
             self.s_lru.wait_event(after)
@@ -301,10 +313,17 @@ class HotPath:
                     self._ev("replay", self.s_replay)
                     self.buffer.run_chunks(g, k0, k1, i == len(pieces) - 1, bits, pf)
                     self._ev("replay", self.s_replay)
-                    if self.piece_hook is not None:
+                    if self.piece_hook is not None and not self.hook_snapshot:
                         self._ev("hook", self.s_replay)
-                        self.piece_hook(k0, k1, i == len(pieces) - 1)
+                        self.piece_hook(k0, k1, i == len(pieces) - 1, self.buffer.state)
                         self._ev("hook", self.s_replay)
+                    if self.hook_snapshot:
+                        slot = i & 1
+                        if hook_done[slot] is not None:   # the hook two pieces back is done with it
+                            self.s_replay.wait_event(hook_done[slot])
+                        self._snaps[slot].copy_(self.buffer.state, non_blocking=True)
+                        snapped = torch.cuda.Event()
+                        snapped.record(self.s_replay)
                     if host_src is not None and k1 > k0:
                         for r in range(2):   # contiguous rows: plain async D2H copies
                             self.cov_host[r, k0:k1].copy_(self.buffer._cov[r, k0:k1],
@@ -312,6 +331,14 @@ class HotPath:
                         e = torch.cuda.Event(external=True)   # an event node in a graph
                         e.record(self.s_replay)
                         self._cov_events.append((k0, k1, e))
+                if self.hook_snapshot:
+                    self.s_hook.wait_event(snapped)
+                    with torch.cuda.stream(self.s_hook):
+                        self._ev("hook", self.s_hook)
+                        self.piece_hook(k0, k1, i == len(pieces) - 1, self._snaps[slot])
+                        self._ev("hook", self.s_hook)
+                        hook_done[slot] = torch.cuda.Event()
+                        hook_done[slot].record(self.s_hook)
         finally:
             L.recmg_set_model_sm_budget(prev)
         if lru_late:   # after the forwards: beside the replay's single-warp chain
@@ -320,6 +347,8 @@ class HotPath:
             run_lru(fwd_done)
         self._ev("tail", main)          # forwards done ...
         main.wait_stream(self.s_replay)
+        if self.s_hook is not None:
+            main.wait_stream(self.s_hook)
         if self.lru is not None:
             main.wait_stream(self.s_lru)
         self._ev("tail", main)          # ... -> last replay piece and LRU done

@@ -99,3 +99,56 @@ def test_streamed_schedule_matches_oracle(monkeypatch, pf_first):
         [ref[k] for k in ("cache_hits", "prefetch_hits", "on_demand", "prefetch_issued",
                           "prefetch_useful", "evictions", "prefetch_inserts")]
     assert rep.coverage == cov
+
+
+@pytest.mark.parametrize("snapshot", [True, False])
+def test_batch_hook_pools_each_batch_like_embedding_bag(snapshot):
+    """Serving batches (piece_chunks) with the K5 + K6 hook after each
+    batch's replay: on the state snapshot (its own stream, overlapping the
+    next batch's replay) or in line on the live state, every batch's pooled
+    bags equal torch embedding_bag of the host rows, the rows of the
+    snapshot's resident slots are in HBM, and the counters equal a hook-less
+    run of the same trace."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2511_08568_b200.engine import RowStore
+    t = rb.generate_trace(rb.TraceGenConfig([3000] * 16, 120_000, 1.05, 0.4, 32, 17))
+    cp = rb.init_params("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
+    pp = rb.init_params("prefetch", t.table_sizes, dim=64, seed=1, init_scale=0.4)
+    n, V, D, P = len(t), t.total_ids, 32, 2
+    C = int(0.2 * t.unique_count)
+    C32 = C - C % 32
+    host = torch.from_numpy(np.random.default_rng(5).standard_normal((V, D))
+                            .astype(np.float32)).pin_memory()
+    got, resident_ok = {}, []
+    st = {}
+
+    def hook(k0, k1, last, state):
+        a0, a1 = 15 * k0, (n if last else 15 * k1)
+        nb = -(-(a1 - a0) // P)
+        off = torch.arange(0, nb * P + 1, P, dtype=torch.int64, device="cuda")
+        off[-1] = a1 - a0
+        st["rows"].refresh(state)
+        out = st["rows"].pool(st["hp"].gids[a0:a1], off, state=state)
+        got[(a0, a1)] = (out, off, state.clone(), st["rows"].buf.clone())
+
+    hp = HotPath(cp, pp, t.table_sizes, C32, n, ways=32, lru_capacity=C32, lru_ways=32,
+                 piece_chunks=1024, piece_hook=hook, hook_snapshot=snapshot)
+    st.update(hp=hp, rows=RowStore(hp.buffer, host))
+    hp.gids[:n].copy_(torch.from_numpy(t.gid_array.astype(np.int32)))
+    hp.launch(n)
+    rep, lru = hp.report()
+    assert len(got) == -(-hp.K // 1024) > 4
+    S = C32 // 32
+    for (a0, a1), (out, off, state, buf) in got.items():
+        ids = torch.from_numpy(t.gid_array[a0:a1]).long()
+        want = F.embedding_bag(ids, host, off[:-1].cpu(), mode="sum")
+        assert torch.equal(out.cpu(), want), (a0, (out.cpu() - want).abs().max())
+        tags = state[64:64 + 4 * S * 32].view(torch.int32).cpu().numpy()
+        res = tags >= 0
+        assert np.array_equal(buf.cpu().numpy()[res], host.numpy()[tags[res]])
+    plain = HotPath(cp, pp, t.table_sizes, C32, n, ways=32, lru_capacity=C32, lru_ways=32,
+                    piece_chunks=1024)
+    plain.gids[:n].copy_(hp.gids[:n])
+    plain.launch(n)
+    assert plain.report() == (rep, lru)
