@@ -135,6 +135,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
         ra.seg_start = p.pb.seg_start;
         ra.seg_end = p.pb.seg_end;
         ra.heavy = p.g.wide ? nullptr : p.pb.heavy;
+        ra.work = p.g.wide ? nullptr : p.pb.work;
     }
     ra.ev = ev;
     ra.vals = vv;
@@ -142,6 +143,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     ra.S = p.g.S;
     ra.W = p.g.W;
     ra.es = cfg->eviction_speed;
+    ra.gid_bits = gid_bits_of(cfg->total_ids);
     ra.l_in = l_in;
     ra.Ec = p.Ec;
     ra.K = p.K;
@@ -423,6 +425,7 @@ int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *g
         ra.seg_start = p.pb.seg_start;
         ra.seg_end = p.pb.seg_end;
         ra.heavy = g.wide ? nullptr : p.pb.heavy;
+        ra.work = g.wide ? nullptr : p.pb.work;
     }
     ra.ev = k;
     ra.vals = v;
@@ -430,6 +433,7 @@ int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *g
     ra.S = g.S;
     ra.W = g.W;
     ra.es = cfg->eviction_speed;            // SRRIP: max rrpv
+    ra.gid_bits = gid_bits_of(cfg->total_ids);
     ra.st = state_view(state, cfg, g);
     ra.hits_misses = hits_misses;
     ra.per_access_hit = hit;

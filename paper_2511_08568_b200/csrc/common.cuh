@@ -27,6 +27,9 @@ constexpr int64_t kSmemMaxWays = 4096;  // sets up to this many ways replay in s
 // sets whose event segment is far above the mean are replayed by the first
 // CTAs of the launch (so the longest dependency chains start first)
 constexpr int kHeavySets = 32;
+constexpr int kHeavyCand = 1024;  // candidates ranked for the heavy list
+// replay work queue words: the next item, then one heavy-chain count per SM id
+constexpr int kWorkWords = 1 + 256;
 
 // Event word: [type:2][gid:30]
 enum : uint32_t { EV_SERVE = 0u, EV_UPD0 = 1u, EV_UPD1 = 2u, EV_PREFETCH = 3u };
@@ -102,6 +105,13 @@ struct Arena {
     }
     bool ok() const { return used <= size; }
 };
+
+// bits needed for the largest gid (total_ids - 1), at least 1
+inline int gid_bits_of(int64_t total_ids) {
+    int b = 1;
+    while (b < 62 && (int64_t(1) << b) < total_ids) b++;
+    return b;
+}
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 

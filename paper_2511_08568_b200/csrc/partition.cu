@@ -219,13 +219,35 @@ __global__ void seg_bounds_kernel(const uint32_t *__restrict__ k, int64_t N, uin
 // first instead of in set order behind thousands of short sets.
 __global__ void heavy_sets_kernel(const uint32_t *__restrict__ start,
                                   const uint32_t *__restrict__ end, int64_t S, uint32_t thr,
-                                  int32_t *__restrict__ heavy) {
+                                  int32_t *__restrict__ cand) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= S) return;
     if (end[s] > start[s] && end[s] - start[s] >= thr) {
-        const int i = atomicAdd(heavy, 1);
-        if (i < kHeavySets) heavy[1 + i] = (int32_t)s;
+        const int i = atomicAdd(cand, 1);
+        if (i < kHeavyCand) cand[1 + i] = (int32_t)s;
     }
+}
+
+// The kHeavySets longest of the candidates, longest first (ties: lower set),
+// so the longest chains are the first items of the replay launch.
+__global__ void __launch_bounds__(kHeavyCand)
+heavy_rank_kernel(const uint32_t *__restrict__ start, const uint32_t *__restrict__ end,
+                  const int32_t *__restrict__ cand, int32_t *__restrict__ heavy) {
+    __shared__ uint32_t len[kHeavyCand];
+    __shared__ int32_t id[kHeavyCand];
+    const int n = min(cand[0], kHeavyCand);
+    const int i = threadIdx.x;
+    if (i < n) {
+        id[i] = cand[1 + i];
+        len[i] = end[id[i]] - start[id[i]];
+    }
+    __syncthreads();
+    if (i == 0) heavy[0] = min(n, kHeavySets);
+    if (i >= n) return;
+    int rank = 0;
+    for (int j = 0; j < n; j++)
+        rank += (len[j] > len[i]) || (len[j] == len[i] && id[j] < id[i]);
+    if (rank < kHeavySets) heavy[1 + rank] = id[i];
 }
 
 int partition_passes(int64_t S) {
@@ -247,6 +269,8 @@ void partition_plan(Arena &a, PartitionBuffers &pb, int64_t N, int64_t S, bool v
     pb.seg_start = a.take<uint32_t>((size_t)S + 1);
     pb.seg_end = a.take<uint32_t>((size_t)S + 1);
     pb.heavy = a.take<int32_t>(1 + kHeavySets);
+    pb.heavy_cand = a.take<int32_t>(1 + kHeavyCand);
+    pb.work = a.take<uint32_t>(kWorkWords);
 }
 
 int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaStream_t s) {
@@ -282,11 +306,14 @@ int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaSt
     seg_bounds_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(keys, N, (uint32_t)S,
                                                                   pb.seg_start, pb.seg_end);
     RECMG_LAUNCH_CHECK();
-    RECMG_CUDA_TRY(cudaMemsetAsync(pb.heavy, 0, sizeof(int32_t), s));
+    RECMG_CUDA_TRY(cudaMemsetAsync(pb.heavy_cand, 0, sizeof(int32_t), s));
     const int64_t mean = N / (S > 0 ? S : 1);
     const uint32_t thr = (uint32_t)(mean * 8 > 4096 ? mean * 8 : 4096);
     heavy_sets_kernel<<<(unsigned)((S + 255) / 256), 256, 0, s>>>(pb.seg_start, pb.seg_end, S,
-                                                                   thr, pb.heavy);
+                                                                   thr, pb.heavy_cand);
+    RECMG_LAUNCH_CHECK();
+    heavy_rank_kernel<<<1, kHeavyCand, 0, s>>>(pb.seg_start, pb.seg_end, pb.heavy_cand,
+                                               pb.heavy);
     RECMG_LAUNCH_CHECK();
     return RECMG_OK;
 }

@@ -11,6 +11,8 @@ struct PartitionBuffers {
     uint32_t *hist = nullptr, *offs = nullptr, *partial = nullptr;
     uint32_t *seg_start = nullptr, *seg_end = nullptr;  // [S+1]
     int32_t *heavy = nullptr;  // [1 + kHeavySets]: count, then the heaviest sets
+    uint32_t *work = nullptr;  // [kWorkWords]: the replay launch's work queue
+    int32_t *heavy_cand = nullptr;  // [1 + kHeavyCand]: count, then sets above the threshold
 };
 
 int partition_passes(int64_t S);

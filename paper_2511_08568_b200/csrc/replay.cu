@@ -20,6 +20,7 @@
 // global memory, an id -> slot map, the same batching by warp 0 and the
 // victim scan by the whole CTA (replay_wide_kernel).
 #include "replay.cuh"
+#include <cstdlib>
 
 namespace recmg {
 
@@ -524,36 +525,219 @@ __device__ __forceinline__ void ht_erase(const SetView &v, uint32_t g) {
     v.ht[i] = kHtEmpty;
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident replay of one set of W <= 32 ways (PRIORITY and LRU, the
+// two policies of the hot path): lane w IS way w -- its gid, its priority
+// (lazy decay, see replay_smem_kernel) and prefetch tag, or its LRU clock
+// live in registers, so membership needs no hash index and a miss no
+// shared-memory bookkeeping.  Per batch of 32 events (lane j holds event j):
+//   membership   32 x (SHFL of event j's gid, compare with my tag, set bit j):
+//                `mine` = the batch's events that name my way; hit = OR of
+//                every way's `mine` (one REDUX.OR)
+//   hit run      the events before the first residency-changing miss, applied
+//                per way from `mine` (first S takes the tag, last U/P sets the
+//                priority; LRU: clock of the last hit), which equals the
+//                sequential order because hits never change residency
+//   miss         victim = argmin (priority, gid) [LRU: min clock] as two
+//                REDUX.MIN over the lanes, the victim lane takes the new gid,
+//                its `mine` becomes the remaining events naming that gid
+// The result (counters, per-access class, per-access hit, the state written
+// back) is identical to replay_smem_kernel's.  Used for every set that is
+// not on the heavy list: sets whose events are mostly misses and short hit
+// runs, where the shared-memory kernel's hash probing, run grouping
+// (MATCH.ANY) and per-miss hash updates cost ~150 warp instructions per event.
+template <int POLICY, bool CLASS>
+__device__ __forceinline__ void replay_set_regs(const ReplayArgs &a, int64_t set, int64_t lo,
+                                                int64_t hi, EventRing &ring, int lane) {
+    constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int W = (int)a.W;
+    const int64_t sbase = set * a.W;
+    const bool is_way = lane < W;
+    int32_t tag = is_way ? a.st.tags[sbase + lane] : -2;   // -2: no such way
+    const int64_t m0 = is_way ? a.st.meta[sbase + lane] : 0;
+    // PRIORITY: pr = stored priority (+ decay), mhi = the meta's high word
+    // (bit 0 = prefetch tag); LRU: clk = clock of the last use
+    int32_t pr = (int32_t)(m0 & 0xFFFFFFFF);
+    uint32_t mhi = (uint32_t)((uint64_t)m0 >> 32);
+    int64_t clk = m0;
+    int count = __popc(__ballot_sync(FULL, tag >= 0));
+    const int64_t clock_base = a.st.header[0];
+    int32_t decay = 0;
+    unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
+    // one 32-bit victim key (a single REDUX.MIN) when it orders the ways
+    // exactly: PRIORITY (priority << gid_bits) | gid while every priority fits
+    // (events only ever set es or es + 1; the decay only lowers them); LRU the
+    // clock relative to clock_base - 2^31 while every clock of the launch fits
+    const int gb = a.gid_bits;
+    const int64_t kbase = clock_base - 0x80000000ll;
+    bool key32;
+    if (PRIO) {
+        const int32_t lim = gb > 0 && gb <= 28 ? (1 << (32 - gb)) - 1 : 0;
+        key32 = a.es + 1 < lim && __all_sync(FULL, tag < 0 || pr < lim);
+    } else {
+        key32 = hi - lo < 0x7FFFFFFFll && clock_base + hi - kbase < 0xFFFFFFFFll &&
+                __all_sync(FULL, tag < 0 || clk >= kbase);
+    }
+
+    for (int64_t pos = lo; pos < hi; pos += 32) {
+        const int nb = (int)imin64(32, hi - pos);
+        ring.ensure(pos - lo, nb);
+        const uint32_t e = lane < nb ? ring.at(pos - lo + lane) : kGidMask;
+        const uint32_t g = ev_gid(e), ty = ev_type(e);
+        const bool real = g != kGidMask;
+        unsigned mine = 0;
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const uint32_t gj = __shfl_sync(FULL, g, j);
+            if ((uint32_t)tag == gj) mine |= 1u << j;
+        }
+        unsigned hit = __reduce_or_sync(FULL, mine);
+        const unsigned Sm = __ballot_sync(FULL, real && ty == EV_SERVE);
+        unsigned cand, UPm = 0, U1m = 0;
+        if (PRIO) {
+            UPm = __ballot_sync(FULL, real && ty != EV_SERVE);
+            U1m = __ballot_sync(FULL, real && ty == EV_UPD1);
+            cand = Sm | __ballot_sync(FULL, real && ty == EV_PREFETCH);
+        } else {
+            cand = __ballot_sync(FULL, real);   // simulate(): every event is a serve
+        }
+        int start = 0;
+        for (;;) {
+            const unsigned from = ~0u << start;
+            const unsigned miss = cand & ~hit & from;
+            const int cut = miss ? __ffs(miss) - 1 : nb;
+            const unsigned R = (cut >= 32 ? ~0u : ((1u << cut) - 1u)) & from;
+            const unsigned rk = mine & R;
+            if (PRIO) {
+                const unsigned sp = rk & Sm, up = rk & UPm;
+                unsigned pfirst = 0;
+                if (sp) {
+                    const unsigned c = __popc(sp);
+                    if (mhi & 1u) { ph += 1; ch += c - 1; mhi &= ~1u; pfirst = sp & (0u - sp); }
+                    else ch += c;
+                }
+                if (up) {
+                    const int last = 31 - __clz(up);
+                    pr = a.es + (int32_t)((U1m >> last) & 1u) + decay;
+                }
+                if (CLASS) {
+                    const unsigned pf = __reduce_or_sync(FULL, pfirst);
+                    if ((R & Sm) >> lane & 1u) write_class(a, pos + lane, (pf >> lane & 1u) ? 1 : 0);
+                }
+            } else if (rk) {
+                lhits += __popc(rk);
+                clk = clock_base + pos + (31 - __clz(rk));
+            }
+            if (cut >= nb) break;
+            // the miss at `cut`
+            const uint32_t gc = __shfl_sync(FULL, g, cut);
+            const bool isS = (Sm >> cut) & 1u;
+            if (PRIO) {
+                if (isS) {
+                    od++;
+                    if (CLASS && lane == 0) write_class(a, pos + cut, 2);
+                } else {
+                    ins++;
+                }
+            } else {
+                od++;
+                if (a.per_access_hit && lane == 0)
+                    a.per_access_hit[a.vals ? a.vals[pos + cut] : pos + cut] = 0;
+            }
+            int target;
+            if (count >= W && key32) {
+                unsigned key;
+                if (PRIO) {
+                    const int32_t pe = pr - decay;
+                    key = tag >= 0 ? ((unsigned)(pe > 0 ? pe : 0) << gb) | (unsigned)tag : ~0u;
+                } else {
+                    key = tag >= 0 ? (unsigned)(clk - kbase) : ~0u;
+                }
+                const unsigned kmin = __reduce_min_sync(FULL, key);
+                target = __ffs(__ballot_sync(FULL, key == kmin)) - 1;
+                if (PRIO) decay++;
+                nev++;
+                count--;
+            } else if (count >= W) {
+                // populate(): victim = argmin (priority, gid)  [LRU: min clock]
+                unsigned khi, klo;
+                if (PRIO) {
+                    const int32_t pe = pr - decay;
+                    khi = tag >= 0 ? (unsigned)(pe > 0 ? pe : 0) : ~0u;
+                    klo = (unsigned)tag;
+                } else {
+                    khi = tag >= 0 ? (unsigned)((uint64_t)clk >> 32) : ~0u;
+                    klo = (unsigned)clk;
+                }
+                const unsigned hmin = __reduce_min_sync(FULL, khi);
+                const unsigned lmin = __reduce_min_sync(FULL, khi == hmin ? klo : ~0u);
+                target = __ffs(__ballot_sync(FULL, khi == hmin && klo == lmin)) - 1;
+                if (PRIO) decay++;
+                nev++;
+                count--;
+            } else {
+                // the first free way (the shared-memory kernel's choice)
+                target = __ffs(__ballot_sync(FULL, tag == -1)) - 1;
+            }
+            const unsigned named = __ballot_sync(FULL, g == gc);
+            if (lane == target) {
+                tag = (int32_t)gc;
+                if (PRIO) {
+                    pr = a.es + decay;
+                    mhi = isS ? 0u : 1u;
+                } else {
+                    clk = clock_base + pos + cut;
+                }
+                mine = named;   // the evicted gid's events now miss
+            }
+            count++;
+            hit = __reduce_or_sync(FULL, mine);
+            start = cut + 1;
+            if (start >= nb) break;
+        }
+    }
+
+    if (is_way) {
+        a.st.tags[sbase + lane] = tag;
+        int64_t m;
+        if (PRIO) {
+            const int32_t pe = pr - decay;
+            m = (int64_t)((uint64_t)mhi << 32) | (int64_t)(uint32_t)(pe > 0 ? pe : 0);
+        } else {
+            m = clk;
+        }
+        a.st.meta[sbase + lane] = m;
+    }
+    if (lane == 0) a.st.count[set] = count;
+    if (PRIO) {
+        ch = __reduce_add_sync(FULL, (unsigned)ch);
+        ph = __reduce_add_sync(FULL, (unsigned)ph);
+        if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
+    } else {
+        lhits = __reduce_add_sync(FULL, (unsigned)lhits);
+        if (lane == 0 && a.hits_misses) {
+            if (lhits) atomicAdd((unsigned long long *)&a.hits_misses[0], lhits);
+            if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
+        }
+    }
+}
+
+// Diagnostic (scripts/replay_set_timeline.py): when set, every replay_smem_kernel
+// warp records [set, start ns, end ns, smid, path] of its set.
+__device__ int64_t *g_set_timing = nullptr;
+
 #ifndef RECMG_REPLAY_MINB
 #define RECMG_REPLAY_MINB 24
 #endif
 template <int POLICY, bool CLASS>
-__global__ void __launch_bounds__(32, RECMG_REPLAY_MINB)
-replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes_per_warp) {
-    extern __shared__ __align__(16) uint8_t dsm[];
+__device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set, uint8_t *base,
+                                               int Wp, int hbits, int regs, bool heavy_item) {
     const unsigned FULL = 0xFFFFFFFFu;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t set = (int64_t)blockIdx.x * warps_per_cta + warp;
-    if (a.heavy) {
-        // CTAs [0, kHeavySets) replay the listed heavy sets, the rest every
-        // other set in order (one warp per CTA when heavy sets are listed)
-        const int nh = min(__ldg(a.heavy), kHeavySets);
-#if defined(RECMG_DIAG_SETS)   // diagnostic builds: 1 = heavy sets only, 2 = the others only
-        if ((RECMG_DIAG_SETS == 1) != (blockIdx.x < kHeavySets)) return;
-#endif
-        if (blockIdx.x < kHeavySets) {
-            if ((int)blockIdx.x >= nh) return;
-            set = __ldg(a.heavy + 1 + blockIdx.x);
-        } else {
-            set = (int64_t)blockIdx.x - kHeavySets;
-            const bool listed = lane < nh && __ldg(a.heavy + 1 + lane) == (int32_t)set;
-            if (__any_sync(0xFFFFFFFFu, listed)) return;
-        }
-    }
+    const int lane = threadIdx.x & 31;
     if (set >= a.S) return;
     const int W = (int)a.W;
     const int64_t sbase = set * a.W;
-    uint8_t *base = dsm + (size_t)warp * bytes_per_warp;
     SetView v;
     v.ring = reinterpret_cast<uint32_t *>(base);
     v.tags = reinterpret_cast<int32_t *>(base + kRingSlots * kRingBlk * 4);
@@ -564,8 +748,33 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
 
     int64_t lo, hi;
     seg_range(a, set, lo, hi);
+    int64_t *const timing = g_set_timing;
+    uint64_t t_start = 0;
+    if (timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    auto note_time = [&](int path) {
+        if (timing && lane == 0) {
+            uint64_t t_end;
+            uint32_t sm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            int64_t *r = timing + 4 * set;
+            r[0] = (int64_t)t_start;
+            r[1] = (int64_t)t_end;
+            r[2] = (int64_t)sm | ((int64_t)path << 32);
+            r[3] = hi - lo;
+        }
+    };
     EventRing ring;
     ring.init(v.ring, a.ev + lo, hi - lo, lane);
+    if constexpr (POLICY == RECMG_POLICY_PRIORITY || POLICY == RECMG_POLICY_LRU) {
+        // every set but the listed heavy ones (their long uniform runs take the
+        // fast path below) replays with its ways in registers
+        if (W <= 32 && !heavy_item && hi - lo < (int64_t)regs) {
+            replay_set_regs<POLICY, CLASS>(a, set, lo, hi, ring, lane);
+            note_time(1);
+            return;
+        }
+    }
 
     for (uint32_t i = lane; i <= v.hmask; i += 32) v.ht[i] = kHtEmpty;
     int cnt = 0;
@@ -981,6 +1190,57 @@ replay_smem_kernel(ReplayArgs a, int warps_per_cta, int Wp, int hbits, int bytes
             if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
         }
     }
+    note_time(0);
+}
+
+// One warp per CTA.  With a work queue (a.work, the hot path's replays): the
+// CTAs of one resident wave pull set items from a global counter -- the
+// listed heavy sets first, then every other set in order -- and a warp that
+// replays a heavy set marks its SM, so the other warps on that SM stop taking
+// new sets once their current one is done: the longest dependency chains
+// (which bound the launch: one set can carry 3% of the events) keep an SM's
+// issue slots to themselves instead of sharing them with ~20 warps of short
+// sets.  Without a queue: one set per CTA, heavy sets in the first CTAs.
+template <int POLICY, bool CLASS>
+__global__ void __launch_bounds__(32, RECMG_REPLAY_MINB)
+replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int64_t items) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const int nh = a.heavy ? min(__ldg(a.heavy), kHeavySets) : 0;
+    const int32_t my_heavy = lane < nh ? __ldg(a.heavy + 1 + lane) : -1;
+    uint32_t *const work = a.work;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    for (int64_t next = blockIdx.x;;) {
+        int64_t item = next;
+        if (work) {
+            if (*(volatile uint32_t *)(work + 1 + smid) != 0) return;
+            uint32_t it = 0;
+            if (lane == 0) it = atomicAdd(work, 1u);
+            item = __shfl_sync(FULL, it, 0);
+        }
+        if (item >= items) return;
+        next = item + gridDim.x;   // no queue: one item per CTA (grid == items)
+        int64_t set = item;
+        bool heavy_item = false;
+        if (a.heavy) {
+            if (item < kHeavySets) {
+                if (item >= nh) { if (work) continue; return; }
+                set = __shfl_sync(FULL, my_heavy, (int)item);
+                heavy_item = true;
+            } else {
+                set = item - kHeavySets;
+                if (__any_sync(FULL, my_heavy == (int32_t)set)) { if (work) continue; return; }
+            }
+        }
+        if (heavy_item && work && lane == 0) atomicAdd(work + 1 + smid, 1u);
+        replay_one_set<POLICY, CLASS>(a, set, dsm, Wp, hbits, regs, heavy_item);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        if (heavy_item && work && lane == 0) atomicSub(work + 1 + smid, 1u);
+        if (!work) return;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1393,6 +1653,15 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
                   cudaStream_t s) {
     (void)narrow;
     if (nsets <= 0) return RECMG_OK;
+    // RECMG_REPLAY_REGS=0: every set through the shared-memory path (A/B, tests)
+    // sets of <= 32 ways shorter than `regs` events (and not on the heavy list)
+    // replay in registers.  RECMG_REPLAY_REGS=0: none (A/B, tests); =N: below N
+    const char *regs_env = getenv("RECMG_REPLAY_REGS");
+    int regs = 0x7FFFFFFF;
+    if (regs_env && regs_env[0]) {
+        const long v = strtol(regs_env, nullptr, 10);
+        regs = v == 1 ? 0x7FFFFFFF : (int)(v < 0 ? 0 : (v > 0x7FFFFFFF ? 0x7FFFFFFF : v));
+    }
     if (a.W <= kSmemMaxWays) {
         const int Wp = (int)((a.W + 31) / 32 * 32);
         int hbits = 6;
@@ -1400,15 +1669,27 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         const int bytes = kRingSlots * kRingBlk * 4 + 12 * Wp + 8 * (1 << hbits);
         // one warp (one set) per CTA: a few KB of shared memory, so replay
         // CTAs co-reside with other kernels' CTAs (pipelined with the forwards)
-        const int wpc = 1;
-        const size_t smem = (size_t)wpc * bytes;
-        const unsigned grid = (unsigned)((nsets + wpc - 1) / wpc + (a.heavy ? kHeavySets : 0));
+        const size_t smem = (size_t)bytes;
+        const int64_t items = nsets + (a.heavy ? kHeavySets : 0);
+        // RECMG_REPLAY_QUEUE=0: one set per CTA, no SM reservation (A/B)
+        const char *q_env = getenv("RECMG_REPLAY_QUEUE");
+        ReplayArgs aq = a;
+        if (q_env && q_env[0] == '0') aq.work = nullptr;
+        if (aq.work) RECMG_CUDA_TRY(cudaMemsetAsync(aq.work, 0, sizeof(uint32_t) * kWorkWords, s));
 #define RECMG_SMEM_LAUNCH(P, C)                                                            \
     do {                                                                                    \
         RECMG_CUDA_TRY(cudaFuncSetAttribute(replay_smem_kernel<P, C>,                       \
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                             (int)smem));                                    \
-        replay_smem_kernel<P, C><<<grid, 32 * wpc, smem, s>>>(a, wpc, Wp, hbits, bytes);    \
+        unsigned grid = (unsigned)items;                                                    \
+        if (aq.work) {                                                                      \
+            int per_sm = 0;                                                                 \
+            RECMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                   \
+                &per_sm, replay_smem_kernel<P, C>, 32, smem));                              \
+            const int64_t wave = (int64_t)kSmCount * (per_sm > 0 ? per_sm : 1);             \
+            grid = (unsigned)(items < wave ? items : wave);                                 \
+        }                                                                                   \
+        replay_smem_kernel<P, C><<<grid, 32, smem, s>>>(aq, Wp, hbits, regs, items);        \
     } while (0)
         if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, true);
@@ -1451,3 +1732,11 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
 }
 
 }  // namespace recmg
+
+// diagnostic: per-set timing records of the following replay launches
+// ([4 * S] int64 on the device, or null to stop)
+extern "C" int recmg_diag_set_timing(int64_t *dev_buf) {
+    return cudaMemcpyToSymbol(recmg::g_set_timing, &dev_buf, sizeof(dev_buf)) == cudaSuccess
+               ? RECMG_OK
+               : RECMG_E_CUDA;
+}

@@ -60,6 +60,8 @@ struct ReplayArgs {
     int64_t *hits_misses;
     uint8_t *per_access_hit;   // pre-filled with 1 by the caller: kernels write the misses
     const int32_t *next_use;   // OPTGEN: next reference of each access (n if none)
+    int32_t gid_bits;          // bits of the largest gid (0: unknown)
+    uint32_t *work = nullptr;  // [kWorkWords] or null: replay work queue (see replay_smem_kernel)
 };
 
 int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_t nsets,

@@ -48,6 +48,7 @@ _GRAPHS = os.environ.get("RECMG_GRAPHS", "1") == "1"
 # then shares the GPU with the replay) instead of at the start, where its
 # kernels take SMs at the forward launch boundary (config 2: +1.8%).
 _LRU_LATE = os.environ.get("RECMG_LRU_LATE", "1") == "1"
+_LRU_PRIO = os.environ.get("RECMG_LRU_PRIO", "1") == "1"
 
 
 class HotPath:
@@ -145,7 +146,9 @@ class HotPath:
         self.s_copy = torch.cuda.Stream()
         self.cov_host = torch.empty((2, max(self.K_max, 1)), dtype=torch.int16, pin_memory=True)
         self._cov_events = []
-        self.s_lru = torch.cuda.Stream(priority=prio)
+        # the LRU comparator yields the SMs to the replay's own event build and
+        # partition (RECMG_LRU_PRIO=1: the replay stream's priority)
+        self.s_lru = torch.cuda.Stream(priority=prio if _LRU_PRIO else 0)
         self.s_hook = torch.cuda.Stream(priority=prio) if self.hook_snapshot else None
         self._snaps = ([torch.empty_like(self.buffer.state) for _ in range(2)]
                        if self.hook_snapshot else None)

@@ -25,14 +25,23 @@ torch.cuda.synchronize()
 K = hp.K
 g, bits, pf = hp.gids[:n], hp.bits[:K], hp.pf[:K]
 buf = hp.buffer
-ms = []
-for _ in range(9):
-    buf.reset()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    buf.run_chunks(g, 0, K, True, bits, pf, skip_stats=True)
-    e1.record()
-    torch.cuda.synchronize()
-    ms.append(e0.elapsed_time(e1))
-print(f"whole-trace replay (events + partition + replay): {np.median(ms[1:]):.2f} ms")
-print("counters", buf.result(with_coverage=False))
+import os
+for regs, queue in (("0", "0"), ("1", "1"), ("16384", "1"), ("4096", "1")):
+    os.environ["RECMG_REPLAY_REGS"] = regs
+    os.environ["RECMG_REPLAY_QUEUE"] = queue
+    ms, ml = [], []
+    for _ in range(7):
+        buf.reset()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        buf.run_chunks(g, 0, K, True, bits, pf, skip_stats=True)
+        e1.record()
+        hp.lru.reset()
+        hp.lru.run(g)
+        e2.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        ml.append(e1.elapsed_time(e2))
+    print(f"RECMG_REPLAY_REGS={regs} QUEUE={queue}: whole-trace replay (events + partition + replay): "
+          f"{np.median(ms[1:]):.2f} ms, LRU {np.median(ml[1:]):.2f} ms")
+    print("   counters", buf.result(with_coverage=False), "lru", hp.lru.result())
