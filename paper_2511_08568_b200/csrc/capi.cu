@@ -144,6 +144,7 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     ra.W = p.g.W;
     ra.es = cfg->eviction_speed;
     ra.gid_bits = gid_bits_of(cfg->total_ids);
+    ra.total_ids = cfg->total_ids;
     ra.l_in = l_in;
     ra.Ec = p.Ec;
     ra.K = p.K;
@@ -434,6 +435,7 @@ int recmg_simulate_ex(const recmg_buffer_cfg *cfg, void *state, const int32_t *g
     ra.W = g.W;
     ra.es = cfg->eviction_speed;            // SRRIP: max rrpv
     ra.gid_bits = gid_bits_of(cfg->total_ids);
+    ra.total_ids = cfg->total_ids;
     ra.st = state_view(state, cfg, g);
     ra.hits_misses = hits_misses;
     ra.per_access_hit = hit;

@@ -547,7 +547,7 @@ __device__ __forceinline__ void ht_erase(const SetView &v, uint32_t g) {
 // runs, where the shared-memory kernel's hash probing, run grouping
 // (MATCH.ANY) and per-miss hash updates cost ~150 warp instructions per event.
 template <int POLICY, bool CLASS>
-__device__ __forceinline__ void replay_set_regs(const ReplayArgs &a, int64_t set, int64_t lo,
+__device__ __forceinline__ unsigned long long replay_set_regs(const ReplayArgs &a, int64_t set, int64_t lo,
                                                 int64_t hi, EventRing &ring, int lane) {
     constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
     const unsigned FULL = 0xFFFFFFFFu;
@@ -580,7 +580,88 @@ __device__ __forceinline__ void replay_set_regs(const ReplayArgs &a, int64_t set
                 __all_sync(FULL, tag < 0 || clk >= kbase);
     }
 
-    for (int64_t pos = lo; pos < hi; pos += 32) {
+    // Wide step: 128 events (4 per lane) at once while the previous steps saw
+    // no residency-changing miss -- the long sets (Zipf's hot ids: one set can
+    // carry 3% of the events with a miss per ~800) are hit runs, so their cost
+    // is the per-step overhead, which this spreads over 4x the events.  A
+    // window with a miss falls back to the 32-event step below.
+    constexpr int kWide = 4;
+    bool try_wide = true;
+    for (int64_t pos = lo; pos < hi;) {
+        if (try_wide && hi - pos >= 32 * kWide) {
+            ring.ensure(pos - lo, 32 * kWide);
+            uint32_t gq[kWide];
+            unsigned mq[kWide], Sq[kWide], UPq[kWide], U1q[kWide];
+            unsigned missing = 0;
+#pragma unroll
+            for (int q = 0; q < kWide; q++) {
+                const uint32_t e = ring.at(pos - lo + 32 * q + lane);
+                gq[q] = ev_gid(e);
+                const uint32_t ty = ev_type(e);
+                const bool real = gq[q] != kGidMask;
+                Sq[q] = __ballot_sync(FULL, real && ty == EV_SERVE);
+                if (PRIO) {
+                    UPq[q] = __ballot_sync(FULL, real && ty != EV_SERVE);
+                    U1q[q] = __ballot_sync(FULL, real && ty == EV_UPD1);
+                }
+                unsigned m = 0;
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const uint32_t gj = __shfl_sync(FULL, gq[q], j);
+                    if ((uint32_t)tag == gj) m |= 1u << j;
+                }
+                mq[q] = m;
+                const unsigned cand = PRIO ? (Sq[q] | __ballot_sync(FULL, real && ty == EV_PREFETCH))
+                                           : __ballot_sync(FULL, real);
+                missing |= cand & ~__reduce_or_sync(FULL, m);
+            }
+            if (missing == 0) {
+                // the whole window is one hit run: per way, the S count (the
+                // first S takes the prefetch tag) and the last U/P write
+                if (PRIO) {
+                    unsigned nS = 0;
+                    int fS = -1, lU = -1;
+#pragma unroll
+                    for (int q = 0; q < kWide; q++) {
+                        const unsigned sp = mq[q] & Sq[q], up = mq[q] & UPq[q];
+                        nS += __popc(sp);
+                        if (fS < 0 && sp) fS = 32 * q + __ffs(sp) - 1;
+                        if (up) lU = 32 * q + 31 - __clz(up);
+                    }
+                    const bool tagged = (mhi & 1u) && nS;
+                    if (nS) {
+                        if (mhi & 1u) { ph += 1; ch += nS - 1; mhi &= ~1u; }
+                        else ch += nS;
+                    }
+                    if (lU >= 0) {
+                        unsigned u1 = U1q[0];
+#pragma unroll
+                        for (int q = 1; q < kWide; q++) u1 = (lU >> 5) == q ? U1q[q] : u1;
+                        pr = a.es + (int32_t)((u1 >> (lU & 31)) & 1u) + decay;
+                    }
+                    if (CLASS) {
+#pragma unroll
+                        for (int q = 0; q < kWide; q++) {
+                            const unsigned pf = __reduce_or_sync(
+                                FULL, (tagged && (fS >> 5) == q) ? 1u << (fS & 31) : 0u);
+                            if ((Sq[q] >> lane) & 1u)
+                                write_class(a, pos + 32 * q + lane, ((pf >> lane) & 1u) ? 1 : 0);
+                        }
+                    }
+                } else {
+                    int last = -1;
+#pragma unroll
+                    for (int q = 0; q < kWide; q++) {
+                        lhits += __popc(mq[q]);
+                        if (mq[q]) last = 32 * q + 31 - __clz(mq[q]);
+                    }
+                    if (last >= 0) clk = clock_base + pos + last;
+                }
+                pos += 32 * kWide;
+                continue;
+            }
+            try_wide = false;
+        }
         const int nb = (int)imin64(32, hi - pos);
         ring.ensure(pos - lo, nb);
         const uint32_t e = lane < nb ? ring.at(pos - lo + lane) : kGidMask;
@@ -696,6 +777,8 @@ __device__ __forceinline__ void replay_set_regs(const ReplayArgs &a, int64_t set
             start = cut + 1;
             if (start >= nb) break;
         }
+        try_wide = start == 0;   // this step had no miss: try the wide step again
+        pos += nb;
     }
 
     if (is_way) {
@@ -721,6 +804,317 @@ __device__ __forceinline__ void replay_set_regs(const ReplayArgs &a, int64_t set
             if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
         }
     }
+    return od + ins;
+}
+
+// ---------------------------------------------------------------------------
+// Long sets (>= kTableMinEvents events; the hot sets of a Zipf trace are hit
+// runs with one residency-changing miss per ~800 events): the same register
+// ways, but membership from a direct-mapped way map in shared memory --
+// every gid of set s is q * S + s, so wmap[q] (q = gid / S, one byte per id
+// of the set: ceil(total_ids / S) bytes) holds its way or 0xFF -- one LDS per
+// event instead of a 32-step shuffle scan; the hit run is applied per
+// distinct way (a ballot per way the run touches: a handful), 128 events per
+// step while the steps see no miss.
+constexpr int64_t kTableMinEvents = 8192;
+constexpr int kTableMaxBytes = 4096;
+
+__device__ __forceinline__ uint32_t div_set(uint32_t g, uint32_t S, uint32_t M) {
+    uint32_t q = __umulhi(g, M);   // M = ceil(2^32 / S): q is floor(g / S) or one more
+    return q * S > g ? q - 1 : q;
+}
+
+template <int POLICY, bool CLASS>
+__device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs &a, int64_t set,
+                                                               int64_t lo, int64_t hi,
+                                                               EventRing &ring, uint8_t *wmap,
+                                                               int lane) {
+    constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
+    constexpr int kNone = 0xFF;
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int W = (int)a.W;
+    const uint32_t S = (uint32_t)a.S, M = a.smagic;
+    const int64_t sbase = set * a.W;
+    const bool is_way = lane < W;
+    int32_t tag = is_way ? a.st.tags[sbase + lane] : -2;
+    const int64_t m0 = is_way ? a.st.meta[sbase + lane] : 0;
+    int32_t pr = (int32_t)(m0 & 0xFFFFFFFF);
+    uint32_t mhi = (uint32_t)((uint64_t)m0 >> 32);
+    int64_t clk = m0;
+    int count = __popc(__ballot_sync(FULL, tag >= 0));
+    const int64_t clock_base = a.st.header[0];
+    int32_t decay = 0;
+    unsigned long long ch = 0, ph = 0, od = 0, nev = 0, ins = 0, lhits = 0;
+    const int gb = a.gid_bits;
+    const int64_t kbase = clock_base - 0x80000000ll;
+    bool key32;
+    if (PRIO) {
+        const int32_t lim = gb > 0 && gb <= 28 ? (1 << (32 - gb)) - 1 : 0;
+        key32 = a.es + 1 < lim && __all_sync(FULL, tag < 0 || pr < lim);
+    } else {
+        key32 = hi - lo < 0x7FFFFFFFll && clock_base + hi - kbase < 0xFFFFFFFFll &&
+                __all_sync(FULL, tag < 0 || clk >= kbase);
+    }
+    for (int i = lane * 16; i < a.qn; i += 32 * 16)
+        *reinterpret_cast<uint4 *>(wmap + i) = make_uint4(~0u, ~0u, ~0u, ~0u);
+    __syncwarp();
+    if (tag >= 0) wmap[div_set((uint32_t)tag, S, M)] = (uint8_t)lane;
+    __syncwarp();
+
+    // applies one way's share of a hit run (the events in m) -- called by the
+    // way's lane; returns the event (bit) whose S took the prefetch tag
+    auto apply_way = [&](unsigned m, unsigned Sm, unsigned UPm, unsigned U1m, int64_t base)
+        -> unsigned {
+        unsigned took = 0;
+        if (PRIO) {
+            const unsigned sp = m & Sm, up = m & UPm;
+            if (sp) {
+                const unsigned c = __popc(sp);
+                if (mhi & 1u) { ph += 1; ch += c - 1; mhi &= ~1u; took = sp & (0u - sp); }
+                else ch += c;
+            }
+            if (up) {
+                const int last = 31 - __clz(up);
+                pr = a.es + (int32_t)((U1m >> last) & 1u) + decay;
+            }
+        } else if (m) {
+            lhits += __popc(m);
+            clk = clock_base + base + (31 - __clz(m));
+        }
+        return took;
+    };
+
+    // 128-event windows, 4 events per lane in registers (lane j of part q holds
+    // event 32 q + j), loaded one window ahead straight from the partitioned
+    // segment (coalesced; L2 prefetch 8 windows ahead); past the segment end
+    // the slots hold kGidMask, an event that is no event
+    constexpr int kWide = 4, kWin = 32 * kWide;
+    const uint32_t *seg = a.ev + lo;
+    const int64_t len = hi - lo;
+    uint32_t nxt[kWide];
+#pragma unroll
+    for (int q = 0; q < kWide; q++) {
+        const int64_t i = 32 * q + lane;
+        nxt[q] = i < len ? __ldcs(seg + i) : kGidMask;
+    }
+    for (int64_t wp = 0; wp < len; wp += kWin) {
+        uint32_t cur[kWide];
+#pragma unroll
+        for (int q = 0; q < kWide; q++) {
+            cur[q] = nxt[q];
+            const int64_t i = wp + kWin + 32 * q + lane;
+            nxt[q] = i < len ? __ldcs(seg + i) : kGidMask;
+        }
+        if (lane < 4 && wp + 8 * kWin + 32 * lane < len)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(seg + wp + 8 * kWin + 32 * lane));
+        const int64_t pos = lo + wp;
+        int wq[kWide];
+        unsigned Sq[kWide], UPq[kWide], U1q[kWide], Hq[kWide], Cq[kWide];
+        unsigned missing = 0;
+#pragma unroll
+        for (int q = 0; q < kWide; q++) {
+            const uint32_t g = ev_gid(cur[q]), ty = ev_type(cur[q]);
+            const bool real = g != kGidMask;
+            wq[q] = real ? wmap[div_set(g, S, M)] : kNone;
+            Sq[q] = __ballot_sync(FULL, real && ty == EV_SERVE);
+            if (PRIO) {
+                UPq[q] = __ballot_sync(FULL, real && ty != EV_SERVE);
+                U1q[q] = __ballot_sync(FULL, real && ty == EV_UPD1);
+            }
+            Hq[q] = __ballot_sync(FULL, wq[q] != kNone);
+            Cq[q] = PRIO ? (Sq[q] | __ballot_sync(FULL, real && ty == EV_PREFETCH))
+                         : __ballot_sync(FULL, real);
+            missing |= Cq[q] & ~Hq[q];
+        }
+        if (missing == 0) {
+            // one hit run of 128 events: per distinct way, S count (the first S
+            // takes the tag), last U/P write [LRU: last hit]
+            unsigned pend[kWide], took[kWide];
+#pragma unroll
+            for (int q = 0; q < kWide; q++) { pend[q] = Hq[q]; took[q] = 0; }
+            while (pend[0] | pend[1] | pend[2] | pend[3]) {
+                const int q0 = pend[0] ? 0 : (pend[1] ? 1 : (pend[2] ? 2 : 3));
+                const unsigned pq = q0 == 0 ? pend[0] : (q0 == 1 ? pend[1] : (q0 == 2 ? pend[2] : pend[3]));
+                const int wsrc = q0 == 0 ? wq[0] : (q0 == 1 ? wq[1] : (q0 == 2 ? wq[2] : wq[3]));
+                const int wv = __shfl_sync(FULL, wsrc, __ffs(pq) - 1);
+                unsigned mm[kWide];
+#pragma unroll
+                for (int q = 0; q < kWide; q++) {
+                    mm[q] = __ballot_sync(FULL, wq[q] == wv);
+                    pend[q] &= ~mm[q];
+                }
+                if (lane == wv) {
+                    if (PRIO) {
+                        unsigned nS = 0, u1 = 0;
+                        int fS = -1, lU = -1;
+#pragma unroll
+                        for (int q = 0; q < kWide; q++) {
+                            const unsigned sp = mm[q] & Sq[q], up = mm[q] & UPq[q];
+                            nS += __popc(sp);
+                            if (fS < 0 && sp) fS = 32 * q + __ffs(sp) - 1;
+                            if (up) { lU = 32 * q + 31 - __clz(up); u1 = U1q[q]; }
+                        }
+                        if (nS) {
+                            if (mhi & 1u) {
+                                ph += 1; ch += nS - 1; mhi &= ~1u;
+#pragma unroll
+                                for (int q = 0; q < kWide; q++)
+                                    if ((fS >> 5) == q) took[q] = 1u << (fS & 31);
+                            } else {
+                                ch += nS;
+                            }
+                        }
+                        if (lU >= 0) pr = a.es + (int32_t)((u1 >> (lU & 31)) & 1u) + decay;
+                    } else {
+                        int last = -1;
+#pragma unroll
+                        for (int q = 0; q < kWide; q++) {
+                            lhits += __popc(mm[q]);
+                            if (mm[q]) last = 32 * q + 31 - __clz(mm[q]);
+                        }
+                        clk = clock_base + pos + last;
+                    }
+                }
+            }
+            if (PRIO && CLASS) {
+#pragma unroll
+                for (int q = 0; q < kWide; q++) {
+                    const unsigned pf = __reduce_or_sync(FULL, took[q]);
+                    if ((Sq[q] >> lane) & 1u)
+                        write_class(a, pos + 32 * q + lane, ((pf >> lane) & 1u) ? 1 : 0);
+                }
+            }
+            continue;
+        }
+        // a miss in the window: its 4 parts in order, misses resolved one by one
+#pragma unroll 1
+        for (int q = 0; q < kWide; q++) {
+            const uint32_t e = q == 0 ? cur[0] : (q == 1 ? cur[1] : (q == 2 ? cur[2] : cur[3]));
+            const uint32_t g = ev_gid(e);
+            const bool real = g != kGidMask;
+            const int64_t base = pos + 32 * q;
+            const unsigned Sm = q == 0 ? Sq[0] : (q == 1 ? Sq[1] : (q == 2 ? Sq[2] : Sq[3]));
+            const unsigned cand = q == 0 ? Cq[0] : (q == 1 ? Cq[1] : (q == 2 ? Cq[2] : Cq[3]));
+            unsigned UPm = 0, U1m = 0;
+            if (PRIO) {
+                UPm = q == 0 ? UPq[0] : (q == 1 ? UPq[1] : (q == 2 ? UPq[2] : UPq[3]));
+                U1m = q == 0 ? U1q[0] : (q == 1 ? U1q[1] : (q == 2 ? U1q[2] : U1q[3]));
+            }
+            int w = real ? wmap[div_set(g, S, M)] : kNone;   // after the earlier parts' misses
+            unsigned hit = __ballot_sync(FULL, w != kNone);
+            int start = 0;
+            for (;;) {
+                const unsigned from = start >= 32 ? 0u : ~0u << start;
+                const unsigned miss = cand & ~hit & from;
+                const int cut = miss ? __ffs(miss) - 1 : 32;
+                const unsigned R = (cut >= 32 ? ~0u : ((1u << cut) - 1u)) & from;
+                unsigned pend = hit & R, took = 0;
+                while (pend) {
+                    const int wv = __shfl_sync(FULL, w, __ffs(pend) - 1);
+                    const unsigned mm = __ballot_sync(FULL, w == wv) & R;
+                    pend &= ~mm;
+                    if (lane == wv) took = apply_way(mm, Sm, UPm, U1m, base);
+                }
+                if (PRIO && CLASS) {
+                    const unsigned pf = __reduce_or_sync(FULL, took);
+                    if ((R & Sm) >> lane & 1u) write_class(a, base + lane, (pf >> lane & 1u) ? 1 : 0);
+                }
+                if (cut >= 32) break;
+                const uint32_t gc = __shfl_sync(FULL, g, cut);
+                const bool isS = (Sm >> cut) & 1u;
+                if (PRIO) {
+                    if (isS) {
+                        od++;
+                        if (CLASS && lane == 0) write_class(a, base + cut, 2);
+                    } else {
+                        ins++;
+                    }
+                } else {
+                    od++;
+                    if (a.per_access_hit && lane == 0)
+                        a.per_access_hit[a.vals ? a.vals[base + cut] : base + cut] = 0;
+                }
+                int target;
+                const bool full = count >= W;
+                if (full && key32) {
+                    unsigned key;
+                    if (PRIO) {
+                        const int32_t pe = pr - decay;
+                        key = tag >= 0 ? ((unsigned)(pe > 0 ? pe : 0) << gb) | (unsigned)tag : ~0u;
+                    } else {
+                        key = tag >= 0 ? (unsigned)(clk - kbase) : ~0u;
+                    }
+                    const unsigned kmin = __reduce_min_sync(FULL, key);
+                    target = __ffs(__ballot_sync(FULL, key == kmin)) - 1;
+                } else if (full) {
+                    unsigned khi, klo;
+                    if (PRIO) {
+                        const int32_t pe = pr - decay;
+                        khi = tag >= 0 ? (unsigned)(pe > 0 ? pe : 0) : ~0u;
+                        klo = (unsigned)tag;
+                    } else {
+                        khi = tag >= 0 ? (unsigned)((uint64_t)clk >> 32) : ~0u;
+                        klo = (unsigned)clk;
+                    }
+                    const unsigned hmin = __reduce_min_sync(FULL, khi);
+                    const unsigned lmin = __reduce_min_sync(FULL, khi == hmin ? klo : ~0u);
+                    target = __ffs(__ballot_sync(FULL, khi == hmin && klo == lmin)) - 1;
+                } else {
+                    target = __ffs(__ballot_sync(FULL, tag == -1)) - 1;
+                }
+                const int32_t evicted = __shfl_sync(FULL, tag, target);   // -1: a free way
+                if (full) {
+                    if (PRIO) decay++;
+                    nev++;
+                    count--;
+                }
+                if (lane == target) {
+                    tag = (int32_t)gc;
+                    if (PRIO) {
+                        pr = a.es + decay;
+                        mhi = isS ? 0u : 1u;
+                    } else {
+                        clk = clock_base + base + cut;
+                    }
+                }
+                if (lane == 0) {
+                    if (evicted >= 0) wmap[div_set((uint32_t)evicted, S, M)] = (uint8_t)kNone;
+                    wmap[div_set(gc, S, M)] = (uint8_t)target;
+                }
+                __syncwarp();
+                if (w == target) w = kNone;        // the evicted gid's events now miss
+                if (real && g == gc) w = target;   // the inserted gid's events hit
+                count++;
+                hit = __ballot_sync(FULL, w != kNone);
+                start = cut + 1;
+            }
+        }
+    }
+
+    if (is_way) {
+        a.st.tags[sbase + lane] = tag;
+        int64_t m;
+        if (PRIO) {
+            const int32_t pe = pr - decay;
+            m = (int64_t)((uint64_t)mhi << 32) | (int64_t)(uint32_t)(pe > 0 ? pe : 0);
+        } else {
+            m = clk;
+        }
+        a.st.meta[sbase + lane] = m;
+    }
+    if (lane == 0) a.st.count[set] = count;
+    if (PRIO) {
+        ch = __reduce_add_sync(FULL, (unsigned)ch);
+        ph = __reduce_add_sync(FULL, (unsigned)ph);
+        if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
+    } else {
+        lhits = __reduce_add_sync(FULL, (unsigned)lhits);
+        if (lane == 0 && a.hits_misses) {
+            if (lhits) atomicAdd((unsigned long long *)&a.hits_misses[0], lhits);
+            if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
+        }
+    }
+    return od + ins;
 }
 
 // Diagnostic (scripts/replay_set_timeline.py): when set, every replay_smem_kernel
@@ -732,7 +1126,8 @@ __device__ int64_t *g_set_timing = nullptr;
 #endif
 template <int POLICY, bool CLASS>
 __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set, uint8_t *base,
-                                               int Wp, int hbits, int regs, bool heavy_item) {
+                                               int Wp, int hbits, int regs, int tables,
+                                               bool heavy_item) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     if (set >= a.S) return;
@@ -751,7 +1146,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
     int64_t *const timing = g_set_timing;
     uint64_t t_start = 0;
     if (timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    auto note_time = [&](int path) {
+    auto note_time = [&](int path, unsigned long long misses) {
         if (timing && lane == 0) {
             uint64_t t_end;
             uint32_t sm;
@@ -761,7 +1156,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
             r[0] = (int64_t)t_start;
             r[1] = (int64_t)t_end;
             r[2] = (int64_t)sm | ((int64_t)path << 32);
-            r[3] = hi - lo;
+            r[3] = (hi - lo) | ((int64_t)misses << 32);
         }
     };
     EventRing ring;
@@ -769,9 +1164,15 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
     if constexpr (POLICY == RECMG_POLICY_PRIORITY || POLICY == RECMG_POLICY_LRU) {
         // every set but the listed heavy ones (their long uniform runs take the
         // fast path below) replays with its ways in registers
-        if (W <= 32 && !heavy_item && hi - lo < (int64_t)regs) {
-            replay_set_regs<POLICY, CLASS>(a, set, lo, hi, ring, lane);
-            note_time(1);
+        if (W <= 32 && (!heavy_item || regs < 0) && hi - lo < (int64_t)(regs < 0 ? 0x7FFFFFFF : regs)) {
+            if (a.qn > 0 && hi - lo >= kTableMinEvents && tables) {
+                const unsigned long long m = replay_set_table<POLICY, CLASS>(
+                    a, set, lo, hi, ring, base + kRingSlots * kRingBlk * 4, lane);
+                note_time(2, m);
+                return;
+            }
+            const unsigned long long m = replay_set_regs<POLICY, CLASS>(a, set, lo, hi, ring, lane);
+            note_time(1, m);
             return;
         }
     }
@@ -1190,7 +1591,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
             if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
         }
     }
-    note_time(0);
+    note_time(0, od + ins);
 }
 
 // One warp per CTA.  With a work queue (a.work, the hot path's replays): the
@@ -1203,7 +1604,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
 // sets.  Without a queue: one set per CTA, heavy sets in the first CTAs.
 template <int POLICY, bool CLASS>
 __global__ void __launch_bounds__(32, RECMG_REPLAY_MINB)
-replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int64_t items) {
+replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int tables, int64_t items) {
     extern __shared__ __align__(16) uint8_t dsm[];
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
@@ -1235,7 +1636,7 @@ replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int64_t items) {
             }
         }
         if (heavy_item && work && lane == 0) atomicAdd(work + 1 + smid, 1u);
-        replay_one_set<POLICY, CLASS>(a, set, dsm, Wp, hbits, regs, heavy_item);
+        replay_one_set<POLICY, CLASS>(a, set, dsm, Wp, hbits, regs, tables, heavy_item);
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         if (heavy_item && work && lane == 0) atomicSub(work + 1 + smid, 1u);
@@ -1654,26 +2055,45 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
     (void)narrow;
     if (nsets <= 0) return RECMG_OK;
     // RECMG_REPLAY_REGS=0: every set through the shared-memory path (A/B, tests)
-    // sets of <= 32 ways shorter than `regs` events (and not on the heavy list)
-    // replay in registers.  RECMG_REPLAY_REGS=0: none (A/B, tests); =N: below N
+    // sets of <= 32 ways replay in registers (replay_set_regs).  A/B and tests:
+    // RECMG_REPLAY_REGS=0: none; =1: all but the heavy list; =N > 1: sets
+    // shorter than N events, heavy ones excluded; unset or -1: all
     const char *regs_env = getenv("RECMG_REPLAY_REGS");
-    int regs = 0x7FFFFFFF;
+    int regs = -1;
     if (regs_env && regs_env[0]) {
         const long v = strtol(regs_env, nullptr, 10);
-        regs = v == 1 ? 0x7FFFFFFF : (int)(v < 0 ? 0 : (v > 0x7FFFFFFF ? 0x7FFFFFFF : v));
+        regs = v == 1 ? 0x7FFFFFFF : (int)(v < -1 ? 0 : (v > 0x7FFFFFFF ? 0x7FFFFFFF : v));
     }
     if (a.W <= kSmemMaxWays) {
         const int Wp = (int)((a.W + 31) / 32 * 32);
         int hbits = 6;
         while ((1 << hbits) < (Wp <= 256 ? 4 * Wp : 2 * Wp)) hbits++;
-        const int bytes = kRingSlots * kRingBlk * 4 + 12 * Wp + 8 * (1 << hbits);
+        int bytes = kRingSlots * kRingBlk * 4 + 12 * Wp + 8 * (1 << hbits);
+        // long sets of <= 32 ways: a direct-mapped way map after the ring
+        // (replay_set_table); RECMG_REPLAY_TABLES=0 disables it
+        const char *t_env = getenv("RECMG_REPLAY_TABLES");
+        const int tables = (t_env && t_env[0] == '0') ? 0 : 1;
+        ReplayArgs at = a;
+        at.qn = 0;
+        if (a.W <= 32 && a.S > 1 && a.total_ids > 0) {
+            const int64_t qn = (a.total_ids + a.S - 1) / a.S;
+            if (qn <= kTableMaxBytes) {
+                at.qn = (int32_t)((qn + 15) / 16 * 16);
+                at.smagic = set_magic((uint32_t)a.S);
+                const int need = kRingSlots * kRingBlk * 4 + at.qn;
+                bytes = bytes > need ? bytes : need;
+            }
+        }
         // one warp (one set) per CTA: a few KB of shared memory, so replay
         // CTAs co-reside with other kernels' CTAs (pipelined with the forwards)
         const size_t smem = (size_t)bytes;
-        const int64_t items = nsets + (a.heavy ? kHeavySets : 0);
+        int64_t items = nsets + (a.heavy ? kHeavySets : 0);
+        // diagnostic: RECMG_REPLAY_ONLY_HEAVY=1 replays the heavy list alone
+        const char *h_env = getenv("RECMG_REPLAY_ONLY_HEAVY");
+        if (h_env && h_env[0] == '1' && a.heavy) items = kHeavySets;
         // RECMG_REPLAY_QUEUE=0: one set per CTA, no SM reservation (A/B)
         const char *q_env = getenv("RECMG_REPLAY_QUEUE");
-        ReplayArgs aq = a;
+        ReplayArgs aq = at;
         if (q_env && q_env[0] == '0') aq.work = nullptr;
         if (aq.work) RECMG_CUDA_TRY(cudaMemsetAsync(aq.work, 0, sizeof(uint32_t) * kWorkWords, s));
 #define RECMG_SMEM_LAUNCH(P, C)                                                            \
@@ -1689,7 +2109,7 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
             const int64_t wave = (int64_t)kSmCount * (per_sm > 0 ? per_sm : 1);             \
             grid = (unsigned)(items < wave ? items : wave);                                 \
         }                                                                                   \
-        replay_smem_kernel<P, C><<<grid, 32, smem, s>>>(aq, Wp, hbits, regs, items);        \
+        replay_smem_kernel<P, C><<<grid, 32, smem, s>>>(aq, Wp, hbits, regs, tables, items);\
     } while (0)
         if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, true);

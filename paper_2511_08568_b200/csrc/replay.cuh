@@ -61,6 +61,9 @@ struct ReplayArgs {
     uint8_t *per_access_hit;   // pre-filled with 1 by the caller: kernels write the misses
     const int32_t *next_use;   // OPTGEN: next reference of each access (n if none)
     int32_t gid_bits;          // bits of the largest gid (0: unknown)
+    int64_t total_ids;         // ids of the trace (0: unknown)
+    int32_t qn;                // way-map bytes per set (0: no way map), set by launch_replay
+    uint32_t smagic;           // ceil(2^32 / S)
     uint32_t *work = nullptr;  // [kWorkWords] or null: replay work queue (see replay_smem_kernel)
 };
 

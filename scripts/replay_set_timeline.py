@@ -38,7 +38,7 @@ rec = torch.zeros(4 * S, dtype=torch.int64, device="cuda")
 
 def report(name, r):
     r = r.reshape(S, 4)
-    st, en, path, ln = r[:, 0], r[:, 1], r[:, 2] >> 32, r[:, 3]
+    st, en, path, ln, ms = r[:, 0], r[:, 1], r[:, 2] >> 32, r[:, 3] & 0xFFFFFFFF, r[:, 3] >> 32
     ok = en > 0
     t0 = st[ok].min()
     span = (en[ok].max() - t0) / 1e6
@@ -46,7 +46,8 @@ def report(name, r):
     last = np.argsort(-en)[:5]
     for s_ in last:
         print(f"   set {s_:6d} path {path[s_]} len {ln[s_]:8d} start {(st[s_]-t0)/1e6:7.3f} "
-              f"dur {(en[s_]-st[s_])/1e6:7.3f} ms  {(en[s_]-st[s_])/max(ln[s_],1):6.1f} ns/ev")
+              f"dur {(en[s_]-st[s_])/1e6:7.3f} ms  {(en[s_]-st[s_])/max(ln[s_],1):6.1f} ns/ev, "
+              f"misses {ms[s_]} ({ms[s_]/max(ln[s_],1):.2f}/ev)")
     for p_ in (0, 1):
         for lo_, hi_ in ((0, 2048), (2048, 8192), (8192, 32768), (32768, 1 << 40)):
             m = ok & (path == p_) & (ln >= lo_) & (ln < hi_)
@@ -56,7 +57,7 @@ def report(name, r):
                       f"{d.sum() / ln[m].sum():6.1f} ns/event, max dur {d.max() / 1e6:.3f} ms")
 
 
-for regs, queue in (("0", "0"), ("1", "1"), ("16384", "1"), ("4096", "1")):
+for regs, queue in (("0", "1"), ("1", "1"), ("-1", "1")):
     os.environ["RECMG_REPLAY_REGS"] = regs
     os.environ["RECMG_REPLAY_QUEUE"] = queue
     for _ in range(2):

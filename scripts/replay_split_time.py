@@ -18,7 +18,8 @@ C32 = C - C % 32
 cp, ec = init_params_device("caching", t.table_sizes, dim=64, seed=0, init_scale=0.4)
 pp, ep = init_params_device("prefetch", t.table_sizes, dim=64, seed=1, init_scale=0.4)
 n = len(t)
-hp = HotPath(DeviceModel(cp, ec), DeviceModel(pp, ep), t.table_sizes, C32, n, ways=32)
+hp = HotPath(DeviceModel(cp, ec), DeviceModel(pp, ep), t.table_sizes, C32, n, ways=32,
+             lru_capacity=C32)
 hp.gids[:n].copy_(torch.from_numpy(t.gid_array.astype(np.int32)))
 hp.launch(n)
 torch.cuda.synchronize()
@@ -26,7 +27,7 @@ K = hp.K
 g, bits, pf = hp.gids[:n], hp.bits[:K], hp.pf[:K]
 buf = hp.buffer
 import os
-for regs, queue in (("0", "0"), ("1", "1"), ("16384", "1"), ("4096", "1")):
+for regs, queue in (("0", "1"), ("1", "1"), ("-1", "1")):
     os.environ["RECMG_REPLAY_REGS"] = regs
     os.environ["RECMG_REPLAY_QUEUE"] = queue
     ms, ml = [], []

@@ -27,7 +27,8 @@ class _regs:
 
     def __enter__(self):
         self.old = os.environ.get("RECMG_REPLAY_REGS")
-        os.environ["RECMG_REPLAY_REGS"] = "1" if self.on else "0"
+        os.environ["RECMG_REPLAY_REGS"] = self.on if isinstance(self.on, str) else (
+            "-1" if self.on else "0")
 
     def __exit__(self, *exc):
         if self.old is None:
@@ -57,7 +58,8 @@ def _workload(seed, V, n):
     # key, so the two-word argmin runs
     (4, 1 << 25, 400_000, 32, 60, 130),
 ])
-def test_priority_replay_regs_vs_oracle_and_smem(seed, V, n, ways, sets, es):
+@pytest.mark.parametrize("mode", ["-1", "1"])
+def test_priority_replay_regs_vs_oracle_and_smem(seed, V, n, ways, sets, es, mode):
     gids, bits, pf = _workload(seed, V, n)
     t = rb.trace_from_gids(gids, [V])
     cap = ways * sets
@@ -65,7 +67,7 @@ def test_priority_replay_regs_vs_oracle_and_smem(seed, V, n, ways, sets, es):
     kw = dict(caching_fn=lambda s: bits[s.origin // 15],
               prefetch_fn=lambda s: [int(g) for g in pf[s.origin // 15] if g >= 0],
               return_access_class=True)
-    with _regs(True):
+    with _regs(mode):
         rep, cls = rb.replay(t, cfg, **kw)
     with _regs(False):
         rep0, cls0 = rb.replay(t, cfg, **kw)
