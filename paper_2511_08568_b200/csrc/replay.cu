@@ -2055,11 +2055,14 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
     (void)narrow;
     if (nsets <= 0) return RECMG_OK;
     // RECMG_REPLAY_REGS=0: every set through the shared-memory path (A/B, tests)
-    // sets of <= 32 ways replay in registers (replay_set_regs).  A/B and tests:
-    // RECMG_REPLAY_REGS=0: none; =1: all but the heavy list; =N > 1: sets
-    // shorter than N events, heavy ones excluded; unset or -1: all
+    // sets of <= 32 ways replay in registers (replay_set_regs / _table).  A/B
+    // and tests: RECMG_REPLAY_REGS=0: none; =1: all but the heavy list; =N > 1:
+    // sets shorter than N events, heavy ones excluded; -1: all.  Default: all
+    // for the priority buffer; the LRU's heavy sets stay on the shared-memory
+    // path, whose uniform-run step takes their long single-id runs in O(1)
+    // (config 2 hot set: 3.3 vs 4.4 ns/event)
     const char *regs_env = getenv("RECMG_REPLAY_REGS");
-    int regs = -1;
+    int regs = policy == RECMG_POLICY_PRIORITY ? -1 : 0x7FFFFFFF;
     if (regs_env && regs_env[0]) {
         const long v = strtol(regs_env, nullptr, 10);
         regs = v == 1 ? 0x7FFFFFFF : (int)(v < -1 ? 0 : (v > 0x7FFFFFFF ? 0x7FFFFFFF : v));
