@@ -680,13 +680,15 @@ def main():
                                             prefetch_transcendentals(15, 5, args.dim) * K,
                                             prof.get("prefetch_fwd", {}), args.pieces),
                 "replay": {"ms": mean["replay"], "gbs": (ev_n * 4 + n) / (mean["replay"] / 1e3) / 1e9,
-                           "bound": "not HBM (7.33 B/access algorithmic): instruction issue on "
-                                    "the ordinary sets' hit-run / miss path (ncu r02e: 60% issue "
-                                    "active at 24 warps/SM); the hot set's serial chain alone is "
-                                    "about half the kernel (DESIGN.md 'Schedule')",
-                           "overlapped": args.pieces > 1},
-                "lru": {"ms": mean["lru"], "gbs": (n * 5) / (mean["lru"] / 1e3) / 1e9,
-                        "overlapped": True}}}
+                           "bound": "not HBM (7.33 B/access algorithmic): the dependency chains "
+                                    "of the few hot sets (one carries 3% of the events; ~6 ns per "
+                                    "event on the register-window path, DESIGN.md 'Schedule')",
+                           "overlapped": args.pieces > 1,
+                           "lru_fused": bool(getattr(hp, "_lru_fused", False))},
+                "lru": ({"ms": mean["lru"], "gbs": (n * 5) / (mean["lru"] / 1e3) / 1e9,
+                         "overlapped": True} if mean["lru"] > 0 else
+                        {"fused_into": "replay", "note": "recmg_replay_chunks_lru: the LRU "
+                         "comparator runs in the replay launch on the same partitioned events"})}}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

@@ -143,6 +143,22 @@ int recmg_replay_chunks_ex(const recmg_buffer_cfg *cfg, void *state, const int32
                            const int32_t *pf, int32_t pf_stride, recmg_counters *counters,
                            uint16_t *cov_num, uint16_t *cov_den, uint8_t *access_class,
                            void *ws, size_t ws_bytes, int32_t flags, void *stream);
+/* recmg_replay_chunks_ex with the 32-way LRU comparator (cache_sim.py:92-106,
+ * simulate() over the same accesses) fused into the same launch: it replays
+ * the serves of the priority replay's own partitioned events (both buffers
+ * have the same sets), so it needs no event build or partition of its own.
+ * lru_cfg: policy RECMG_POLICY_LRU, the same sets, ways (<= 32) and total_ids
+ * as cfg; lru_state its state (recmg_buffer_reset), lru_hits_misses [2] int64
+ * accumulates (hits, misses) like recmg_simulate_ex's.  No access classes.
+ * RECMG_E_INVALID_CONFIG when the geometries differ (run recmg_simulate_ex). */
+int recmg_replay_chunks_lru(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids,
+                            int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio,
+                            int64_t k_begin, int64_t k_end, int32_t with_tail,
+                            const uint8_t *bits, const int32_t *pf, int32_t pf_stride,
+                            recmg_counters *counters, uint16_t *cov_num, uint16_t *cov_den,
+                            const recmg_buffer_cfg *lru_cfg, void *lru_state,
+                            int64_t *lru_hits_misses, void *ws, size_t ws_bytes, int32_t flags,
+                            void *stream);
 /* The prefetch statistics of chunks [k_begin, k_end) alone: they depend only
  * on the ids and the decoded prefetch ids (runtime.py:271-276), not on the
  * buffer, so they can run as soon as the prefetch forward is done.          */

@@ -113,6 +113,9 @@ def lib():
         "recmg_replay_chunks_ex": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64,
                                                   i32, vp, vp, i32, vp, vp, vp, vp, vp, sz, i32,
                                                   vp]),
+        "recmg_replay_chunks_lru": (ctypes.c_int, [cfgp, vp, vp, i64, i32, i32, i32, i64, i64,
+                                                   i32, vp, vp, i32, vp, vp, vp, cfgp, vp, vp,
+                                                   vp, sz, i32, vp]),
         "recmg_prefetch_stats": (ctypes.c_int, [vp, i64, i32, i32, i32, i64, i64, vp, i32, vp,
                                                 vp, vp, vp]),
         "recmg_set_model_sm_budget": (ctypes.c_int, [ctypes.c_int]),
@@ -148,6 +151,8 @@ def lib():
                                                ctypes.c_int, vp]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("RECMG_LIB") and not hasattr(L, name):
+            continue   # an older A/B build without this entry point
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

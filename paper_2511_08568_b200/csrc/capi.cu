@@ -87,7 +87,8 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
                  int64_t k_end, int with_tail, const uint8_t *bits, const int32_t *pf,
                  int32_t pf_stride, recmg_counters *counters, uint16_t *cov_num,
                  uint16_t *cov_den, uint8_t *access_class, void *ws, size_t ws_bytes,
-                 cudaStream_t s, int32_t flags = 0) {
+                 cudaStream_t s, int32_t flags = 0, const recmg_buffer_cfg *lru_cfg = nullptr,
+                 void *lru_state = nullptr, int64_t *lru_hm = nullptr) {
     if (!pf) pf_stride = 0;
     ChainTimer tm(s);
     (void)tm;
@@ -152,9 +153,39 @@ int replay_range(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids, 
     ra.st = st;
     ra.ctr = counters;
     ra.access_class = access_class;
-    int rc = launch_replay(cfg->policy, !p.g.wide, access_class != nullptr, ra, p.g.S, s);
+    // the LRU comparator fused in (recmg_replay_chunks_lru): the same sets, its
+    // own state, the serves of these events; hits = accesses - misses
+    ReplayArgs rl;
+    const ReplayArgs *lru2 = nullptr;
+    if (lru_cfg) {
+        Geometry gl;
+        if (!geometry_of(lru_cfg, &gl) || lru_cfg->policy != RECMG_POLICY_LRU || !lru_state ||
+            !lru_hm || gl.S != p.g.S || gl.W != p.g.W || p.g.wide || p.g.W > 32 || p.g.S < 2 ||
+            cfg->policy != RECMG_POLICY_PRIORITY || lru_cfg->total_ids != cfg->total_ids)
+            return RECMG_E_INVALID_CONFIG;
+        rl = ra;
+        rl.st = state_view(lru_state, lru_cfg, gl);
+        rl.ctr = nullptr;
+        rl.access_class = nullptr;
+        rl.per_access_hit = nullptr;
+        rl.next_use = nullptr;
+        rl.hits_misses = lru_hm;
+        rl.es = lru_cfg->eviction_speed;
+        rl.serve_only = 1;
+        lru2 = &rl;
+        const int64_t n_acc = p.nk * l_in + (p.tail ? n - p.K * l_in : 0);
+        add_i64_kernel<<<1, 1, 0, s>>>(lru_hm, n_acc);
+        RECMG_LAUNCH_CHECK();
+    }
+    int rc = launch_replay(cfg->policy, !p.g.wide, access_class != nullptr, ra, p.g.S, s, lru2);
     if (rc) return rc;
     RECMG_LAP("replay");
+    if (lru2) {
+        // the comparator's clocks are event positions of this call: keep them
+        // monotonic across calls
+        clock_bump_kernel<<<1, 1, 0, s>>>(rl.st.header, p.E);
+        RECMG_LAUNCH_CHECK();
+    }
     if (cfg->policy == RECMG_POLICY_LRU_PF) {
         // clocks are event positions of this call: keep them monotonic across calls
         clock_bump_kernel<<<1, 1, 0, s>>>(st.header, p.E);
@@ -254,6 +285,21 @@ int recmg_replay_chunks_ex(const recmg_buffer_cfg *cfg, void *state, const int32
     return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, k_begin, k_end,
                         with_tail, bits, pf, pf_stride, counters, cov_num, cov_den,
                         access_class, ws, ws_bytes, as_stream(stream), flags);
+}
+
+int recmg_replay_chunks_lru(const recmg_buffer_cfg *cfg, void *state, const int32_t *gids,
+                            int64_t n, int32_t l_in, int32_t l_out, int32_t window_ratio,
+                            int64_t k_begin, int64_t k_end, int32_t with_tail,
+                            const uint8_t *bits, const int32_t *pf, int32_t pf_stride,
+                            recmg_counters *counters, uint16_t *cov_num, uint16_t *cov_den,
+                            const recmg_buffer_cfg *lru_cfg, void *lru_state,
+                            int64_t *lru_hits_misses, void *ws, size_t ws_bytes, int32_t flags,
+                            void *stream) {
+    if (flags & ~RECMG_REPLAY_SKIP_STATS) return RECMG_E_INVALID_CONFIG;
+    if (!lru_cfg) return RECMG_E_INVALID_CONFIG;
+    return replay_range(cfg, state, gids, n, l_in, l_out, window_ratio, k_begin, k_end,
+                        with_tail, bits, pf, pf_stride, counters, cov_num, cov_den, nullptr, ws,
+                        ws_bytes, as_stream(stream), flags, lru_cfg, lru_state, lru_hits_misses);
 }
 
 int recmg_prefetch_stats(const int32_t *gids, int64_t n, int32_t l_in, int32_t l_out,

@@ -367,6 +367,32 @@ __device__ __forceinline__ void write_class(const ReplayArgs &a, int64_t pos, ui
     a.access_class[access_of_event(orig, a.Ec, a.K, a.l_in)] = c;
 }
 
+// LRU counts: hits and misses; in serve_only mode (the comparator fused into
+// the priority replay's launch, on its events) the caller pre-added the
+// call's accesses to the hits and each miss moves one over, because the
+// event builder drops serves that are guaranteed hits (collapsed repeats)
+__device__ __forceinline__ void flush_lru(const ReplayArgs &a, unsigned long long hits,
+                                          unsigned long long misses) {
+    if (!a.hits_misses) return;
+    if (a.serve_only) {
+        if (misses) {
+            atomicAdd((unsigned long long *)&a.hits_misses[0], (unsigned long long)(-(long long)misses));
+            atomicAdd((unsigned long long *)&a.hits_misses[1], misses);
+        }
+        return;
+    }
+    if (hits) atomicAdd((unsigned long long *)&a.hits_misses[0], hits);
+    if (misses) atomicAdd((unsigned long long *)&a.hits_misses[1], misses);
+}
+
+// the event as the LRU comparator sees it: in serve_only mode every
+// non-serve event is no event
+template <int POLICY>
+__device__ __forceinline__ uint32_t lru_view(const ReplayArgs &a, uint32_t e) {
+    if (POLICY != RECMG_POLICY_LRU) return e;
+    return (a.serve_only && ev_type(e) != EV_SERVE) ? kGidMask : e;
+}
+
 __device__ __forceinline__ void flush_counters(recmg_counters *ctr, unsigned long long ch,
                                                unsigned long long ph, unsigned long long od,
                                                unsigned long long ev, unsigned long long ins,
@@ -595,7 +621,7 @@ __device__ __forceinline__ unsigned long long replay_set_regs(const ReplayArgs &
             unsigned missing = 0;
 #pragma unroll
             for (int q = 0; q < kWide; q++) {
-                const uint32_t e = ring.at(pos - lo + 32 * q + lane);
+                const uint32_t e = lru_view<POLICY>(a, ring.at(pos - lo + 32 * q + lane));
                 gq[q] = ev_gid(e);
                 const uint32_t ty = ev_type(e);
                 const bool real = gq[q] != kGidMask;
@@ -664,7 +690,7 @@ __device__ __forceinline__ unsigned long long replay_set_regs(const ReplayArgs &
         }
         const int nb = (int)imin64(32, hi - pos);
         ring.ensure(pos - lo, nb);
-        const uint32_t e = lane < nb ? ring.at(pos - lo + lane) : kGidMask;
+        const uint32_t e = lane < nb ? lru_view<POLICY>(a, ring.at(pos - lo + lane)) : kGidMask;
         const uint32_t g = ev_gid(e), ty = ev_type(e);
         const bool real = g != kGidMask;
         unsigned mine = 0;
@@ -799,10 +825,7 @@ __device__ __forceinline__ unsigned long long replay_set_regs(const ReplayArgs &
         if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
     } else {
         lhits = __reduce_add_sync(FULL, (unsigned)lhits);
-        if (lane == 0 && a.hits_misses) {
-            if (lhits) atomicAdd((unsigned long long *)&a.hits_misses[0], lhits);
-            if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
-        }
+        if (lane == 0) flush_lru(a, lhits, od);
     }
     return od + ins;
 }
@@ -901,7 +924,7 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
         uint32_t cur[kWide];
 #pragma unroll
         for (int q = 0; q < kWide; q++) {
-            cur[q] = nxt[q];
+            cur[q] = lru_view<POLICY>(a, nxt[q]);   // (not at the load: it would wait)
             const int64_t i = wp + kWin + 32 * q + lane;
             nxt[q] = i < len ? __ldcs(seg + i) : kGidMask;
         }
@@ -1109,10 +1132,7 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
         if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
     } else {
         lhits = __reduce_add_sync(FULL, (unsigned)lhits);
-        if (lane == 0 && a.hits_misses) {
-            if (lhits) atomicAdd((unsigned long long *)&a.hits_misses[0], lhits);
-            if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
-        }
+        if (lane == 0) flush_lru(a, lhits, od);
     }
     return od + ins;
 }
@@ -1152,7 +1172,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
             uint32_t sm;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            int64_t *r = timing + 4 * set;
+            int64_t *r = timing + 4 * (set + (a.serve_only ? a.S : 0));
             r[0] = (int64_t)t_start;
             r[1] = (int64_t)t_end;
             r[2] = (int64_t)sm | ((int64_t)path << 32);
@@ -1586,10 +1606,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
         if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
     } else {
         lhits = __reduce_add_sync(FULL, (unsigned)lhits);
-        if (lane == 0 && a.hits_misses) {
-            if (lhits) atomicAdd((unsigned long long *)&a.hits_misses[0], lhits);
-            if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
-        }
+        if (lane == 0) flush_lru(a, lhits, od);
     }
     note_time(0, od + ins);
 }
@@ -1602,9 +1619,14 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
 // (which bound the launch: one set can carry 3% of the events) keep an SM's
 // issue slots to themselves instead of sharing them with ~20 warps of short
 // sets.  Without a queue: one set per CTA, heavy sets in the first CTAs.
-template <int POLICY, bool CLASS>
+// LRU2 (the priority replay with the LRU comparator fused in, on the same
+// partitioned events): b holds the comparator's state; items are the heavy
+// sets of both (priority first), then every set of the priority buffer, then
+// every set of the comparator.
+template <int POLICY, bool CLASS, bool LRU2>
 __global__ void __launch_bounds__(32, RECMG_REPLAY_MINB)
-replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int tables, int64_t items) {
+replay_smem_kernel(ReplayArgs a, ReplayArgs b, int Wp, int hbits, int regs, int tables,
+                   int64_t items) {
     extern __shared__ __align__(16) uint8_t dsm[];
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
@@ -1613,16 +1635,32 @@ replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int tables, int64_
     uint32_t *const work = a.work;
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    for (int64_t next = blockIdx.x;;) {
+    // with a queue, the heavy items go to the first CTAs directly -- one per SM
+    // in the launch's first wave -- so no two long chains share an SM; every
+    // other item is pulled from the queue
+    const int64_t hv = (work && a.heavy) ? (LRU2 ? 2 * kHeavySets : kHeavySets) : 0;
+    for (int64_t next = blockIdx.x, round = 0;; round++) {
         int64_t item = next;
-        if (work) {
+        if (work && !(round == 0 && (int64_t)blockIdx.x < hv)) {
             if (*(volatile uint32_t *)(work + 1 + smid) != 0) return;
             uint32_t it = 0;
             if (lane == 0) it = atomicAdd(work, 1u);
-            item = __shfl_sync(FULL, it, 0);
+            item = hv + (int64_t)__shfl_sync(FULL, it, 0);
         }
         if (item >= items) return;
         next = item + gridDim.x;   // no queue: one item per CTA (grid == items)
+        bool second = false;       // LRU2: an item of the comparator
+        if (LRU2) {
+            if (item < 2 * kHeavySets) {
+                second = item >= kHeavySets;
+                if (second) item -= kHeavySets;
+            } else {
+                int64_t r = item - 2 * kHeavySets;
+                second = r >= a.S;
+                if (second) r -= a.S;
+                item = kHeavySets + r;
+            }
+        }
         int64_t set = item;
         bool heavy_item = false;
         if (a.heavy) {
@@ -1636,7 +1674,10 @@ replay_smem_kernel(ReplayArgs a, int Wp, int hbits, int regs, int tables, int64_
             }
         }
         if (heavy_item && work && lane == 0) atomicAdd(work + 1 + smid, 1u);
-        replay_one_set<POLICY, CLASS>(a, set, dsm, Wp, hbits, regs, tables, heavy_item);
+        if (LRU2 && second)
+            replay_one_set<RECMG_POLICY_LRU, false>(b, set, dsm, Wp, hbits, -1, tables, heavy_item);
+        else
+            replay_one_set<POLICY, CLASS>(a, set, dsm, Wp, hbits, regs, tables, heavy_item);
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         if (heavy_item && work && lane == 0) atomicSub(work + 1 + smid, 1u);
@@ -1921,10 +1962,7 @@ replay_wide_kernel(ReplayArgs a) {
         if (lane == 0) flush_counters(a.ctr, ch, ph, od, nev, ins, (unsigned long long)count);
     } else {
         lhits = __reduce_add_sync(FULL, (unsigned)lhits);
-        if (lane == 0 && a.hits_misses) {
-            if (lhits) atomicAdd((unsigned long long *)&a.hits_misses[0], lhits);
-            if (od) atomicAdd((unsigned long long *)&a.hits_misses[1], od);
-        }
+        if (lane == 0) flush_lru(a, lhits, od);
     }
 }
 
@@ -1943,6 +1981,7 @@ __global__ void state_reset_kernel(StateView st, int64_t SW, int64_t S, int64_t 
 }
 
 __global__ void clock_bump_kernel(int64_t *header, int64_t by) { header[0] += by; }
+__global__ void add_i64_kernel(int64_t *x, int64_t by) { x[0] += by; }
 
 // next_use[i] = index of the next access to gids[i] (n if none), from the
 // accesses stably sorted by id (cache_sim.py:80-89)
@@ -2051,7 +2090,7 @@ __global__ void buffer_op_kernel(StateView st, int64_t S, int64_t W, int32_t op,
 
 // ---------------------------------------------------------------------------
 int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_t nsets,
-                  cudaStream_t s) {
+                  cudaStream_t s, const ReplayArgs *lru2) {
     (void)narrow;
     if (nsets <= 0) return RECMG_OK;
     // RECMG_REPLAY_REGS=0: every set through the shared-memory path (A/B, tests)
@@ -2091,30 +2130,46 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         // CTAs co-reside with other kernels' CTAs (pipelined with the forwards)
         const size_t smem = (size_t)bytes;
         int64_t items = nsets + (a.heavy ? kHeavySets : 0);
+        const bool fused = lru2 && policy == RECMG_POLICY_PRIORITY && a.heavy && a.W <= 32 && !cls;
+        ReplayArgs bq;
+        if (fused) {
+            bq = *lru2;
+            bq.qn = at.qn;
+            bq.smagic = at.smagic;
+            bq.heavy = a.heavy;
+            bq.work = a.work;
+            items *= 2;
+        } else {
+            memset(&bq, 0, sizeof(bq));
+        }
         // diagnostic: RECMG_REPLAY_ONLY_HEAVY=1 replays the heavy list alone
         const char *h_env = getenv("RECMG_REPLAY_ONLY_HEAVY");
-        if (h_env && h_env[0] == '1' && a.heavy) items = kHeavySets;
+        if (h_env && h_env[0] == '1' && a.heavy) items = fused ? 2 * kHeavySets : kHeavySets;
         // RECMG_REPLAY_QUEUE=0: one set per CTA, no SM reservation (A/B)
         const char *q_env = getenv("RECMG_REPLAY_QUEUE");
         ReplayArgs aq = at;
         if (q_env && q_env[0] == '0') aq.work = nullptr;
         if (aq.work) RECMG_CUDA_TRY(cudaMemsetAsync(aq.work, 0, sizeof(uint32_t) * kWorkWords, s));
-#define RECMG_SMEM_LAUNCH(P, C)                                                            \
+#define RECMG_SMEM_LAUNCH2(P, C, L2)                                                       \
     do {                                                                                    \
-        RECMG_CUDA_TRY(cudaFuncSetAttribute(replay_smem_kernel<P, C>,                       \
+        RECMG_CUDA_TRY(cudaFuncSetAttribute(replay_smem_kernel<P, C, L2>,                   \
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                             (int)smem));                                    \
         unsigned grid = (unsigned)items;                                                    \
         if (aq.work) {                                                                      \
             int per_sm = 0;                                                                 \
             RECMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                   \
-                &per_sm, replay_smem_kernel<P, C>, 32, smem));                              \
+                &per_sm, replay_smem_kernel<P, C, L2>, 32, smem));                          \
             const int64_t wave = (int64_t)kSmCount * (per_sm > 0 ? per_sm : 1);             \
             grid = (unsigned)(items < wave ? items : wave);                                 \
         }                                                                                   \
-        replay_smem_kernel<P, C><<<grid, 32, smem, s>>>(aq, Wp, hbits, regs, tables, items);\
+        replay_smem_kernel<P, C, L2><<<grid, 32, smem, s>>>(aq, bq, Wp, hbits, regs,        \
+                                                           tables, items);                  \
     } while (0)
-        if (policy == RECMG_POLICY_PRIORITY) {
+#define RECMG_SMEM_LAUNCH(P, C) RECMG_SMEM_LAUNCH2(P, C, false)
+        if (fused) {
+            RECMG_SMEM_LAUNCH2(RECMG_POLICY_PRIORITY, false, true);
+        } else if (policy == RECMG_POLICY_PRIORITY) {
             if (cls) RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, true);
             else RECMG_SMEM_LAUNCH(RECMG_POLICY_PRIORITY, false);
         } else if (policy == RECMG_POLICY_LRU_PF) {
@@ -2130,6 +2185,7 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
             RECMG_SMEM_LAUNCH(RECMG_POLICY_LRU, false);
         }
 #undef RECMG_SMEM_LAUNCH
+#undef RECMG_SMEM_LAUNCH2
     } else {
 #define RECMG_WIDE_LAUNCH(P, C) \
     replay_wide_kernel<P, C><<<(unsigned)nsets, kWideThreads, 0, s>>>(a)

@@ -35,6 +35,7 @@ __global__ void prefetch_stats_kernel(const int32_t *__restrict__ gids, int64_t 
                                       recmg_counters *__restrict__ ctr);
 __global__ void state_reset_kernel(StateView st, int64_t SW, int64_t S, int64_t V);
 __global__ void clock_bump_kernel(int64_t *header, int64_t by);
+__global__ void add_i64_kernel(int64_t *x, int64_t by);
 __global__ void next_use_kernel(const uint32_t *__restrict__ sorted_ids,
                                 const uint32_t *__restrict__ sorted_pos, int64_t n,
                                 int32_t *__restrict__ next_use);
@@ -64,10 +65,13 @@ struct ReplayArgs {
     int64_t total_ids;         // ids of the trace (0: unknown)
     int32_t qn;                // way-map bytes per set (0: no way map), set by launch_replay
     uint32_t smagic;           // ceil(2^32 / S)
+    int32_t serve_only;        // LRU on the priority replay's events: serves only
     uint32_t *work = nullptr;  // [kWorkWords] or null: replay work queue (see replay_smem_kernel)
 };
 
+// lru2: the LRU comparator fused into a priority replay of sets <= 32 ways on
+// the same partitioned events (its own state, serve_only) -- or null
 int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_t nsets,
-                  cudaStream_t s);
+                  cudaStream_t s, const ReplayArgs *lru2 = nullptr);
 
 }  // namespace recmg

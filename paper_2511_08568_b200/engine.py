@@ -86,6 +86,38 @@ class BufferReplay:
             self._ws.numel(), _native.REPLAY_SKIP_STATS if skip_stats else 0,
             _native.stream_handle(self.torch)), "replay_chunks")
 
+    def run_chunks_lru(self, gids, k0, k1, with_tail, lru, bits=None, pf=None,
+                       skip_stats=False):
+        """run_chunks with the LRU comparator `lru` (an LruSim over the same sets)
+        fused into the replay launch (recmg_replay_chunks_lru): it replays the
+        serves of this replay's own events.  False (nothing launched) when the
+        geometries do not allow it."""
+        n = gids.numel()
+        stride = int(pf.shape[1]) if pf is not None else 0
+        self.reserve(n, stride)
+        self.K = num_chunks(n, self.l_in, self.l_out, self.window_ratio)
+        rc = _native.lib().recmg_replay_chunks_lru(
+            ctypes.byref(self.cfg), _native.ptr(self.state), _native.ptr(gids), n, self.l_in,
+            self.l_out, self.window_ratio, int(k0), int(k1), 1 if with_tail else 0,
+            _native.ptr(bits), _native.ptr(pf), stride, _native.ptr(self.counters),
+            _native.ptr(self._cov[0]), _native.ptr(self._cov[1]), ctypes.byref(lru.cfg),
+            _native.ptr(lru.state), _native.ptr(lru.hm), _native.ptr(self._ws),
+            self._ws.numel(), _native.REPLAY_SKIP_STATS if skip_stats else 0,
+            _native.stream_handle(self.torch))
+        if rc == _native.RECMG_E_INVALID_CONFIG:
+            return False
+        _native.check(rc, "replay_chunks_lru")
+        return True
+
+    def fusable_lru(self, lru):
+        """Whether run_chunks_lru can carry `lru` (same sets and ways <= 32)."""
+        a, b = self.cfg, lru.cfg
+        if b.policy != _native.POLICY_LRU or a.policy != _native.POLICY_PRIORITY:
+            return False
+        if a.total_ids != b.total_ids or a.ways <= 0 or a.ways > 32 or b.ways != a.ways:
+            return False
+        return a.capacity // a.ways == b.capacity // b.ways and a.capacity // a.ways >= 2
+
     def stats_chunks(self, gids, k0, k1, pf=None):
         """Prefetch statistics (counters + coverage counts) of chunks [k0, k1)
         alone (recmg_prefetch_stats): they need the decoded ids, not the buffer."""

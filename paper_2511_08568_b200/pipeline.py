@@ -49,6 +49,11 @@ _GRAPHS = os.environ.get("RECMG_GRAPHS", "1") == "1"
 # kernels take SMs at the forward launch boundary (config 2: +1.8%).
 _LRU_LATE = os.environ.get("RECMG_LRU_LATE", "1") == "1"
 _LRU_PRIO = os.environ.get("RECMG_LRU_PRIO", "1") == "1"
+# Serial schedule: the LRU comparator runs inside the replay launch, on the
+# serves of the replay's own partitioned events (recmg_replay_chunks_lru), so
+# it builds and partitions no events of its own (RECMG_LRU_FUSED=0: its own
+# launches on the LRU stream)
+_LRU_FUSED = os.environ.get("RECMG_LRU_FUSED", "1") == "1"
 
 
 class HotPath:
@@ -251,14 +256,18 @@ class HotPath:
 
         # late only in the serial schedule: pipelined runs (few-set buffers, config
         # 3's one-hot-set shards) have chain-bound LRUs that must hide under the forwards
-        lru_late = _LRU_LATE and self.lru is not None and serial
-        if self.lru is not None and not lru_late:
+        self._lru_fused = (_LRU_FUSED and self.lru is not None and serial
+                           and self.buffer.fusable_lru(self.lru))
+        lru_late = _LRU_LATE and self.lru is not None and serial and not self._lru_fused
+        if self.lru is not None and not lru_late and not self._lru_fused:
             run_lru(all_ids)
         prev = L.recmg_set_model_sm_budget(self.model_sms)
         try:
             self.s_replay.wait_event(all_ids)
             with torch.cuda.stream(self.s_replay):
                 self.buffer.reset()
+                if self._lru_fused:
+                    self.lru.reset()
             bits = self.bits[:K] if (K and self.caching is not None) else None
             pf = self.pf[:K] if (K and self.prefetch is not None) else None
             models = K > 0 and (self.caching is not None or self.prefetch is not None)
@@ -352,7 +361,7 @@ class HotPath:
         main.wait_stream(self.s_replay)
         if self.s_hook is not None:
             main.wait_stream(self.s_hook)
-        if self.lru is not None:
+        if self.lru is not None and not self._lru_fused:
             main.wait_stream(self.s_lru)
         self._ev("tail", main)          # ... -> last replay piece and LRU done
         self.K = K
@@ -413,7 +422,13 @@ class HotPath:
         self.s_replay.wait_event(scored)
         with torch.cuda.stream(self.s_replay):
             self._ev("replay", self.s_replay)
-            self.buffer.run_chunks(g, 0, K, True, bits, pf, skip_stats=early_stats)
+            if self._lru_fused and not self.buffer.run_chunks_lru(
+                    g, 0, K, True, self.lru, bits, pf, skip_stats=early_stats):
+                self.buffer.run_chunks(g, 0, K, True, bits, pf, skip_stats=early_stats)
+                self.lru.reset()
+                self.lru.run(g)
+            elif not self._lru_fused:
+                self.buffer.run_chunks(g, 0, K, True, bits, pf, skip_stats=early_stats)
             self._ev("replay", self.s_replay)
             if host_src is not None and not early_stats:
                 for r in range(2):
@@ -536,7 +551,9 @@ class HotPath:
                         self.launch(n, host_src=src)
                     self._graph = g
                     self._graph_state = (list(self._cov_events), self.K, self.n)
-                except Exception:   # not capturable here: stay eager
+                except Exception as e:   # not capturable here: stay eager
+                    import warnings
+                    warnings.warn(f"HotPath: CUDA graph capture failed, running eagerly ({e})")
                     self._graph = None
                     torch.cuda.synchronize()
             if self._graph is not None:

@@ -33,19 +33,19 @@ g, bits, pf = hp.gids[:n], hp.bits[:K], hp.pf[:K]
 buf = hp.buffer
 L = _native.lib()
 L.recmg_diag_set_timing.argtypes = [ctypes.c_void_p]
-rec = torch.zeros(4 * S, dtype=torch.int64, device="cuda")
+rec = torch.zeros(8 * S, dtype=torch.int64, device="cuda")
 
 
 def report(name, r):
-    r = r.reshape(S, 4)
+    r = r[:4 * S].reshape(S, 4)
     st, en, path, ln, ms = r[:, 0], r[:, 1], r[:, 2] >> 32, r[:, 3] & 0xFFFFFFFF, r[:, 3] >> 32
     ok = en > 0
     t0 = st[ok].min()
     span = (en[ok].max() - t0) / 1e6
     print(f"== {name}: span {span:.2f} ms over {ok.sum()} sets")
-    last = np.argsort(-en)[:5]
+    last = np.argsort(-en)[:12]
     for s_ in last:
-        print(f"   set {s_:6d} path {path[s_]} len {ln[s_]:8d} start {(st[s_]-t0)/1e6:7.3f} "
+        print(f"   set {s_:6d} path {path[s_]} sm {r[s_, 2] & 0xFFFFFFFF:3d} len {ln[s_]:8d} start {(st[s_]-t0)/1e6:7.3f} "
               f"dur {(en[s_]-st[s_])/1e6:7.3f} ms  {(en[s_]-st[s_])/max(ln[s_],1):6.1f} ns/ev, "
               f"misses {ms[s_]} ({ms[s_]/max(ln[s_],1):.2f}/ev)")
     for p_ in (0, 1):
@@ -57,7 +57,46 @@ def report(name, r):
                       f"{d.sum() / ln[m].sum():6.1f} ns/event, max dur {d.max() / 1e6:.3f} ms")
 
 
-for regs, queue in (("0", "1"), ("1", "1"), ("-1", "1")):
+from paper_2511_08568_b200.engine import LruSim  # noqa: E402
+lru = LruSim(C32, t.total_ids if hasattr(t, "total_ids") else sum(t.table_sizes), 32, n)
+for _ in range(2):
+    rec.zero_()
+    L.recmg_diag_set_timing(rec.data_ptr())
+    buf.reset()
+    lru.reset()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    assert buf.run_chunks_lru(g, 0, K, True, lru, bits, pf, skip_stats=True)
+    e1.record()
+    torch.cuda.synchronize()
+print(f"fused replay + LRU (events + partition + both): {e0.elapsed_time(e1):.2f} ms")
+r = rec.cpu().numpy()
+both = np.concatenate([r[:4 * S].reshape(S, 4), r[4 * S:].reshape(S, 4)])
+t0 = both[:, 0][both[:, 1] > 0].min()
+report("fused: priority replay items", r[:4 * S])
+rr = r[4 * S:].copy()
+report("fused: LRU items", rr)
+L.recmg_diag_set_timing(None)
+if os.environ.get("TIMELINE_ONLY_HEAVY"):
+    os.environ["RECMG_REPLAY_ONLY_HEAVY"] = "1"
+    for fused in (True, False):
+        rec.zero_()
+        L.recmg_diag_set_timing(rec.data_ptr())
+        buf.reset()
+        lru.reset()
+        if fused:
+            assert buf.run_chunks_lru(g, 0, K, True, lru, bits, pf, skip_stats=True)
+        else:
+            buf.run_chunks(g, 0, K, True, bits, pf, skip_stats=True)
+        torch.cuda.synchronize()
+        r = rec.cpu().numpy()
+        report(f"heavy only, fused={fused}: priority items", r[:4 * S])
+        if fused:
+            report("heavy only, fused: LRU items", r[4 * S:].copy())
+    L.recmg_diag_set_timing(None)
+    os.environ.pop("RECMG_REPLAY_ONLY_HEAVY")
+
+for regs, queue in ():
     os.environ["RECMG_REPLAY_REGS"] = regs
     os.environ["RECMG_REPLAY_QUEUE"] = queue
     for _ in range(2):

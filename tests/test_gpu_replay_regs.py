@@ -131,3 +131,37 @@ def test_priority_state_after_piecewise_replay_matches_smem():
     for x, y in zip(out[0][1:], out[1][1:]):
         assert np.array_equal(x, y)
     assert (out[0][1] >= 0).sum() == out[0][3].sum()
+
+
+@pytest.mark.parametrize("seed,V,n,sets,pieces", [
+    (20, 200_000, 2_000_000, 500, 1),
+    (21, 60_000, 900_000, 120, 3),
+    (22, 3_000, 100_000, 8, 2),
+])
+def test_lru_fused_into_replay(seed, V, n, sets, pieces):
+    """recmg_replay_chunks_lru: the 32-way LRU comparator replayed on the serves
+    of the priority replay's own events (collapsed repeat serves included as
+    hits) equals simulate() and the oracle, with the priority replay itself
+    unchanged; chunk ranges continue both states."""
+    import torch
+    from paper_2511_08568_b200.engine import BufferReplay, LruSim
+    gids, bits, pf = _workload(seed, V, n)
+    K = rb.num_chunks(n)
+    dev = torch.device("cuda:0")
+    g = torch.as_tensor(gids.astype(np.int32), device=dev)
+    b = torch.as_tensor(bits, device=dev)
+    p = torch.as_tensor(pf.astype(np.int32), device=dev)
+    cap = 32 * sets
+    fused, plain = BufferReplay(cap, V, 4, 32, n=n, pf_stride=5), BufferReplay(cap, V, 4, 32, n=n,
+                                                                                pf_stride=5)
+    lru = LruSim(cap, V, 32, n)
+    assert fused.fusable_lru(lru)
+    cuts = [K * i // pieces for i in range(pieces + 1)]
+    for k0, k1 in zip(cuts[:-1], cuts[1:]):
+        assert fused.run_chunks_lru(g, k0, k1, k1 == K, lru, bits=b, pf=p)
+        plain.run_chunks(g, k0, k1, k1 == K, bits=b, pf=p)
+    assert fused.result() == plain.result()
+    h, m = lru.result()
+    hr, _ = oracle.lru(gids, V, cap, 32, per_access=True)
+    assert (h, m) == (hr, n - hr)
+    assert rb.simulate(gids, rb.CacheConfig(cap, rb.Policy.LRU, 32)).hits == h
