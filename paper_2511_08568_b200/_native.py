@@ -53,6 +53,7 @@ EXPORTS = (
     "recmg_trace_generate_block", "recmg_shard_local_ids", "recmg_trace_parse_text",
     "recmg_coverage_accumulate", "recmg_embedding_bag_a2a", "recmg_peer_alloc",
     "recmg_peer_free", "recmg_peer_handle", "recmg_peer_open", "recmg_peer_close",
+    "recmg_replay_chunks_lru",
     "recmg_model_forward_signal", "recmg_wait_progress", "recmg_replay_chunks_ex",
     "recmg_prefetch_stats",
 )
