@@ -1627,6 +1627,7 @@ int model_pack_tc(const recmg_model_shape *m, const float *raw, const float *emb
 
 static int g_model_sm_budget = kSmCount;
 
+int model_sm_budget() { return g_model_sm_budget; }
 int set_model_sm_budget(int n) {
     const int prev = g_model_sm_budget;
     g_model_sm_budget = n < 1 ? 1 : (n > kSmCount ? kSmCount : n);

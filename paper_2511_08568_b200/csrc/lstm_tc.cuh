@@ -30,5 +30,6 @@ int model_forward_tc(const recmg_model_shape *m, const void *packed_dense, const
 int wait_progress(const int32_t *progress, int32_t target, cudaStream_t s);
 size_t tc_workspace_bytes(const recmg_model_shape *m, int64_t batch);
 int set_model_sm_budget(int n);
+int model_sm_budget();
 
 }  // namespace recmg

@@ -20,6 +20,7 @@
 // global memory, an id -> slot map, the same batching by warp 0 and the
 // victim scan by the whole CTA (replay_wide_kernel).
 #include "replay.cuh"
+#include "lstm_tc.cuh"
 #include <cstdlib>
 
 namespace recmg {
@@ -2146,9 +2147,15 @@ int launch_replay(int policy, bool narrow, bool cls, const ReplayArgs &a, int64_
         const char *h_env = getenv("RECMG_REPLAY_ONLY_HEAVY");
         if (h_env && h_env[0] == '1' && a.heavy) items = fused ? 2 * kHeavySets : kHeavySets;
         // RECMG_REPLAY_QUEUE=0: one set per CTA, no SM reservation (A/B)
+        // The queue (and its SM reservation for the heavy chains) only when the
+        // replay has the GPU to itself: beside the forwards of a pipelined
+        // schedule (a model SM budget below the SM count) the few free SMs
+        // must all take sets (config 3 shard 0: 372 vs 431 M acc/s)
         const char *q_env = getenv("RECMG_REPLAY_QUEUE");
         ReplayArgs aq = at;
-        if (q_env && q_env[0] == '0') aq.work = nullptr;
+        if ((q_env && q_env[0] == '0') || (!(q_env && q_env[0] == '1') &&
+                                           model_sm_budget() < kSmCount))
+            aq.work = nullptr;
         if (aq.work) RECMG_CUDA_TRY(cudaMemsetAsync(aq.work, 0, sizeof(uint32_t) * kWorkWords, s));
 #define RECMG_SMEM_LAUNCH2(P, C, L2)                                                       \
     do {                                                                                    \

@@ -259,10 +259,12 @@ class HotPath:
         self._lru_fused = (_LRU_FUSED and self.lru is not None and serial
                            and self.buffer.fusable_lru(self.lru))
         lru_late = _LRU_LATE and self.lru is not None and serial and not self._lru_fused
-        if self.lru is not None and not lru_late and not self._lru_fused:
-            run_lru(all_ids)
+        # (the SM budget first: a replay-engine launch made under a budget below
+        # the SM count -- beside the forwards -- spreads over every free SM)
         prev = L.recmg_set_model_sm_budget(self.model_sms)
         try:
+            if self.lru is not None and not lru_late and not self._lru_fused:
+                run_lru(all_ids)
             self.s_replay.wait_event(all_ids)
             with torch.cuda.stream(self.s_replay):
                 self.buffer.reset()
