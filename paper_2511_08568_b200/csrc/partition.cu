@@ -23,9 +23,10 @@ __device__ __forceinline__ uint32_t set_of_event(uint32_t e, uint32_t S) {
 
 __global__ void __launch_bounds__(kPartThreads)
 part_hist_kernel(const uint32_t *__restrict__ keys, int64_t N, uint32_t S, int shift,
-                 uint32_t *__restrict__ hist, int ntiles) {
+                 uint32_t *__restrict__ hist, int ntiles, const uint32_t *__restrict__ n_lim) {
     __shared__ uint32_t h[256];
     const int tile = blockIdx.x;
+    if (n_lim) N = imin64(N, (int64_t)*n_lim);
     for (int i = threadIdx.x; i < 256; i += kPartThreads) h[i] = 0;
     __syncthreads();
     const int64_t base = (int64_t)tile * kPartTile;
@@ -33,7 +34,10 @@ part_hist_kernel(const uint32_t *__restrict__ keys, int64_t N, uint32_t S, int s
     for (int r = 0; r < kPartItems; r++) {
         int64_t i = base + (int64_t)r * kPartThreads + threadIdx.x;
         uint32_t d = 0xFFFFFFFFu;
-        if (i < N) d = (set_of_event(__ldg(keys + i), S) >> shift) & 255u;
+        if (i < N) {
+            const uint32_t st = set_of_event(__ldg(keys + i), S);
+            if (st < S) d = (st >> shift) & 255u;   // no-events (set S) are dropped
+        }
         unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
         if (d != 0xFFFFFFFFu && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1))
             atomicAdd(&h[d], (uint32_t)__popc(peers));
@@ -46,8 +50,10 @@ template <bool VALS>
 __global__ void __launch_bounds__(kPartThreads)
 part_scatter_kernel(const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin,
                     uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, int64_t N,
-                    uint32_t S, int shift, const uint32_t *__restrict__ offs, int ntiles) {
+                    uint32_t S, int shift, const uint32_t *__restrict__ offs, int ntiles,
+                    const uint32_t *__restrict__ n_lim) {
     __shared__ uint32_t wcnt[kPartWarps][256];
+    if (n_lim) N = imin64(N, (int64_t)*n_lim);
     __shared__ uint32_t toff[256];
     const int tile = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -66,7 +72,8 @@ part_scatter_kernel(const uint32_t *__restrict__ kin, const uint32_t *__restrict
         if (i < N) {
             k[r] = __ldg(kin + i);
             if (VALS) v[r] = __ldg(vin + i);
-            d[r] = (set_of_event(k[r], S) >> shift) & 255u;
+            const uint32_t st = set_of_event(k[r], S);
+            if (st < S) d[r] = (st >> shift) & 255u;
         }
     }
 #pragma unroll
@@ -205,13 +212,23 @@ int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t M, uint32_t *p
 
 // --- segment bounds after the sort -----------------------------------------
 __global__ void seg_bounds_kernel(const uint32_t *__restrict__ k, int64_t N, uint32_t S,
-                                  uint32_t *__restrict__ start, uint32_t *__restrict__ end) {
+                                  uint32_t *__restrict__ start, uint32_t *__restrict__ end,
+                                  const uint32_t *__restrict__ n_lim) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    N = imin64(N, (int64_t)*n_lim);
     if (i >= N) return;
     uint32_t s = set_of_event(k[i], S);
     if (s >= S) return;
     if (i == 0 || set_of_event(k[i - 1], S) != s) start[s] = (uint32_t)i;
     if (i == N - 1 || set_of_event(k[i + 1], S) != s) end[s] = (uint32_t)(i + 1);
+}
+
+// events kept by the first pass (every no-event, set S, is dropped there):
+// the exclusive scan's last offset plus the last count
+__global__ void n_real_kernel(const uint32_t *__restrict__ hist,
+                              const uint32_t *__restrict__ offs, int64_t M,
+                              uint32_t *__restrict__ n_real) {
+    n_real[0] = offs[M - 1] + hist[M - 1];
 }
 
 // Sets whose segment is much longer than the mean (Zipf skew: one set can
@@ -270,6 +287,7 @@ void partition_plan(Arena &a, PartitionBuffers &pb, int64_t N, int64_t S, bool v
     pb.seg_end = a.take<uint32_t>((size_t)S + 1);
     pb.heavy = a.take<int32_t>(1 + kHeavySets);
     pb.heavy_cand = a.take<int32_t>(1 + kHeavyCand);
+    pb.n_real = a.take<uint32_t>(1);
     pb.work = a.take<uint32_t>(kWorkWords);
 }
 
@@ -283,17 +301,24 @@ int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaSt
     const int64_t M = (int64_t)256 * pb.ntiles;
     for (int p = 0; p < passes; p++) {
         int shift = 8 * p;
+        // pass 0 reads all N events and keeps the real ones (n_real of them);
+        // later passes read those
+        const uint32_t *lim = p == 0 ? nullptr : pb.n_real;
         part_hist_kernel<<<pb.ntiles, kPartThreads, 0, s>>>(kin, N, (uint32_t)S, shift, pb.hist,
-                                                           pb.ntiles);
+                                                           pb.ntiles, lim);
         RECMG_LAUNCH_CHECK();
         int rc = exclusive_scan_u32(pb.hist, pb.offs, M, pb.partial, s);
         if (rc) return rc;
+        if (p == 0) {
+            n_real_kernel<<<1, 1, 0, s>>>(pb.hist, pb.offs, M, pb.n_real);
+            RECMG_LAUNCH_CHECK();
+        }
         if (vin)
             part_scatter_kernel<true><<<pb.ntiles, kPartThreads, 0, s>>>(
-                kin, vin, kout, vout, N, (uint32_t)S, shift, pb.offs, pb.ntiles);
+                kin, vin, kout, vout, N, (uint32_t)S, shift, pb.offs, pb.ntiles, lim);
         else
             part_scatter_kernel<false><<<pb.ntiles, kPartThreads, 0, s>>>(
-                kin, nullptr, kout, nullptr, N, (uint32_t)S, shift, pb.offs, pb.ntiles);
+                kin, nullptr, kout, nullptr, N, (uint32_t)S, shift, pb.offs, pb.ntiles, lim);
         RECMG_LAUNCH_CHECK();
         uint32_t *t = kin; kin = kout; kout = t;
         t = vin; vin = vout; vout = t;
@@ -304,7 +329,8 @@ int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaSt
     keys = kin;
     vals = vin;
     seg_bounds_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(keys, N, (uint32_t)S,
-                                                                  pb.seg_start, pb.seg_end);
+                                                                  pb.seg_start, pb.seg_end,
+                                                                  pb.n_real);
     RECMG_LAUNCH_CHECK();
     RECMG_CUDA_TRY(cudaMemsetAsync(pb.heavy_cand, 0, sizeof(int32_t), s));
     const int64_t mean = N / (S > 0 ? S : 1);

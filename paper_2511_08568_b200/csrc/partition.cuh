@@ -13,13 +13,16 @@ struct PartitionBuffers {
     int32_t *heavy = nullptr;  // [1 + kHeavySets]: count, then the heaviest sets
     uint32_t *work = nullptr;  // [kWorkWords]: the replay launch's work queue
     int32_t *heavy_cand = nullptr;  // [1 + kHeavyCand]: count, then sets above the threshold
+    uint32_t *n_real = nullptr;     // [1]: events kept (no-events, set S, are dropped)
 };
 
 int partition_passes(int64_t S);
 void partition_plan(Arena &a, PartitionBuffers &pb, int64_t N, int64_t S, bool vals);
-// Sorts keys (and vals) stably by set; on return keys/vals point at the
-// sorted arrays (which may be the workspace copies) and seg_start/seg_end
-// hold each set's [start, end) range (empty sets: 0,0).
+// Sorts keys (and vals) stably by set, dropping the no-events (gid kGidMask,
+// set S: collapsed serves, dead updates, padding); on return keys/vals point
+// at the sorted arrays (which may be the workspace copies), *n_real of them
+// valid, and seg_start/seg_end hold each set's [start, end) range (empty
+// sets: 0,0).
 int partition_run(PartitionBuffers &pb, uint32_t *&keys, uint32_t *&vals, cudaStream_t s);
 
 size_t scan_workspace_elems(int64_t M);
