@@ -256,7 +256,11 @@ class HotPath:
 
         # late only in the serial schedule: pipelined runs (few-set buffers, config
         # 3's one-hot-set shards) have chain-bound LRUs that must hide under the forwards
-        self._lru_fused = (_LRU_FUSED and self.lru is not None and serial
+        # (every schedule but the streamed one: each replay call carries the
+        # comparator over its chunk range, the states continue across calls)
+        self._lru_fused = (_LRU_FUSED and self.lru is not None and K > 0 and has_models
+                           and not (_STREAMED and len(pieces) > 1 and self.piece_hook is None
+                                    and not self.piece_chunks)
                            and self.buffer.fusable_lru(self.lru))
         lru_late = _LRU_LATE and self.lru is not None and serial and not self._lru_fused
         # (the SM budget first: a replay-engine launch made under a budget below
@@ -325,7 +329,12 @@ class HotPath:
                 self.s_replay.wait_event(scored)
                 with torch.cuda.stream(self.s_replay):
                     self._ev("replay", self.s_replay)
-                    self.buffer.run_chunks(g, k0, k1, i == len(pieces) - 1, bits, pf)
+                    last = i == len(pieces) - 1
+                    if not (self._lru_fused and self.buffer.run_chunks_lru(
+                            g, k0, k1, last, self.lru, bits, pf)):
+                        self.buffer.run_chunks(g, k0, k1, last, bits, pf)
+                        if self._lru_fused:
+                            raise RuntimeError("recmg_replay_chunks_lru refused a fusable LRU")
                     self._ev("replay", self.s_replay)
                     if self.piece_hook is not None and not self.hook_snapshot:
                         self._ev("hook", self.s_replay)
