@@ -950,168 +950,167 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
                          : __ballot_sync(FULL, real);
             missing |= Cq[q] & ~Hq[q];
         }
-        if (missing == 0) {
-            // one hit run of 128 events: per distinct way, S count (the first S
-            // takes the tag), last U/P write [LRU: last hit]
-            unsigned pend[kWide], took[kWide];
+        // The window as hit runs and misses: the run before the first miss is
+        // applied per distinct way it touches (a ballot per way: a handful;
+        // the first S takes the tag, the last U/P writes the priority [LRU: the
+        // last hit sets the clock]), the miss is resolved, the window's way
+        // numbers are patched for the two gids it changed, and the next run
+        // starts after it.  A window without a miss is one run.
+        (void)missing;
+        uint32_t gw[kWide];
 #pragma unroll
-            for (int q = 0; q < kWide; q++) { pend[q] = Hq[q]; took[q] = 0; }
-            while (pend[0] | pend[1] | pend[2] | pend[3]) {
-                const int q0 = pend[0] ? 0 : (pend[1] ? 1 : (pend[2] ? 2 : 3));
-                const unsigned pq = q0 == 0 ? pend[0] : (q0 == 1 ? pend[1] : (q0 == 2 ? pend[2] : pend[3]));
-                const int wsrc = q0 == 0 ? wq[0] : (q0 == 1 ? wq[1] : (q0 == 2 ? wq[2] : wq[3]));
-                const int wv = __shfl_sync(FULL, wsrc, __ffs(pq) - 1);
-                unsigned mm[kWide];
+        for (int q = 0; q < kWide; q++) gw[q] = ev_gid(cur[q]);
+        int start = 0;
+        for (;;) {
+            unsigned Rq[kWide], mq[kWide];
+            int m = kWin;
+#pragma unroll
+            for (int q = kWide - 1; q >= 0; q--) {
+                const int lo32 = start - 32 * q;
+                const unsigned from = lo32 <= 0 ? ~0u : (lo32 >= 32 ? 0u : ~0u << lo32);
+                mq[q] = Cq[q] & ~Hq[q] & from;
+                if (mq[q]) m = 32 * q + __ffs(mq[q]) - 1;
+                Rq[q] = from;
+            }
+#pragma unroll
+            for (int q = 0; q < kWide; q++) {
+                const int hi32 = m - 32 * q;
+                Rq[q] &= hi32 >= 32 ? ~0u : (hi32 <= 0 ? 0u : (1u << hi32) - 1u);
+            }
+            // each way's events of the run: one ballot per part for every way
+            // the window names -- independent ballots, no per-way round trip
+            unsigned mine[kWide], took[kWide];
+            unsigned named_l = 0;
+#pragma unroll
+            for (int q = 0; q < kWide; q++) {
+                mine[q] = 0;
+                took[q] = 0;
+                if (wq[q] != kNone) named_l |= 1u << wq[q];
+            }
+            for (unsigned named = __reduce_or_sync(FULL, named_l); named; named &= named - 1) {
+                const int wv = __ffs(named) - 1;
 #pragma unroll
                 for (int q = 0; q < kWide; q++) {
-                    mm[q] = __ballot_sync(FULL, wq[q] == wv);
-                    pend[q] &= ~mm[q];
+                    const unsigned b = __ballot_sync(FULL, wq[q] == wv);
+                    if (lane == wv) mine[q] = b & Rq[q];
                 }
-                if (lane == wv) {
-                    if (PRIO) {
-                        unsigned nS = 0, u1 = 0;
-                        int fS = -1, lU = -1;
+            }
+            if (mine[0] | mine[1] | mine[2] | mine[3]) {
+                if (PRIO) {
+                    unsigned nS = 0, u1 = 0;
+                    int fS = -1, lU = -1;
 #pragma unroll
-                        for (int q = 0; q < kWide; q++) {
-                            const unsigned sp = mm[q] & Sq[q], up = mm[q] & UPq[q];
-                            nS += __popc(sp);
-                            if (fS < 0 && sp) fS = 32 * q + __ffs(sp) - 1;
-                            if (up) { lU = 32 * q + 31 - __clz(up); u1 = U1q[q]; }
-                        }
-                        if (nS) {
-                            if (mhi & 1u) {
-                                ph += 1; ch += nS - 1; mhi &= ~1u;
-#pragma unroll
-                                for (int q = 0; q < kWide; q++)
-                                    if ((fS >> 5) == q) took[q] = 1u << (fS & 31);
-                            } else {
-                                ch += nS;
-                            }
-                        }
-                        if (lU >= 0) pr = a.es + (int32_t)((u1 >> (lU & 31)) & 1u) + decay;
-                    } else {
-                        int last = -1;
-#pragma unroll
-                        for (int q = 0; q < kWide; q++) {
-                            lhits += __popc(mm[q]);
-                            if (mm[q]) last = 32 * q + 31 - __clz(mm[q]);
-                        }
-                        clk = clock_base + pos + last;
+                    for (int q = 0; q < kWide; q++) {
+                        const unsigned sp = mine[q] & Sq[q], up = mine[q] & UPq[q];
+                        nS += __popc(sp);
+                        if (fS < 0 && sp) fS = 32 * q + __ffs(sp) - 1;
+                        if (up) { lU = 32 * q + 31 - __clz(up); u1 = U1q[q]; }
                     }
+                    if (nS) {
+                        if (mhi & 1u) {
+                            ph += 1; ch += nS - 1; mhi &= ~1u;
+#pragma unroll
+                            for (int q = 0; q < kWide; q++)
+                                if ((fS >> 5) == q) took[q] = 1u << (fS & 31);
+                        } else {
+                            ch += nS;
+                        }
+                    }
+                    if (lU >= 0) pr = a.es + (int32_t)((u1 >> (lU & 31)) & 1u) + decay;
+                } else {
+                    int last = -1;
+#pragma unroll
+                    for (int q = 0; q < kWide; q++) {
+                        lhits += __popc(mine[q]);
+                        if (mine[q]) last = 32 * q + 31 - __clz(mine[q]);
+                    }
+                    clk = clock_base + pos + last;
                 }
             }
             if (PRIO && CLASS) {
 #pragma unroll
                 for (int q = 0; q < kWide; q++) {
                     const unsigned pf = __reduce_or_sync(FULL, took[q]);
-                    if ((Sq[q] >> lane) & 1u)
+                    if ((Sq[q] & Rq[q]) >> lane & 1u)
                         write_class(a, pos + 32 * q + lane, ((pf >> lane) & 1u) ? 1 : 0);
                 }
             }
-            continue;
-        }
-        // a miss in the window: its 4 parts in order, misses resolved one by one
-#pragma unroll 1
-        for (int q = 0; q < kWide; q++) {
-            const uint32_t e = q == 0 ? cur[0] : (q == 1 ? cur[1] : (q == 2 ? cur[2] : cur[3]));
-            const uint32_t g = ev_gid(e);
-            const bool real = g != kGidMask;
-            const int64_t base = pos + 32 * q;
-            const unsigned Sm = q == 0 ? Sq[0] : (q == 1 ? Sq[1] : (q == 2 ? Sq[2] : Sq[3]));
-            const unsigned cand = q == 0 ? Cq[0] : (q == 1 ? Cq[1] : (q == 2 ? Cq[2] : Cq[3]));
-            unsigned UPm = 0, U1m = 0;
+            if (m >= kWin) break;
+            // the miss at window position m
+            const int qm = m >> 5, lm = m & 31;
+            const uint32_t gsel = qm == 0 ? gw[0] : (qm == 1 ? gw[1] : (qm == 2 ? gw[2] : gw[3]));
+            const uint32_t gc = __shfl_sync(FULL, gsel, lm);
+            const unsigned Ssel = qm == 0 ? Sq[0] : (qm == 1 ? Sq[1] : (qm == 2 ? Sq[2] : Sq[3]));
+            const bool isS = (Ssel >> lm) & 1u;
+            const int64_t at_m = pos + m;
             if (PRIO) {
-                UPm = q == 0 ? UPq[0] : (q == 1 ? UPq[1] : (q == 2 ? UPq[2] : UPq[3]));
-                U1m = q == 0 ? U1q[0] : (q == 1 ? U1q[1] : (q == 2 ? U1q[2] : U1q[3]));
-            }
-            int w = real ? wmap[div_set(g, S, M)] : kNone;   // after the earlier parts' misses
-            unsigned hit = __ballot_sync(FULL, w != kNone);
-            int start = 0;
-            for (;;) {
-                const unsigned from = start >= 32 ? 0u : ~0u << start;
-                const unsigned miss = cand & ~hit & from;
-                const int cut = miss ? __ffs(miss) - 1 : 32;
-                const unsigned R = (cut >= 32 ? ~0u : ((1u << cut) - 1u)) & from;
-                unsigned pend = hit & R, took = 0;
-                while (pend) {
-                    const int wv = __shfl_sync(FULL, w, __ffs(pend) - 1);
-                    const unsigned mm = __ballot_sync(FULL, w == wv) & R;
-                    pend &= ~mm;
-                    if (lane == wv) took = apply_way(mm, Sm, UPm, U1m, base);
-                }
-                if (PRIO && CLASS) {
-                    const unsigned pf = __reduce_or_sync(FULL, took);
-                    if ((R & Sm) >> lane & 1u) write_class(a, base + lane, (pf >> lane & 1u) ? 1 : 0);
-                }
-                if (cut >= 32) break;
-                const uint32_t gc = __shfl_sync(FULL, g, cut);
-                const bool isS = (Sm >> cut) & 1u;
-                if (PRIO) {
-                    if (isS) {
-                        od++;
-                        if (CLASS && lane == 0) write_class(a, base + cut, 2);
-                    } else {
-                        ins++;
-                    }
-                } else {
+                if (isS) {
                     od++;
-                    if (a.per_access_hit && lane == 0)
-                        a.per_access_hit[a.vals ? a.vals[base + cut] : base + cut] = 0;
-                }
-                int target;
-                const bool full = count >= W;
-                if (full && key32) {
-                    unsigned key;
-                    if (PRIO) {
-                        const int32_t pe = pr - decay;
-                        key = tag >= 0 ? ((unsigned)(pe > 0 ? pe : 0) << gb) | (unsigned)tag : ~0u;
-                    } else {
-                        key = tag >= 0 ? (unsigned)(clk - kbase) : ~0u;
-                    }
-                    const unsigned kmin = __reduce_min_sync(FULL, key);
-                    target = __ffs(__ballot_sync(FULL, key == kmin)) - 1;
-                } else if (full) {
-                    unsigned khi, klo;
-                    if (PRIO) {
-                        const int32_t pe = pr - decay;
-                        khi = tag >= 0 ? (unsigned)(pe > 0 ? pe : 0) : ~0u;
-                        klo = (unsigned)tag;
-                    } else {
-                        khi = tag >= 0 ? (unsigned)((uint64_t)clk >> 32) : ~0u;
-                        klo = (unsigned)clk;
-                    }
-                    const unsigned hmin = __reduce_min_sync(FULL, khi);
-                    const unsigned lmin = __reduce_min_sync(FULL, khi == hmin ? klo : ~0u);
-                    target = __ffs(__ballot_sync(FULL, khi == hmin && klo == lmin)) - 1;
+                    if (CLASS && lane == 0) write_class(a, at_m, 2);
                 } else {
-                    target = __ffs(__ballot_sync(FULL, tag == -1)) - 1;
+                    ins++;
                 }
-                const int32_t evicted = __shfl_sync(FULL, tag, target);   // -1: a free way
-                if (full) {
-                    if (PRIO) decay++;
-                    nev++;
-                    count--;
-                }
-                if (lane == target) {
-                    tag = (int32_t)gc;
-                    if (PRIO) {
-                        pr = a.es + decay;
-                        mhi = isS ? 0u : 1u;
-                    } else {
-                        clk = clock_base + base + cut;
-                    }
-                }
-                if (lane == 0) {
-                    if (evicted >= 0) wmap[div_set((uint32_t)evicted, S, M)] = (uint8_t)kNone;
-                    wmap[div_set(gc, S, M)] = (uint8_t)target;
-                }
-                __syncwarp();
-                if (w == target) w = kNone;        // the evicted gid's events now miss
-                if (real && g == gc) w = target;   // the inserted gid's events hit
-                count++;
-                hit = __ballot_sync(FULL, w != kNone);
-                start = cut + 1;
+            } else {
+                od++;
+                if (a.per_access_hit && lane == 0)
+                    a.per_access_hit[a.vals ? a.vals[at_m] : at_m] = 0;
             }
+            int target;
+            const bool full = count >= W;
+            if (full && key32) {
+                unsigned key;
+                if (PRIO) {
+                    const int32_t pe = pr - decay;
+                    key = tag >= 0 ? ((unsigned)(pe > 0 ? pe : 0) << gb) | (unsigned)tag : ~0u;
+                } else {
+                    key = tag >= 0 ? (unsigned)(clk - kbase) : ~0u;
+                }
+                const unsigned kmin = __reduce_min_sync(FULL, key);
+                target = __ffs(__ballot_sync(FULL, key == kmin)) - 1;
+            } else if (full) {
+                unsigned khi, klo;
+                if (PRIO) {
+                    const int32_t pe = pr - decay;
+                    khi = tag >= 0 ? (unsigned)(pe > 0 ? pe : 0) : ~0u;
+                    klo = (unsigned)tag;
+                } else {
+                    khi = tag >= 0 ? (unsigned)((uint64_t)clk >> 32) : ~0u;
+                    klo = (unsigned)clk;
+                }
+                const unsigned hmin = __reduce_min_sync(FULL, khi);
+                const unsigned lmin = __reduce_min_sync(FULL, khi == hmin ? klo : ~0u);
+                target = __ffs(__ballot_sync(FULL, khi == hmin && klo == lmin)) - 1;
+            } else {
+                target = __ffs(__ballot_sync(FULL, tag == -1)) - 1;
+            }
+            const int32_t evicted = __shfl_sync(FULL, tag, target);   // -1: a free way
+            if (full) {
+                if (PRIO) decay++;
+                nev++;
+                count--;
+            }
+            if (lane == target) {
+                tag = (int32_t)gc;
+                if (PRIO) {
+                    pr = a.es + decay;
+                    mhi = isS ? 0u : 1u;
+                } else {
+                    clk = clock_base + at_m;
+                }
+            }
+            if (lane == 0) {
+                if (evicted >= 0) wmap[div_set((uint32_t)evicted, S, M)] = (uint8_t)kNone;
+                wmap[div_set(gc, S, M)] = (uint8_t)target;
+            }
+            count++;
+#pragma unroll
+            for (int q = 0; q < kWide; q++) {
+                if (wq[q] == target) wq[q] = kNone;        // the evicted gid's events now miss
+                if (gw[q] == gc) wq[q] = target;           // the inserted gid's events hit
+                Hq[q] = __ballot_sync(FULL, wq[q] != kNone);
+            }
+            __syncwarp();
+            start = m + 1;
         }
     }
 
