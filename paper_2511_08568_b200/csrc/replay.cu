@@ -851,8 +851,7 @@ __device__ __forceinline__ uint32_t div_set(uint32_t g, uint32_t S, uint32_t M) 
 template <int POLICY, bool CLASS>
 __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs &a, int64_t set,
                                                                int64_t lo, int64_t hi,
-                                                               EventRing &ring, uint8_t *wmap,
-                                                               int lane) {
+                                                               uint8_t *wmap, int lane) {
     constexpr bool PRIO = (POLICY == RECMG_POLICY_PRIORITY);
     constexpr int kNone = 0xFF;
     const unsigned FULL = 0xFFFFFFFFu;
@@ -934,7 +933,6 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
         const int64_t pos = lo + wp;
         int wq[kWide];
         unsigned Sq[kWide], UPq[kWide], U1q[kWide], Hq[kWide], Cq[kWide];
-        unsigned missing = 0;
 #pragma unroll
         for (int q = 0; q < kWide; q++) {
             const uint32_t g = ev_gid(cur[q]), ty = ev_type(cur[q]);
@@ -948,7 +946,6 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
             Hq[q] = __ballot_sync(FULL, wq[q] != kNone);
             Cq[q] = PRIO ? (Sq[q] | __ballot_sync(FULL, real && ty == EV_PREFETCH))
                          : __ballot_sync(FULL, real);
-            missing |= Cq[q] & ~Hq[q];
         }
         // The window as hit runs and misses: the run before the first miss is
         // applied per distinct way it touches (a ballot per way: a handful;
@@ -956,7 +953,6 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
         // last hit sets the clock]), the miss is resolved, the window's way
         // numbers are patched for the two gids it changed, and the next run
         // starts after it.  A window without a miss is one run.
-        (void)missing;
         uint32_t gw[kWide];
 #pragma unroll
         for (int q = 0; q < kWide; q++) gw[q] = ev_gid(cur[q]);
@@ -1187,7 +1183,7 @@ __device__ __forceinline__ void replay_one_set(const ReplayArgs &a, int64_t set,
         if (W <= 32 && (!heavy_item || regs < 0) && hi - lo < (int64_t)(regs < 0 ? 0x7FFFFFFF : regs)) {
             if (a.qn > 0 && hi - lo >= kTableMinEvents && tables) {
                 const unsigned long long m = replay_set_table<POLICY, CLASS>(
-                    a, set, lo, hi, ring, base + kRingSlots * kRingBlk * 4, lane);
+                    a, set, lo, hi, base + kRingSlots * kRingBlk * 4, lane);
                 note_time(2, m);
                 return;
             }
