@@ -911,7 +911,10 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
     // event 32 q + j), loaded one window ahead straight from the partitioned
     // segment (coalesced; L2 prefetch 8 windows ahead); past the segment end
     // the slots hold kGidMask, an event that is no event
-    constexpr int kWide = 4, kWin = 32 * kWide;
+#ifndef RECMG_TABLE_WIDE
+#define RECMG_TABLE_WIDE 4
+#endif
+    constexpr int kWide = RECMG_TABLE_WIDE, kWin = 32 * kWide;
     const uint32_t *seg = a.ev + lo;
     const int64_t len = hi - lo;
     uint32_t nxt[kWide];
@@ -991,7 +994,10 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
                     if (lane == wv) mine[q] = b & Rq[q];
                 }
             }
-            if (mine[0] | mine[1] | mine[2] | mine[3]) {
+            unsigned any_mine = 0;
+#pragma unroll
+            for (int q = 0; q < kWide; q++) any_mine |= mine[q];
+            if (any_mine) {
                 if (PRIO) {
                     unsigned nS = 0, u1 = 0;
                     int fS = -1, lU = -1;
@@ -1034,9 +1040,12 @@ __device__ __forceinline__ unsigned long long replay_set_table(const ReplayArgs 
             if (m >= kWin) break;
             // the miss at window position m
             const int qm = m >> 5, lm = m & 31;
-            const uint32_t gsel = qm == 0 ? gw[0] : (qm == 1 ? gw[1] : (qm == 2 ? gw[2] : gw[3]));
+            uint32_t gsel = gw[0];
+            unsigned Ssel = Sq[0];
+#pragma unroll
+            for (int q = 1; q < kWide; q++)
+                if (qm == q) { gsel = gw[q]; Ssel = Sq[q]; }
             const uint32_t gc = __shfl_sync(FULL, gsel, lm);
-            const unsigned Ssel = qm == 0 ? Sq[0] : (qm == 1 ? Sq[1] : (qm == 2 ? Sq[2] : Sq[3]));
             const bool isS = (Ssel >> lm) & 1u;
             const int64_t at_m = pos + m;
             if (PRIO) {
